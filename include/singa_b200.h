@@ -1,0 +1,332 @@
+/*
+ * singa_b200.h — C ABI of the B200-native SINGA TrainOneBatch path.
+ *
+ * The calls follow the paper's own abstractions (arXiv 1603.07846, PAPER.md):
+ *   NeuralNet / Layer ComputeFeature, ComputeGradient ........ §4.1.1-4.1.2
+ *   BPTrainOneBatch (Collect, ComputeFeature; ComputeGradient, Update)  Alg. 1
+ *   Updater (server-side parameter update protocol) .......... §4.1.4
+ *   Cluster topology: 1 worker group x K workers, 1 server group x K co-located
+ *     servers = the AllReduce framework ...................... §5.1-5.2.1
+ *   partition_dim 0 (batch, data parallel) / 1 (feature, model parallel) per
+ *     layer, connection layers inserted automatically ........ §5.3
+ *
+ * Conventions (all functions):
+ *   - Every function returns sg_status: SG_OK (0) or a negative error code; no
+ *     C++ exception crosses the boundary.  sg_last_error() returns a
+ *     thread-local message naming the layer and shapes involved.
+ *   - "dev" pointers are CUDA device pointers on the calling rank's device;
+ *     "host" pointers are host memory (pageable or pinned).
+ *   - stream arguments are cudaStream_t passed as void*; NULL = legacy stream.
+ *     Device work is stream-ordered and asynchronous: the return code covers
+ *     validation and launch errors; device-side conditions (bad label,
+ *     non-finite loss) surface at sg_net_sync().
+ *   - Calls marked COLLECTIVE must be made by every rank, in the same order.
+ *   - Layouts: images NHWC fp32; conv weights [Cout][R][S][Cin]; inner-product
+ *     weights [d_v][d_h] (y = xW + b); biases [n]; labels int32.
+ *   - Ownership: the caller owns every buffer it passes and the streams; the
+ *     library owns everything it allocates (params, blobs, workspaces, the NCCL
+ *     communicator) and frees it in the matching *_destroy.
+ *   - A handle is used by one host thread at a time.
+ */
+#ifndef SINGA_B200_H
+#define SINGA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_ABI_VERSION 1
+#define SG_API __attribute__((visibility("default")))
+
+typedef int32_t sg_status;
+enum {
+  SG_OK = 0,
+  SG_ERR_INVALID_ARG = -1, /* null handle/pointer, bad enum value, index out of range */
+  SG_ERR_DIMENSION = -2,   /* shape mismatch (e.g. conv Cin not a multiple of 4 at the op level) */
+  SG_ERR_PARTITION = -3,   /* parts > extent; b % K != 0 for a dim-0 loss; K does not divide a dim-1 width */
+  SG_ERR_CONFIG = -4,      /* unknown kind, bad hyper-parameter, loss not last, dim-1 conv/pool/LRN */
+  SG_ERR_SEQUENCE = -5,    /* ComputeGradient before ComputeFeature, no input set */
+  SG_ERR_PROTOCOL = -6,    /* Update before ComputeGradient of that layer in this step */
+  SG_ERR_DIVERGED = -7,    /* non-finite loss (reported by sg_net_sync) */
+  SG_ERR_LABEL = -8,       /* label outside [0, num_classes) (reported by sg_net_sync) */
+  SG_ERR_CUDA = -9,
+  SG_ERR_NCCL = -10,
+  SG_ERR_OOM = -11,
+  SG_ERR_UNSUPPORTED = -12 /* >1 worker/server group (asynchronous frameworks), servers != workers */
+};
+
+SG_API const char* sg_last_error(void);
+SG_API int32_t sg_abi_version(void);
+
+/* ======================================================================
+ * Partition map (host only; P:479-484 slice by row / by column).
+ * Remainder-first: len_i = floor(E/K) + [i < E mod K], off_i = sum_{j<i} len_j
+ * (reading A12).  SG_ERR_PARTITION if parts > extent,
+ * SG_ERR_INVALID_ARG if parts < 1, idx outside [0, parts) or a null output.
+ * ====================================================================== */
+SG_API sg_status sg_partition_range(int64_t extent, int32_t parts, int32_t idx, int64_t* off, int64_t* len);
+
+/* ======================================================================
+ * Layer-isolated operations (ComputeFeature / ComputeGradient of one layer on
+ * caller buffers).  Device pointers, stream-ordered; scratch space for
+ * split-K partials is owned by the library (per device, grown on demand:
+ * these calls are NOT CUDA-graph capturable, the net path is).
+ * ====================================================================== */
+
+/* Plain TF32 tensor-core GEMM (test entry of the implicit-GEMM engine):
+ * C[M][N] = op(A) op(B); A is [M][K] (ta=0) or [K][M] (ta=1); B is [K][N]
+ * (tb=0) or [N][K] (tb=1); all row-major fp32, fp32 accumulate. */
+SG_API sg_status sg_op_gemm(const float* A_dev, int32_t ta, const float* B_dev, int32_t tb, float* C_dev, int32_t M,
+                            int32_t N, int32_t K, void* stream);
+
+/* Convolution (reading A4: cross-correlation, zero padding,
+ * Ho = floor((H + 2p - R)/s) + 1).  x [N][H][W][C] with C % 4 == 0
+ * (SG_ERR_DIMENSION otherwise), W [Co][R][S][C], b [Co], y [N][Ho][Wo][Co]. */
+typedef struct {
+  int32_t N, H, W, C, Co, R, S, stride, pad;
+} sg_conv_desc;
+SG_API sg_status sg_conv_out_shape(const sg_conv_desc* d, int32_t* Ho, int32_t* Wo);
+SG_API sg_status sg_op_conv_forward(const sg_conv_desc* d, const float* x_dev, const float* W_dev, const float* b_dev,
+                                    float* y_dev, void* stream);
+/* dW = sum dy (x) x-window, db = sum dy, dx (skipped when dx_dev == NULL). */
+SG_API sg_status sg_op_conv_backward(const sg_conv_desc* d, const float* x_dev, const float* W_dev,
+                                     const float* dy_dev, float* dx_dev, float* dW_dev, float* db_dev, void* stream);
+
+/* Inner product ("rotates (multiply W), shifts (plus b)"):
+ * y[rows][dh] = x[rows][dv] W[dv][dh] + b ; dW = x^T dy ; db = colsum dy ;
+ * dx = dy W^T (skipped when dx_dev == NULL). */
+SG_API sg_status sg_op_ip_forward(const float* x_dev, const float* W_dev, const float* b_dev, float* y_dev,
+                                  int32_t rows, int32_t dv, int32_t dh, void* stream);
+SG_API sg_status sg_op_ip_backward(const float* x_dev, const float* W_dev, const float* dy_dev, float* dx_dev,
+                                   float* dW_dev, float* db_dev, int32_t rows, int32_t dv, int32_t dh, void* stream);
+
+/* Pooling (P:553, P:658-659 Caffe pooling; reading A5: ceil-mode output
+ * size, avg divisor = window size before clipping, max = first maximum in
+ * row-major window scan).  mode 0 = max, 1 = avg.  mask_dev (max only) receives
+ * the uint8 offset (dh*kernel + dw) of the argmax inside its window, consumed by
+ * the backward; sg_op_pool_argmax expands it to int32 flat h*W + w. */
+typedef struct {
+  int32_t N, H, W, C, kernel, stride, pad, mode;
+} sg_pool_desc;
+SG_API sg_status sg_pool_out_shape(const sg_pool_desc* d, int32_t* Ho, int32_t* Wo);
+SG_API sg_status sg_op_pool_forward(const sg_pool_desc* d, const float* x_dev, float* y_dev, uint8_t* mask_dev,
+                                    void* stream);
+SG_API sg_status sg_op_pool_backward(const sg_pool_desc* d, const float* dy_dev, const uint8_t* mask_dev,
+                                     float* dx_dev, void* stream);
+SG_API sg_status sg_op_pool_argmax(const sg_pool_desc* d, const uint8_t* mask_dev, int32_t* argmax_dev, void* stream);
+
+/* LRN across channels (reading A6): scale = k + alpha/n sum_{window} x^2,
+ * y = x scale^-beta.  x, y, scale: [pixels][C]. */
+typedef struct {
+  int64_t pixels;
+  int32_t C, size;
+  float alpha, beta, k;
+} sg_lrn_desc;
+SG_API sg_status sg_op_lrn_forward(const sg_lrn_desc* d, const float* x_dev, float* y_dev, float* scale_dev,
+                                   void* stream);
+SG_API sg_status sg_op_lrn_backward(const sg_lrn_desc* d, const float* x_dev, const float* y_dev,
+                                    const float* scale_dev, const float* dy_dev, float* dx_dev, void* stream);
+
+/* Elementwise neurons: kind SG_RELU or SG_SIGMOID (see sg_kind). ReLU'(0) = 0. */
+SG_API sg_status sg_op_neuron_forward(int32_t kind, const float* x_dev, float* y_dev, int64_t n, void* stream);
+SG_API sg_status sg_op_neuron_backward(int32_t kind, const float* y_dev, const float* dy_dev, float* dx_dev,
+                                       int64_t n, void* stream);
+
+/* Softmax cross-entropy (readings A2, A7):
+ * row_loss[i] = LSE(z_i) - z_{i,y_i}; dz = (softmax(z) - onehot(y)) / n_loc.
+ * err_dev (int32, may be NULL) is set to nonzero for a label outside [0, C). */
+SG_API sg_status sg_op_softmax_ce(const float* z_dev, const int32_t* labels_dev, int32_t rows, int32_t C,
+                                  int32_t n_loc, float* row_loss_dev, float* dz_dev, int32_t* err_dev, void* stream);
+/* Euclidean loss: row_loss[i] = 0.5 ||u_i - v_i||^2, du = (u - v) / n_loc. */
+SG_API sg_status sg_op_euclidean(const float* u_dev, const float* v_dev, int32_t rows, int32_t d, int32_t n_loc,
+                                 float* row_loss_dev, float* du_dev, void* stream);
+
+/* Updater (P:282-284 + north star; reading A1):
+ * g' = s g + wd w ; v = mu v - lr g' ; w = w + v   (fp32, fixed FMA order). */
+SG_API sg_status sg_op_sgd_momentum(float* w_dev, const float* g_dev, float* v_dev, int64_t n, float lr, float mu,
+                                    float wd, float s, void* stream);
+
+/* ======================================================================
+ * Cluster topology (AllReduce framework P:419-422).
+ * ====================================================================== */
+typedef struct sg_cluster sg_cluster;
+typedef struct {
+  int32_t rank, world_size, device;
+  int32_t nworker_groups, workers_per_group; /* must be 1, world_size */
+  int32_t nserver_groups, servers_per_group; /* must be 1, world_size (servers co-located) */
+  uint8_t nccl_id[128];                      /* from sg_get_unique_id on rank 0, broadcast by the caller */
+} sg_cluster_cfg;
+/* rank 0 only; the caller broadcasts the 128 bytes to all ranks (process boundary). */
+SG_API sg_status sg_get_unique_id(uint8_t out[128]);
+/* COLLECTIVE. Sets the CUDA device, creates the NCCL communicator (skipped at world_size 1).
+ * Asynchronous topologies (several worker / server groups) -> SG_ERR_UNSUPPORTED. */
+SG_API sg_status sg_cluster_create(const sg_cluster_cfg* cfg, sg_cluster** out);
+SG_API sg_status sg_cluster_framework(const sg_cluster* c, const char** name); /* "AllReduce" */
+SG_API sg_status sg_cluster_destroy(sg_cluster* c);
+
+/* ======================================================================
+ * NeuralNet configuration (layers record their source layers; here
+ * a single-path chain, the source of layer i is layer i-1 and of layer 0 the
+ * input; P:479-493 partition_dim per layer).
+ * ====================================================================== */
+typedef enum {
+  SG_CONV = 1,
+  SG_POOL_MAX = 2,
+  SG_POOL_AVG = 3,
+  SG_RELU = 4,
+  SG_SIGMOID = 5,
+  SG_LRN = 6,
+  SG_INNER_PRODUCT = 7,
+  SG_SOFTMAX_CE = 8,
+  SG_EUCLIDEAN = 9,
+  /* connection layers, inserted by the planner only (Table II) */
+  SG_INPUT = 20,
+  SG_CONCAT = 21, /* all-gather: rows (dim0 -> dim1) or features (dim1 -> dim1 IP) */
+  SG_SLICE = 22   /* all-to-all: feature-split rows -> row-split rows (dim1 -> dim0 loss) */
+} sg_kind;
+
+typedef struct {
+  const char* name;
+  int32_t kind;           /* sg_kind, user kinds only */
+  int32_t partition_dim;  /* -1 inherit from source, 0 batch, 1 feature */
+  int32_t num_output;     /* conv Cout / inner-product d_h */
+  int32_t kernel, stride, pad;
+  int32_t lrn_size;
+  float lrn_alpha, lrn_beta, lrn_k;
+  float lr_scale, wd_scale; /* per-Param multipliers (0 -> 1) */
+} sg_layer_cfg;
+
+typedef struct {
+  int32_t nlayers;
+  const sg_layer_cfg* layers;
+  int32_t batch;               /* global mini-batch b, "summed over all workers" */
+  int32_t in_c, in_h, in_w;    /* image input; in_h = in_w = 0 for a vector of in_c features */
+  int32_t num_classes;         /* softmax classes (0 for a Euclidean net) */
+} sg_net_cfg;
+
+/* ---- Host-only planning (no device needed): partitioning, connection-layer
+ * insertion, shape inference, Param table, server shard map.  Every map is
+ * compared bit-exactly with the oracle's. ---- */
+typedef struct sg_plan sg_plan;
+SG_API sg_status sg_plan_create(const sg_net_cfg* cfg, int32_t rank, int32_t world, sg_plan** out);
+SG_API sg_status sg_plan_destroy(sg_plan* p);
+
+typedef struct {
+  char name[64];
+  int32_t kind, partition_dim, is_connection, src;
+  /* global and local (this rank's) blob shapes: {rows, h, w, c} or {rows, features, 1, 1};
+   * local_offset = where the local block starts in the global blob. */
+  int64_t global_shape[4], local_shape[4], local_offset[4];
+} sg_layer_info;
+SG_API sg_status sg_plan_num_layers(const sg_plan* p, int32_t* n);
+SG_API sg_status sg_plan_layer_info(const sg_plan* p, int32_t i, sg_layer_info* out); /* execution order */
+
+typedef struct {
+  char name[64];           /* "<layer>/W" or "<layer>/b" */
+  int32_t layer;           /* index into the layer list (execution order) */
+  int32_t split_dim;       /* -1: replicated (dim-0 layer, server-sharded); 1: columns split (dim-1 layer) */
+  int64_t rows, cols;      /* global, user layout: conv W rows=Cout cols=R*S*Cin ; IP W rows=d_v cols=d_h ; bias rows=1 */
+  int64_t local_col_off, local_cols;
+  int32_t bucket;          /* gradient bucket (dim-0 layer) or -1 */
+  int64_t bucket_off;      /* element offset of this Param in its bucket */
+} sg_param_info;
+SG_API sg_status sg_plan_num_params(const sg_plan* p, int32_t* n);
+SG_API sg_status sg_plan_param_info(const sg_plan* p, int32_t i, sg_param_info* out);
+
+/* Server shard map (reading A13): per dim-0 layer a bucket
+ * concat(W, b) zero-padded to E' = ceil(E / 32K) * 32K; rank k owns
+ * [k E'/K, (k+1) E'/K).  One entry per (param, owner) slice. */
+typedef struct {
+  int32_t param, bucket, owner_rank;
+  int64_t param_off, bucket_off, len;
+} sg_shard_range;
+SG_API sg_status sg_plan_num_buckets(const sg_plan* p, int32_t* n, int64_t* padded_sizes /* cap n or NULL */);
+SG_API sg_status sg_plan_shard_map(const sg_plan* p, sg_shard_range* out, int32_t cap, int32_t* n);
+
+/* ---- The net on the device ---- */
+typedef struct sg_net sg_net;
+/* COLLECTIVE (world > 1).  Plans (as sg_plan_create with the cluster's rank /
+ * world), allocates every blob / Param / workspace on the cluster's device,
+ * initialises Params to 0 (set them with sg_param_set_value). */
+SG_API sg_status sg_net_create(sg_cluster* c, const sg_net_cfg* cfg, sg_net** out);
+SG_API sg_status sg_net_destroy(sg_net* n);
+SG_API sg_status sg_net_plan(const sg_net* n, const sg_plan** out); /* borrowed, valid until destroy */
+
+/* Param values in GLOBAL user layout on the host.  set: every rank passes the
+ * full value, the rank keeps its part (synchronous).  get: COLLECTIVE for
+ * world > 1, returns the full value.  get_grad: COLLECTIVE, the aggregated
+ * (sum over workers, unscaled) gradient of the last step. */
+SG_API sg_status sg_param_set_value(sg_net* n, int32_t p, const float* global_host);
+SG_API sg_status sg_param_get_value(sg_net* n, int32_t p, float* global_host);
+SG_API sg_status sg_param_get_grad(sg_net* n, int32_t p, float* global_host);
+SG_API sg_status sg_param_get_history(sg_net* n, int32_t p, float* global_host); /* momentum v, COLLECTIVE */
+
+/* ---- Updater ---- */
+typedef struct sg_updater sg_updater;
+typedef struct {
+  float base_lr, momentum, weight_decay;
+  float grad_scale;   /* <= 0: library default s = n_loc / b (1/K for a dim-0 loss, 1 for a dim-1 loss) */
+  int32_t lr_policy;  /* 0 fixed, 1 step: lr = base_lr * gamma^floor(step / step_size) */
+  float gamma;
+  int32_t step_size;
+} sg_updater_cfg;
+SG_API sg_status sg_updater_create(sg_net* n, const sg_updater_cfg* cfg, sg_updater** out);
+SG_API sg_status sg_updater_destroy(sg_updater* u);
+
+/* ---- BPTrainOneBatch (Alg. 1) ----
+ * x_dev: this rank's input rows (rows = local_shape[0] of the input layer:
+ * b/K for a dim-0 first layer, b for a dim-1 first layer), NHWC with the
+ * configured in_c channels (3 for images) or [rows][in_c].  labels_dev: this
+ * rank's labels for the loss layer's rows (b/K for a dim-0 softmax loss);
+ * NULL for a Euclidean net.  loss_dev: device float, receives the global mean
+ * loss L = (1/b) sum_i l_i.  COLLECTIVE for world > 1. */
+SG_API sg_status sg_train_one_batch(sg_net* n, sg_updater* u, int64_t step, const float* x_dev,
+                                    const int32_t* labels_dev, float* loss_dev, void* stream);
+/* End-to-end variant from HOST buffers: copies the inputs host->device, runs the
+ * step, copies the loss back and synchronises the stream (so *loss_host is valid
+ * on return).  Use pinned buffers for asynchronous copies. COLLECTIVE. */
+SG_API sg_status sg_train_one_batch_host(sg_net* n, sg_updater* u, int64_t step, const float* x_host,
+                                         const int32_t* labels_host, float* loss_host, void* stream);
+
+/* Alg. 1 driven layer by layer (same work as sg_train_one_batch):
+ *   sg_net_set_input; for i: sg_net_collect(i), sg_layer_compute_feature(i);
+ *   for i reversed: sg_layer_compute_gradient(i), sg_net_update(i). */
+SG_API sg_status sg_net_set_input(sg_net* n, const float* x_dev, const int32_t* labels_dev, void* stream);
+SG_API sg_status sg_net_collect(sg_net* n, int32_t layer, void* stream);
+SG_API sg_status sg_layer_compute_feature(sg_net* n, int32_t layer, void* stream);
+SG_API sg_status sg_layer_compute_gradient(sg_net* n, int32_t layer, void* stream);
+SG_API sg_status sg_net_update(sg_net* n, sg_updater* u, int32_t layer, int64_t step, void* stream);
+SG_API sg_status sg_net_loss(sg_net* n, float* loss_dev, void* stream);
+/* Drain all streams; returns SG_ERR_LABEL / SG_ERR_DIVERGED raised by device kernels since the last sync. */
+SG_API sg_status sg_net_sync(sg_net* n);
+/* Capture the whole sg_train_one_batch step in a CUDA graph (NCCL included) and replay it. */
+SG_API sg_status sg_net_enable_graph(sg_net* n, int32_t enable);
+/* Kernel launches issued by the last sg_train_one_batch (graph replay counts the captured kernels). */
+SG_API sg_status sg_net_last_launch_count(const sg_net* n, int64_t* launches);
+
+/* ---- Blob access for layer-isolated parity (this rank's local blob) ----
+ * which: 0 data (layer output), 1 grad (gradient w.r.t. the layer's SOURCE
+ * data, i.e. the layer's dx), 2 argmax (max pool, int32 flat h*W + w).
+ * Layout: as sg_layer_info.local_shape; the internal input blob of an image
+ * net has channels padded to a multiple of 4 (pad channel = 0). */
+SG_API sg_status sg_blob_size(sg_net* n, int32_t layer, int32_t which, size_t* bytes);
+SG_API sg_status sg_blob_get(sg_net* n, int32_t layer, int32_t which, void* dst_dev, size_t bytes, void* stream);
+SG_API sg_status sg_blob_set(sg_net* n, int32_t layer, int32_t which, const void* src_dev, size_t bytes,
+                             void* stream);
+
+/* ======================================================================
+ * Server-group synchronisation of one flat Param (C5 sweep):
+ * reduce-scatter(sum) grad_full -> Updater on this rank's shard of w_full
+ * (with v_shard) -> all-gather w_full.  n must be a multiple of 32 * world.
+ * grad_full is overwritten.  COLLECTIVE.
+ * ====================================================================== */
+SG_API sg_status sg_server_sync(sg_cluster* c, const sg_updater_cfg* cfg, int64_t step, float* grad_full_dev,
+                                float* w_full_dev, float* v_shard_dev, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SINGA_B200_H */

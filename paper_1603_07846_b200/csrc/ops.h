@@ -1,0 +1,108 @@
+// Internal kernel launchers (host side).  Every function enqueues work on
+// `st` and returns cudaError_t from the launch; shapes are validated by the
+// callers (runtime / ABI layer).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sg {
+
+// Scratch for deterministic split-K partials (owned by the caller).
+struct Workspace {
+  float* ptr = nullptr;
+  size_t floats = 0;
+};
+
+// Blocked row-major 2-D view description for FC operands / outputs:
+// element (i, j) at p[(j / cb) * bs + i * ld + j % cb]; cb = cols for a plain matrix.
+struct View2D {
+  float* p;
+  long long ld, bs;
+  int cb, rows, cols;
+};
+inline View2D plain(float* p, int rows, int cols, long long ld = -1) {
+  return View2D{p, ld < 0 ? cols : ld, 0, cols, rows, cols};
+}
+
+struct ConvShape {
+  int N, H, W, C;  // C multiple of 4 (padded)
+  int Co, R, S, st, pad;
+  int Ho, Wo;
+};
+
+// Number of floats of split-K workspace a GEMM of this shape may use.
+size_t gemm_ws_floats(int M, int N, int K);
+
+// ---- convolution (implicit GEMM, tcgen05 kind::tf32) ----
+cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const float* b, float* y, int relu,
+                     Workspace ws, cudaStream_t st);
+cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* W, float* dx, Workspace ws,
+                       cudaStream_t st);
+// dW [Co][R][S][C]; db [Co] (db may be null)
+cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dW, float* db, Workspace ws,
+                       cudaStream_t st);
+
+// ---- inner product:  y = x W + b ; W [d_v][d_h] ----
+cudaError_t ip_fwd(View2D x, const float* W, int dv, int dh, const float* b, View2D y, int relu, Workspace ws,
+                   cudaStream_t st);
+cudaError_t ip_dgrad(View2D dy, const float* W, int dv, int dh, View2D dx, Workspace ws, cudaStream_t st);
+cudaError_t ip_wgrad(View2D x, View2D dy, int dv, int dh, float* dW, float* db, Workspace ws, cudaStream_t st);
+
+// Generic TF32 GEMM on plain row-major matrices (test entry):
+// C[M][N] = op(A) op(B) with A [M][K] (ta=0) or [K][M] (ta=1), B [K][N] (tb=0) or [N][K] (tb=1).
+cudaError_t gemm_plain(const float* A, int ta, const float* B, int tb, float* C, int M, int N, int K, Workspace ws,
+                       cudaStream_t st);
+
+// ---- column sums (bias gradient): out[n] = sum_m X[m][n] ----
+cudaError_t colsum(const float* X, int M, int N, long long ld, float* out, Workspace ws, cudaStream_t st);
+
+// ---- elementwise / pooling / LRN / loss ----
+cudaError_t relu_fwd(const float* x, float* y, long long n, cudaStream_t st);
+cudaError_t relu_bwd(const float* y, const float* dy, float* dx, long long n, cudaStream_t st);
+cudaError_t sigmoid_fwd(const float* x, float* y, long long n, cudaStream_t st);
+cudaError_t sigmoid_bwd(const float* y, const float* dy, float* dx, long long n, cudaStream_t st);
+// 2-D variants for column-sliced FC features (rows x cols with leading dim ld)
+cudaError_t relu_fwd2d(const float* x, float* y, int rows, int cols, long long ld, cudaStream_t st);
+
+struct PoolShape {
+  int N, H, W, C, k, s, p, Ho, Wo;
+};
+cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* arg, cudaStream_t st);
+cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg, float* dx, cudaStream_t st);
+cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st);
+cudaError_t avgpool_bwd(const PoolShape& s, const float* dy, float* dx, cudaStream_t st);
+// argmax window offset -> int32 flat h*W+w in the input plane (ABI export format)
+cudaError_t pool_argmax_expand(const PoolShape& s, const uint8_t* arg, int32_t* out, cudaStream_t st);
+
+struct LrnShape {
+  long long pixels;
+  int C, n;
+  float alpha, beta, k;
+};
+cudaError_t lrn_fwd(const LrnShape& s, const float* x, float* y, float* scale, cudaStream_t st);
+cudaError_t lrn_bwd(const LrnShape& s, const float* x, const float* y, const float* scale, const float* dy, float* dx,
+                    cudaStream_t st);
+
+// Softmax cross-entropy over rows of a (blocked) logits view; per-row loss and
+// dz = (softmax - onehot) / n_loc written with the same blocking. Labels out of
+// [0, C) set *err = 1.
+cudaError_t softmax_ce(View2D z, const int32_t* labels, float* row_loss, View2D dz, float inv_nloc, int* err,
+                       cudaStream_t st);
+// Euclidean: per-row 0.5 ||u - v||^2 and du = (u - v) / n_loc.
+cudaError_t euclidean(View2D u, View2D v, float* row_loss, View2D du, float inv_nloc, cudaStream_t st);
+// out[0] = scale * sum(v[0..n)) (fixed-order, single block); also flags non-finite in *err (bit 2)
+cudaError_t sum_scaled(const float* v, int n, float scale, float* out, int* err, cudaStream_t st);
+
+// ---- Updater: g' = s g + wd w ; v = mu v - lr g' ; w += v ----
+cudaError_t sgd_momentum(float* w, const float* g, float* v, long long n, float lr, float mu, float wd, float s,
+                         cudaStream_t st);
+// Same with lr read from device memory (graph-capturable): lr = lr_dev[0] * lr_scale
+cudaError_t sgd_momentum_dev(float* w, const float* g, float* v, long long n, const float* lr_dev, float lr_scale,
+                             float mu, float wd, float s, cudaStream_t st);
+
+// ---- input layer: NHWC with C=3 (user layout) -> padded C=4 ----
+cudaError_t pad_channels(const float* x, float* y, long long pixels, int cin, int cout, cudaStream_t st);
+// copy rows x cols fp32 (strided) — used for feature-blocked gathers on the host side of tests
+cudaError_t copy2d(const float* src, long long sld, float* dst, long long dld, int rows, int cols, cudaStream_t st);
+
+}  // namespace sg

@@ -11,3 +11,13 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path through the C ABI)")
     config.addinivalue_line("markers", "slow: long-running oracle test")
+
+
+@pytest.fixture(autouse=True)
+def _release_device_buffers():
+    yield
+    try:
+        from tests import gpu_util
+        gpu_util.KEEP.clear()
+    except Exception:
+        pass

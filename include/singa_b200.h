@@ -220,6 +220,12 @@ typedef struct {
   /* global and local (this rank's) blob shapes: {rows, h, w, c} or {rows, features, 1, 1};
    * local_offset = where the local block starts in the global blob. */
   int64_t global_shape[4], local_shape[4], local_offset[4];
+  /* element stride between consecutive feature rows of the local blob (vector
+   * blobs are padded to a multiple of 4 floats; = h*w*c for images).  A
+   * feature-gathered (Concat dim 1) or all-to-all (Slice) blob is stored as K
+   * rank blocks [K][rows][ld]; nblocks = K then (else 1). */
+  int64_t ld;
+  int32_t nblocks;
 } sg_layer_info;
 SG_API sg_status sg_plan_num_layers(const sg_plan* p, int32_t* n);
 SG_API sg_status sg_plan_layer_info(const sg_plan* p, int32_t i, sg_layer_info* out); /* execution order */
@@ -231,7 +237,9 @@ typedef struct {
   int64_t rows, cols;      /* global, user layout: conv W rows=Cout cols=R*S*Cin ; IP W rows=d_v cols=d_h ; bias rows=1 */
   int64_t local_col_off, local_cols;
   int32_t bucket;          /* gradient bucket (dim-0 layer) or -1 */
-  int64_t bucket_off;      /* element offset of this Param in its bucket */
+  int64_t bucket_off;      /* element offset of this Param in its bucket (internal elements) */
+  int64_t internal_size;   /* elements of the local internal layout (first-conv channels padded
+                              to 4, inner-product output columns padded to a multiple of 4) */
 } sg_param_info;
 SG_API sg_status sg_plan_num_params(const sg_plan* p, int32_t* n);
 SG_API sg_status sg_plan_param_info(const sg_plan* p, int32_t i, sg_param_info* out);

@@ -64,13 +64,14 @@ class NetCfg(C.Structure):
 class LayerInfo(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("kind", C.c_int32), ("partition_dim", C.c_int32),
                 ("is_connection", C.c_int32), ("src", C.c_int32),
-                ("global_shape", C.c_int64 * 4), ("local_shape", C.c_int64 * 4), ("local_offset", C.c_int64 * 4)]
+                ("global_shape", C.c_int64 * 4), ("local_shape", C.c_int64 * 4), ("local_offset", C.c_int64 * 4),
+                ("ld", C.c_int64), ("nblocks", C.c_int32)]
 
 
 class ParamInfo(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("layer", C.c_int32), ("split_dim", C.c_int32),
                 ("rows", C.c_int64), ("cols", C.c_int64), ("local_col_off", C.c_int64), ("local_cols", C.c_int64),
-                ("bucket", C.c_int32), ("bucket_off", C.c_int64)]
+                ("bucket", C.c_int32), ("bucket_off", C.c_int64), ("internal_size", C.c_int64)]
 
 
 class ShardRange(C.Structure):

@@ -7,6 +7,13 @@
 
 namespace sg {
 
+// Number of kernels launched by this library (all launchers bump it).
+extern long long g_kernel_launches;
+inline cudaError_t launched() {
+  ++g_kernel_launches;
+  return cudaGetLastError();
+}
+
 // Scratch for deterministic split-K partials (owned by the caller).
 struct Workspace {
   float* ptr = nullptr;
@@ -105,4 +112,9 @@ cudaError_t pad_channels(const float* x, float* y, long long pixels, int cin, in
 // copy rows x cols fp32 (strided) — used for feature-blocked gathers on the host side of tests
 cudaError_t copy2d(const float* src, long long sld, float* dst, long long dld, int rows, int cols, cudaStream_t st);
 
+}  // namespace sg
+
+namespace sg {
+// p[0] = v (stream-ordered; used to feed per-step scalars to captured graphs)
+cudaError_t fill_scalar(float* p, float v, cudaStream_t st);
 }  // namespace sg

@@ -73,14 +73,14 @@ cudaError_t launch_map1(const float* x, float* y, long long n, F f, cudaStream_t
   if (n <= 0) return cudaSuccess;
   if (!aligned16(x) || !aligned16(y)) return cudaErrorMisalignedAddress;
   map1_kernel<<<blocks_for(n / 4 + 1, 256), 256, 0, st>>>(x, y, n, f);
-  return cudaGetLastError();
+  return launched();
 }
 template <class F>
 cudaError_t launch_map2(const float* a, const float* b, float* y, long long n, F f, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (!aligned16(a) || !aligned16(b) || !aligned16(y)) return cudaErrorMisalignedAddress;
   map2_kernel<<<blocks_for(n / 4 + 1, 256), 256, 0, st>>>(a, b, y, n, f);
-  return cudaGetLastError();
+  return launched();
 }
 
 // ---------------------------------------------------------------- pooling --
@@ -401,58 +401,58 @@ cudaError_t sigmoid_bwd(const float* y, const float* dy, float* dx, long long n,
 }
 cudaError_t relu_fwd2d(const float* x, float* y, int rows, int cols, long long ld, cudaStream_t st) {
   relu2d_kernel<<<blocks_for((long long)rows * cols, 256), 256, 0, st>>>(x, y, rows, cols, ld);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* arg, cudaStream_t st) {
   if (s.C % 4 || s.k * s.k > 256) return cudaErrorInvalidValue;
   maxpool_fwd_kernel<<<blocks_for((long long)s.N * s.Ho * s.Wo * s.C / 4, 256), 256, 0, st>>>(s, x, y, arg);
-  return cudaGetLastError();
+  return launched();
 }
 cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg, float* dx, cudaStream_t st) {
   if (s.C % 4) return cudaErrorInvalidValue;
   maxpool_bwd_kernel<<<blocks_for((long long)s.N * s.H * s.W * s.C / 4, 256), 256, 0, st>>>(s, dy, arg, dx);
-  return cudaGetLastError();
+  return launched();
 }
 cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st) {
   if (s.C % 4) return cudaErrorInvalidValue;
   avgpool_fwd_kernel<<<blocks_for((long long)s.N * s.Ho * s.Wo * s.C / 4, 256), 256, 0, st>>>(s, x, y);
-  return cudaGetLastError();
+  return launched();
 }
 cudaError_t avgpool_bwd(const PoolShape& s, const float* dy, float* dx, cudaStream_t st) {
   if (s.C % 4) return cudaErrorInvalidValue;
   avgpool_bwd_kernel<<<blocks_for((long long)s.N * s.H * s.W * s.C / 4, 256), 256, 0, st>>>(s, dy, dx);
-  return cudaGetLastError();
+  return launched();
 }
 cudaError_t pool_argmax_expand(const PoolShape& s, const uint8_t* arg, int32_t* out, cudaStream_t st) {
   argmax_expand_kernel<<<blocks_for((long long)s.N * s.Ho * s.Wo * s.C, 256), 256, 0, st>>>(s, arg, out);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t lrn_fwd(const LrnShape& s, const float* x, float* y, float* scale, cudaStream_t st) {
   lrn_fwd_kernel<<<blocks_for(s.pixels * s.C, 256), 256, 0, st>>>(s, x, y, scale);
-  return cudaGetLastError();
+  return launched();
 }
 cudaError_t lrn_bwd(const LrnShape& s, const float* x, const float* y, const float* scale, const float* dy, float* dx,
                     cudaStream_t st) {
   lrn_bwd_kernel<<<blocks_for(s.pixels * s.C, 256), 256, 0, st>>>(s, x, y, scale, dy, dx);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t softmax_ce(View2D z, const int32_t* labels, float* row_loss, View2D dz, float inv_nloc, int* err,
                        cudaStream_t st) {
   if (z.rows <= 0) return cudaSuccess;
   softmax_ce_kernel<<<(z.rows + 7) / 8, 256, 0, st>>>(z, labels, row_loss, dz, inv_nloc, err);
-  return cudaGetLastError();
+  return launched();
 }
 cudaError_t euclidean(View2D u, View2D v, float* row_loss, View2D du, float inv_nloc, cudaStream_t st) {
   if (u.rows <= 0) return cudaSuccess;
   euclidean_kernel<<<(u.rows + 7) / 8, 256, 0, st>>>(u, v, row_loss, du, inv_nloc);
-  return cudaGetLastError();
+  return launched();
 }
 cudaError_t sum_scaled(const float* v, int n, float scale, float* out, int* err, cudaStream_t st) {
   sum_scaled_kernel<<<1, 1024, 0, st>>>(v, n, scale, out, err);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t sgd_momentum(float* w, const float* g, float* v, long long n, float lr, float mu, float wd, float s,
@@ -460,23 +460,33 @@ cudaError_t sgd_momentum(float* w, const float* g, float* v, long long n, float 
   if (n <= 0) return cudaSuccess;
   if (!aligned16(w) || !aligned16(g) || !aligned16(v)) return cudaErrorMisalignedAddress;
   sgd_kernel<<<blocks_for(n / 4 + 1, 256), 256, 0, st>>>(w, g, v, n, nullptr, 1.f, lr, mu, wd, s);
-  return cudaGetLastError();
+  return launched();
 }
 cudaError_t sgd_momentum_dev(float* w, const float* g, float* v, long long n, const float* lr_dev, float lr_scale,
                              float mu, float wd, float s, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (!aligned16(w) || !aligned16(g) || !aligned16(v)) return cudaErrorMisalignedAddress;
   sgd_kernel<<<blocks_for(n / 4 + 1, 256), 256, 0, st>>>(w, g, v, n, lr_dev, lr_scale, 0.f, mu, wd, s);
-  return cudaGetLastError();
+  return launched();
 }
 
 cudaError_t pad_channels(const float* x, float* y, long long pixels, int cin, int cout, cudaStream_t st) {
   pad_channels_kernel<<<blocks_for(pixels * cout, 256), 256, 0, st>>>(x, y, pixels, cin, cout);
-  return cudaGetLastError();
+  return launched();
 }
 cudaError_t copy2d(const float* src, long long sld, float* dst, long long dld, int rows, int cols, cudaStream_t st) {
   copy2d_kernel<<<blocks_for((long long)rows * cols, 256), 256, 0, st>>>(src, sld, dst, dld, rows, cols);
-  return cudaGetLastError();
+  return launched();
 }
 
+}  // namespace sg
+
+namespace sg {
+namespace {
+__global__ void fill_scalar_kernel(float* p, float v) { *p = v; }
+}  // namespace
+cudaError_t fill_scalar(float* p, float v, cudaStream_t st) {
+  fill_scalar_kernel<<<1, 1, 0, st>>>(p, v);
+  return launched();
+}
 }  // namespace sg

@@ -9,6 +9,7 @@
 
 namespace sg {
 
+long long g_kernel_launches = 0;
 
 namespace {
 
@@ -29,7 +30,7 @@ Plan plan_gemm(int M, int N, int K, size_t ws_floats_avail) {
   int splits = 1;
   if (tiles < kNumSMs && nkb >= 8) {
     splits = std::min((2 * kNumSMs + tiles - 1) / tiles, nkb / 4);
-    while (splits > 1 && (size_t)splits * M * N > ws_floats_avail) --splits;
+    while (splits > 1 && (size_t)splits * M * ((N + 3) & ~3) > ws_floats_avail) --splits;
     if (splits < 1) splits = 1;
   }
   p.kb_per_split = (nkb + splits - 1) / splits;
@@ -51,7 +52,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, l
     n = (int)(idx - (long long)m * N);
   }
   float acc = 0.f;
-  const float* p = ws + (long long)m * N + n;
+  const float* p = ws + (long long)m * ((N + 3) & ~3) + n;
   for (int s = 0; s < splits; ++s) acc += p[s * split_stride];
   if (e.bias) acc += e.bias_on_m ? e.bias[m] : e.bias[n];
   if (e.relu) acc = fmaxf(acc, 0.f);
@@ -74,7 +75,7 @@ cudaError_t launch_bn(const GemmArgs<LA, LB>& args, const Plan& p, cudaStream_t 
   }
   dim3 grid(p.mt, p.nt, p.splits);
   kern<<<grid, GEMM_THREADS, SMEM, st>>>(args);
-  return cudaGetLastError();
+  return launched();
 }
 
 template <class LA, class LB>
@@ -84,8 +85,8 @@ cudaError_t run_gemm(const LA& a, const LB& b, int M, int N, int K, EpiArgs epi,
   GemmArgs<LA, LB> args{a, b, M, N, K, p.kb_per_split, epi};
   if (p.splits > 1) {
     args.epi.ws = ws.ptr;
-    args.epi.ws_ld = N;
-    args.epi.ws_split_stride = (long long)M * N;
+    args.epi.ws_ld = (N + 3) & ~3;
+    args.epi.ws_split_stride = (long long)M * ((N + 3) & ~3);
   } else {
     args.epi.ws = nullptr;
   }
@@ -98,9 +99,9 @@ cudaError_t run_gemm(const LA& a, const LB& b, int M, int N, int K, EpiArgs epi,
   }
   if (e != cudaSuccess || p.splits == 1) return e;
   long long total = (long long)M * N;
-  splitk_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(ws.ptr, p.splits, (long long)M * N, M, N,
+  splitk_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(ws.ptr, p.splits, (long long)M * ((N + 3) & ~3), M, N,
                                                                          epi);
-  return cudaGetLastError();
+  return launched();
 }
 
 MatView mv(const float* p, int rows, int cols, long long ld, long long bs = 0, int cb = 0) {
@@ -172,7 +173,7 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int nparts, 
 
 size_t gemm_ws_floats(int M, int N, int K) {
   Plan p = plan_gemm(M, N, K, (size_t)1 << 62);
-  return p.splits > 1 ? (size_t)p.splits * M * N : 0;
+  return p.splits > 1 ? (size_t)p.splits * M * ((N + 3) & ~3) : 0;
 }
 
 cudaError_t colsum(const float* X, int M, int N, long long ld, float* out, Workspace ws, cudaStream_t st) {
@@ -180,10 +181,10 @@ cudaError_t colsum(const float* X, int M, int N, long long ld, float* out, Works
   if ((size_t)nparts * N > ws.floats) return cudaErrorInvalidValue;
   dim3 grid((N + 31) / 32, nparts);
   colsum_partial_kernel<<<grid, dim3(32, 8), 0, st>>>(X, M, N, ld, ws.ptr);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launched();
   if (e != cudaSuccess) return e;
   colsum_final_kernel<<<(N + 127) / 128, 128, 0, st>>>(ws.ptr, nparts, N, out);
-  return cudaGetLastError();
+  return launched();
 }
 
 size_t colsum_ws_floats(int M, int N) { return (size_t)((M + CS_ROWS_PER_BLOCK - 1) / CS_ROWS_PER_BLOCK) * N; }

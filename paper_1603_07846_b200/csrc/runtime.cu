@@ -1,0 +1,914 @@
+// Runtime: cluster topology, NeuralNet on the device, BPTrainOneBatch
+// (Alg. 1), server-group Updater over sharded Params (P:282-284,
+// P:419-422) and the connection layers' collectives over NCCL.
+//
+// Streams: every net owns a compute stream (forward / backward / connection
+// collectives on the activation communicator) and a parameter stream (per-layer
+// Update = reduce-scatter -> sharded Updater -> all-gather on the parameter
+// communicator), joined by events: Update(layer) overlaps the backward of the
+// layers below it, Collect(layer) waits for its Update (Alg. 1 line "Collect").
+// sg_train_one_batch can be captured once into a CUDA graph and replayed.
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "abi_common.h"
+#include "ops.h"
+#include "plan.h"
+
+namespace sg {
+size_t colsum_ws_floats(int M, int N);
+}
+
+#define SG_NCCL(expr)                                                                                 \
+  do {                                                                                                \
+    ncclResult_t _r = (expr);                                                                         \
+    if (_r != ncclSuccess) SG_FAIL(SG_ERR_NCCL, "NCCL error %s at %s:%d (%s)", ncclGetErrorString(_r), \
+                                   __FILE__, __LINE__, #expr);                                        \
+  } while (0)
+
+#define SG_LCH(expr)                                                                               \
+  do {                                                                                             \
+    cudaError_t _e = (expr);                                                                       \
+    if (_e != cudaSuccess) SG_FAIL(SG_ERR_CUDA, "%s: %s (%s)", L.name.c_str(), cudaGetErrorString(_e), #expr); \
+  } while (0)
+
+struct sg_cluster {
+  int rank = 0, world = 1, device = 0;
+  ncclComm_t comm_act = nullptr;  // activations / connection layers (compute stream)
+  ncclComm_t comm_par = nullptr;  // parameter sync (parameter stream)
+};
+
+struct sg_updater {
+  sg_updater_cfg cfg;
+  float s;
+};
+
+struct sg_net {
+  sg_cluster* cl = nullptr;
+  sg_plan plan;
+  cudaStream_t cs = nullptr, ps = nullptr;
+  std::vector<float*> data, grad, scale;
+  std::vector<uint8_t*> mask;
+  std::vector<float*> sw, sgr, sv;  // per store: weights (full), gradients (full), history (shard)
+  float* row_loss = nullptr;
+  float* loss_int = nullptr;
+  float* lr_dev = nullptr;
+  int* err = nullptr;
+  int32_t* labels = nullptr;
+  float* x_stage = nullptr;
+  const float* x_src = nullptr;
+  sg::Workspace ws;
+  std::vector<cudaEvent_t> ev_grad, ev_upd;
+  std::vector<char> upd_pending, fwd_done, bwd_done;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
+  bool input_set = false;
+  // graph
+  bool graph_on = false;
+  cudaGraphExec_t gexec = nullptr;
+  sg_updater* graph_upd = nullptr;
+  long long graph_launches = 0;
+  long long last_launches = 0;
+  std::vector<void*> allocs;
+};
+
+namespace sg {
+namespace {
+
+const Plan& PL(const sg_net* n) { return n->plan.p; }
+
+sg_status dalloc(sg_net* n, size_t bytes, void** out) {
+  if (bytes == 0) bytes = 16;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) SG_FAIL(SG_ERR_OOM, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+  e = cudaMemset(p, 0, bytes);
+  if (e != cudaSuccess) SG_FAIL(SG_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+  n->allocs.push_back(p);
+  *out = p;
+  return SG_OK;
+}
+template <class T>
+sg_status dalloc_t(sg_net* n, size_t count, T** out) {
+  void* p;
+  SG_TRY(dalloc(n, count * sizeof(T), &p));
+  *out = static_cast<T*>(p);
+  return SG_OK;
+}
+
+float lr_at(const sg_updater_cfg& c, int64_t step) {
+  if (c.lr_policy == 1 && c.step_size > 0) return (float)(c.base_lr * std::pow((double)c.gamma, (double)(step / c.step_size)));
+  return c.base_lr;
+}
+
+// ---- views of blobs ----
+View2D feat_view(const LayerPlan& L, float* p, int64_t logical_cols) {
+  View2D v;
+  v.p = p;
+  v.ld = L.ld;
+  v.bs = L.rows * L.ld;
+  v.rows = (int)L.rows;
+  v.cols = (int)logical_cols;
+  v.cb = L.nblocks > 1 ? (int)L.ld : (int)logical_cols;
+  return v;
+}
+// real-column view (losses): blocked with the real block width
+View2D real_view(const LayerPlan& L, float* p) {
+  View2D v;
+  v.p = p;
+  v.ld = L.ld;
+  v.bs = L.rows * L.ld;
+  v.rows = (int)L.rows;
+  v.cols = (int)(L.nblocks > 1 ? L.feat : L.cols);
+  v.cb = L.nblocks > 1 ? (int)L.blk_cols : v.cols;
+  return v;
+}
+
+ConvShape conv_shape(const LayerPlan& L, const LayerPlan& S) {
+  return ConvShape{(int)L.rows, S.h, S.w, S.c, L.c, L.kernel, L.kernel, L.stride, L.pad, L.h, L.w};
+}
+PoolShape pool_shape(const LayerPlan& L, const LayerPlan& S) {
+  return PoolShape{(int)L.rows, S.h, S.w, S.c, L.kernel, L.stride, L.pad, L.h, L.w};
+}
+
+// ---- ComputeFeature ----
+sg_status forward(sg_net* n, int i) {
+  const Plan& P = PL(n);
+  const LayerPlan& L = P.layers[i];
+  cudaStream_t st = n->cs;
+  const int K = P.world;
+  float* W = L.pW >= 0 ? n->sw[L.store] + P.params[L.pW].store_off : nullptr;
+  float* b = L.pb >= 0 ? n->sw[L.store] + P.params[L.pb].store_off : nullptr;
+  const LayerPlan* S = L.src >= 0 ? &P.layers[L.src] : nullptr;
+  switch (L.kind) {
+    case SG_INPUT:
+      SG_CHECK(n->x_src, SG_ERR_SEQUENCE, "sequence error: no input set (sg_net_set_input)");
+      if (L.image)
+        SG_LCH(pad_channels(n->x_src, n->data[i], L.rows * L.h * L.w, L.c_real, L.c, st));
+      else
+        SG_LCH(copy2d(n->x_src, L.feat, n->data[i], L.ld, (int)L.rows, (int)L.feat, st));
+      break;
+    case SG_CONV:
+      SG_LCH(conv_fwd(conv_shape(L, *S), n->data[L.src], W, b, n->data[i], 0, n->ws, st));
+      break;
+    case SG_POOL_MAX:
+      SG_LCH(maxpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], n->mask[i], st));
+      break;
+    case SG_POOL_AVG:
+      SG_LCH(avgpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], st));
+      break;
+    case SG_LRN:
+      SG_LCH(lrn_fwd(LrnShape{L.rows * L.h * L.w, L.c, L.lrn_size, L.alpha, L.beta, L.k}, n->data[L.src],
+                     n->data[i], n->scale[i], st));
+      break;
+    case SG_RELU:
+      SG_LCH(relu_fwd(n->data[L.src], n->data[i], L.blob_floats(), st));
+      break;
+    case SG_SIGMOID:
+      SG_LCH(sigmoid_fwd(n->data[L.src], n->data[i], L.blob_floats(), st));
+      break;
+    case SG_INNER_PRODUCT:
+      SG_LCH(ip_fwd(feat_view(*S, n->data[L.src], L.kin), W, (int)L.kin, (int)L.nout, b,
+                    plain(n->data[i], (int)L.rows, (int)L.nout, L.ld), 0, n->ws, st));
+      break;
+    case SG_CONCAT:
+      SG_NCCL(ncclAllGather(n->data[L.src], n->data[i], (size_t)(S->rows * S->ld), ncclFloat, n->cl->comm_act, st));
+      break;
+    case SG_SLICE: {
+      const size_t cnt = (size_t)(L.rows * S->ld);
+      SG_NCCL(ncclGroupStart());
+      for (int j = 0; j < K; ++j) {
+        SG_NCCL(ncclSend(n->data[L.src] + j * cnt, cnt, ncclFloat, j, n->cl->comm_act, st));
+        SG_NCCL(ncclRecv(n->data[i] + j * cnt, cnt, ncclFloat, j, n->cl->comm_act, st));
+      }
+      SG_NCCL(ncclGroupEnd());
+      break;
+    }
+    case SG_SOFTMAX_CE:
+      SG_LCH(softmax_ce(real_view(*S, n->data[L.src]), n->labels, n->row_loss, real_view(*S, n->grad[L.src]),
+                        (float)(1.0 / (double)P.loss_rows), n->err, st));
+      break;
+    case SG_EUCLIDEAN: {
+      const LayerPlan& in = P.layers[0];
+      View2D u = real_view(*S, n->data[L.src]);
+      View2D v = plain(n->data[0] + S->col_off, (int)S->rows, (int)S->cols, in.ld);
+      SG_LCH(euclidean(u, v, n->row_loss, real_view(*S, n->grad[L.src]), (float)(1.0 / (double)P.loss_rows), st));
+      break;
+    }
+  }
+  return SG_OK;
+}
+
+// ---- ComputeGradient ----
+sg_status backward(sg_net* n, int i) {
+  const Plan& P = PL(n);
+  const LayerPlan& L = P.layers[i];
+  cudaStream_t st = n->cs;
+  const int K = P.world;
+  if (L.kind == SG_INPUT || L.kind == SG_SOFTMAX_CE || L.kind == SG_EUCLIDEAN) return SG_OK;
+  const LayerPlan& S = P.layers[L.src];
+  const bool need_dx = S.kind != SG_INPUT;
+  float* W = L.pW >= 0 ? n->sw[L.store] + P.params[L.pW].store_off : nullptr;
+  float* dW = L.pW >= 0 ? n->sgr[L.store] + P.params[L.pW].store_off : nullptr;
+  float* db = L.pb >= 0 ? n->sgr[L.store] + P.params[L.pb].store_off : nullptr;
+  switch (L.kind) {
+    case SG_CONV:
+      SG_LCH(conv_wgrad(conv_shape(L, S), n->data[L.src], n->grad[i], dW, db, n->ws, st));
+      if (need_dx) SG_LCH(conv_dgrad(conv_shape(L, S), n->grad[i], W, n->grad[L.src], n->ws, st));
+      break;
+    case SG_POOL_MAX:
+      if (need_dx) SG_LCH(maxpool_bwd(pool_shape(L, S), n->grad[i], n->mask[i], n->grad[L.src], st));
+      break;
+    case SG_POOL_AVG:
+      if (need_dx) SG_LCH(avgpool_bwd(pool_shape(L, S), n->grad[i], n->grad[L.src], st));
+      break;
+    case SG_LRN:
+      if (need_dx)
+        SG_LCH(lrn_bwd(LrnShape{L.rows * L.h * L.w, L.c, L.lrn_size, L.alpha, L.beta, L.k}, n->data[L.src],
+                       n->data[i], n->scale[i], n->grad[i], n->grad[L.src], st));
+      break;
+    case SG_RELU:
+      if (need_dx) SG_LCH(relu_bwd(n->data[i], n->grad[i], n->grad[L.src], L.blob_floats(), st));
+      break;
+    case SG_SIGMOID:
+      if (need_dx) SG_LCH(sigmoid_bwd(n->data[i], n->grad[i], n->grad[L.src], L.blob_floats(), st));
+      break;
+    case SG_INNER_PRODUCT: {
+      View2D dy = plain(n->grad[i], (int)L.rows, (int)L.nout, L.ld);
+      SG_LCH(ip_wgrad(feat_view(S, n->data[L.src], L.kin), dy, (int)L.kin, (int)L.nout, dW, db, n->ws, st));
+      if (need_dx) SG_LCH(ip_dgrad(dy, W, (int)L.kin, (int)L.nout, feat_view(S, n->grad[L.src], L.kin), n->ws, st));
+      break;
+    }
+    case SG_CONCAT:
+      SG_NCCL(ncclReduceScatter(n->grad[i], n->grad[L.src], (size_t)(S.rows * S.ld), ncclFloat, ncclSum,
+                                n->cl->comm_act, st));
+      break;
+    case SG_SLICE: {
+      const size_t cnt = (size_t)(L.rows * S.ld);
+      SG_NCCL(ncclGroupStart());
+      for (int j = 0; j < K; ++j) {
+        SG_NCCL(ncclSend(n->grad[i] + j * cnt, cnt, ncclFloat, j, n->cl->comm_act, st));
+        SG_NCCL(ncclRecv(n->grad[L.src] + j * cnt, cnt, ncclFloat, j, n->cl->comm_act, st));
+      }
+      SG_NCCL(ncclGroupEnd());
+      break;
+    }
+  }
+  return SG_OK;
+}
+
+// ---- Update(layer.params()): worker group -> server group -> workers ----
+sg_status update(sg_net* n, sg_updater* u, int i) {
+  const Plan& P = PL(n);
+  const LayerPlan& L = P.layers[i];
+  if (L.store < 0) return SG_OK;
+  const StorePlan& S = P.stores[L.store];
+  SG_CUDA(cudaEventRecord(n->ev_grad[i], n->cs));
+  SG_CUDA(cudaStreamWaitEvent(n->ps, n->ev_grad[i], 0));
+  const float mu = u->cfg.momentum, wd = u->cfg.weight_decay * L.wd_scale;
+  if (S.sharded) {
+    const int64_t shard = S.padded / P.world;
+    float* g = n->sgr[L.store];
+    float* w = n->sw[L.store];
+    SG_NCCL(ncclReduceScatter(g, g + P.rank * shard, (size_t)shard, ncclFloat, ncclSum, n->cl->comm_par, n->ps));
+    SG_LCH(sgd_momentum_dev(w + P.rank * shard, g + P.rank * shard, n->sv[L.store], shard, n->lr_dev, L.lr_scale, mu,
+                            wd, u->s, n->ps));
+    SG_NCCL(ncclAllGather(w + P.rank * shard, w, (size_t)shard, ncclFloat, n->cl->comm_par, n->ps));
+  } else {
+    SG_LCH(sgd_momentum_dev(n->sw[L.store], n->sgr[L.store], n->sv[L.store], S.padded, n->lr_dev, L.lr_scale, mu, wd,
+                            u->s, n->ps));
+  }
+  SG_CUDA(cudaEventRecord(n->ev_upd[i], n->ps));
+  n->upd_pending[i] = 1;
+  return SG_OK;
+}
+
+sg_status collect(sg_net* n, int i) {
+  if (n->upd_pending[i]) {
+    SG_CUDA(cudaStreamWaitEvent(n->cs, n->ev_upd[i], 0));
+    n->upd_pending[i] = 0;
+  }
+  return SG_OK;
+}
+
+sg_status loss_reduce(sg_net* n) {
+  const Plan& P = PL(n);
+  cudaError_t e = sum_scaled(n->row_loss, (int)P.loss_rows, (float)(1.0 / P.batch), n->loss_int, n->err, n->cs);
+  SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "loss reduction: %s", cudaGetErrorString(e));
+  if (P.world > 1) SG_NCCL(ncclAllReduce(n->loss_int, n->loss_int, 1, ncclFloat, ncclSum, n->cl->comm_act, n->cs));
+  return SG_OK;
+}
+
+sg_status set_input(sg_net* n, const float* x, const int32_t* labels) {
+  const Plan& P = PL(n);
+  SG_CHECK(x, SG_ERR_INVALID_ARG, "set_input: null input");
+  n->x_src = x;
+  if (P.layers[P.loss].kind == SG_SOFTMAX_CE) {
+    SG_CHECK(labels, SG_ERR_INVALID_ARG, "set_input: labels required for a softmax loss");
+    SG_CUDA(cudaMemcpyAsync(n->labels, labels, P.loss_rows * sizeof(int32_t), cudaMemcpyDeviceToDevice, n->cs));
+  }
+  n->input_set = true;
+  std::fill(n->fwd_done.begin(), n->fwd_done.end(), 0);
+  std::fill(n->bwd_done.begin(), n->bwd_done.end(), 0);
+  return SG_OK;
+}
+
+// The whole Alg. 1 step on the compute stream (input already set).
+sg_status step_body(sg_net* n, sg_updater* u) {
+  const Plan& P = PL(n);
+  const int nl = (int)P.layers.size();
+  for (int i = 0; i < nl; ++i) {
+    SG_TRY(collect(n, i));
+    SG_TRY(forward(n, i));
+  }
+  for (int i = nl - 1; i >= 0; --i) {
+    SG_TRY(backward(n, i));
+    SG_TRY(update(n, u, i));
+  }
+  SG_TRY(loss_reduce(n));
+  // join the parameter stream (all Updates of this step) back into the compute stream
+  SG_CUDA(cudaEventRecord(n->ev_join, n->ps));
+  SG_CUDA(cudaStreamWaitEvent(n->cs, n->ev_join, 0));
+  std::fill(n->upd_pending.begin(), n->upd_pending.end(), 0);
+  return SG_OK;
+}
+
+sg_status enter(sg_net* n, void* stream) {
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  SG_CUDA(cudaEventRecord(n->ev_in, reinterpret_cast<cudaStream_t>(stream)));
+  SG_CUDA(cudaStreamWaitEvent(n->cs, n->ev_in, 0));
+  return SG_OK;
+}
+sg_status leave(sg_net* n, void* stream) {
+  SG_CUDA(cudaEventRecord(n->ev_out, n->cs));
+  SG_CUDA(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), n->ev_out, 0));
+  return SG_OK;
+}
+
+// ---- user layout <-> internal layout of one Param (host arrays) ----
+void to_internal(const Plan& P, const ParamPlan& q, const float* user, std::vector<float>& out) {
+  const LayerPlan& L = P.layers[q.layer];
+  const LayerPlan& S = P.layers[L.src];
+  out.assign(q.isize, 0.f);
+  if (L.kind == SG_CONV) {
+    if (q.is_bias) {
+      for (int64_t j = 0; j < q.isize; ++j) out[j] = user[j];
+      return;
+    }
+    const int RS = L.kernel * L.kernel;
+    for (int co = 0; co < L.c; ++co)
+      for (int rs = 0; rs < RS; ++rs)
+        for (int c = 0; c < S.c_real; ++c)
+          out[((int64_t)co * RS + rs) * S.c + c] = user[((int64_t)co * RS + rs) * S.c_real + c];
+    return;
+  }
+  const int64_t dh = q.cols;
+  if (q.is_bias) {
+    for (int64_t j = 0; j < L.cols; ++j) out[j] = user[L.col_off + j];
+    return;
+  }
+  for (int64_t i = 0; i < L.kin; ++i) {
+    int64_t r = i;
+    if (L.rmap_pad > 0) {
+      const int64_t blk = i / L.rmap_pad, jj = i % L.rmap_pad;
+      if (jj >= L.rmap_real) continue;
+      r = blk * L.rmap_real + jj;
+    }
+    const float* src = user + r * dh + L.col_off;
+    float* dst = out.data() + i * L.nout;
+    for (int64_t j = 0; j < L.cols; ++j) dst[j] = src[j];
+  }
+}
+
+// internal local block of rank `rk` -> user layout (only the entries that rank owns)
+void from_internal(const Plan& P, const ParamPlan& q, const float* in, int rk, float* user) {
+  const LayerPlan& L = P.layers[q.layer];
+  const LayerPlan& S = P.layers[L.src];
+  if (L.kind == SG_CONV) {
+    if (q.is_bias) {
+      for (int64_t j = 0; j < q.cols; ++j) user[j] = in[j];
+      return;
+    }
+    const int RS = L.kernel * L.kernel;
+    for (int co = 0; co < L.c; ++co)
+      for (int rs = 0; rs < RS; ++rs)
+        for (int c = 0; c < S.c_real; ++c)
+          user[((int64_t)co * RS + rs) * S.c_real + c] = in[((int64_t)co * RS + rs) * S.c + c];
+    return;
+  }
+  const int64_t dh = q.cols;
+  const int64_t col_off = (q.split_dim == 1) ? rk * L.cols : 0;
+  if (q.is_bias) {
+    for (int64_t j = 0; j < L.cols; ++j) user[col_off + j] = in[j];
+    return;
+  }
+  for (int64_t i = 0; i < L.kin; ++i) {
+    int64_t r = i;
+    if (L.rmap_pad > 0) {
+      const int64_t blk = i / L.rmap_pad, jj = i % L.rmap_pad;
+      if (jj >= L.rmap_real) continue;
+      r = blk * L.rmap_real + jj;
+    }
+    for (int64_t j = 0; j < L.cols; ++j) user[r * dh + col_off + j] = in[i * L.nout + j];
+  }
+}
+
+// Gathers a Param-shaped quantity (which: 0 value, 1 grad, 2 history) into the user layout.
+sg_status param_export(sg_net* n, int p, int which, float* user) {
+  const Plan& P = PL(n);
+  SG_CHECK(p >= 0 && p < (int)P.params.size(), SG_ERR_INVALID_ARG, "param index %d out of range", p);
+  SG_CHECK(user, SG_ERR_INVALID_ARG, "null host buffer");
+  const ParamPlan& q = P.params[p];
+  const StorePlan& S = P.stores[q.store];
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  SG_CUDA(cudaStreamSynchronize(n->ps));
+  SG_CUDA(cudaStreamSynchronize(n->cs));
+  const int K = P.world;
+  if (q.split_dim == 1) {
+    const float* src = (which == 0 ? n->sw : which == 1 ? n->sgr : n->sv)[q.store] + q.store_off;
+    float* tmp;
+    SG_CUDA(cudaMalloc(&tmp, (size_t)q.isize * K * sizeof(float)));
+    ncclResult_t r = ncclAllGather(src, tmp, (size_t)q.isize, ncclFloat, n->cl->comm_act, n->cs);
+    std::vector<float> h((size_t)q.isize * K);
+    cudaError_t e = cudaStreamSynchronize(n->cs);
+    if (e == cudaSuccess) e = cudaMemcpy(h.data(), tmp, h.size() * sizeof(float), cudaMemcpyDeviceToHost);
+    cudaFree(tmp);
+    SG_CHECK(r == ncclSuccess, SG_ERR_NCCL, "param export: %s", ncclGetErrorString(r));
+    SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "param export: %s", cudaGetErrorString(e));
+    for (int rk = 0; rk < K; ++rk) from_internal(P, q, h.data() + (size_t)rk * q.isize, rk, user);
+    return SG_OK;
+  }
+  // replicated (dim-0) Param: full value on every rank; grad / history sharded when K > 1
+  std::vector<float> h((size_t)S.padded);
+  if (which == 0 || !S.sharded) {
+    const float* src = (which == 0 ? n->sw : which == 1 ? n->sgr : n->sv)[q.store];
+    SG_CUDA(cudaMemcpy(h.data(), src, (size_t)S.padded * sizeof(float), cudaMemcpyDeviceToHost));
+  } else {
+    const int64_t shard = S.padded / K;
+    const float* src = which == 1 ? n->sgr[q.store] + P.rank * shard : n->sv[q.store];
+    float* tmp;
+    SG_CUDA(cudaMalloc(&tmp, (size_t)S.padded * sizeof(float)));
+    ncclResult_t r = ncclAllGather(src, tmp, (size_t)shard, ncclFloat, n->cl->comm_act, n->cs);
+    cudaError_t e = cudaStreamSynchronize(n->cs);
+    if (e == cudaSuccess) e = cudaMemcpy(h.data(), tmp, h.size() * sizeof(float), cudaMemcpyDeviceToHost);
+    cudaFree(tmp);
+    SG_CHECK(r == ncclSuccess, SG_ERR_NCCL, "param export: %s", ncclGetErrorString(r));
+    SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "param export: %s", cudaGetErrorString(e));
+  }
+  from_internal(P, q, h.data() + q.store_off, P.rank, user);
+  return SG_OK;
+}
+
+sg_status destroy_net(sg_net* n) {
+  if (!n) return SG_OK;
+  cudaSetDevice(n->cl ? n->cl->device : 0);
+  if (n->cs) cudaStreamSynchronize(n->cs);
+  if (n->ps) cudaStreamSynchronize(n->ps);
+  if (n->gexec) cudaGraphExecDestroy(n->gexec);
+  for (void* p : n->allocs) cudaFree(p);
+  for (auto e : n->ev_grad) cudaEventDestroy(e);
+  for (auto e : n->ev_upd) cudaEventDestroy(e);
+  for (auto e : {n->ev_in, n->ev_out, n->ev_fork, n->ev_join})
+    if (e) cudaEventDestroy(e);
+  if (n->cs) cudaStreamDestroy(n->cs);
+  if (n->ps) cudaStreamDestroy(n->ps);
+  delete n;
+  return SG_OK;
+}
+
+sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
+  SG_TRY(build_plan(cfg, c->rank, c->world, &n->plan.p));
+  const Plan& P = n->plan.p;
+  SG_CUDA(cudaSetDevice(c->device));
+  SG_CUDA(cudaStreamCreateWithFlags(&n->cs, cudaStreamNonBlocking));
+  SG_CUDA(cudaStreamCreateWithFlags(&n->ps, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&n->ev_in, &n->ev_out, &n->ev_fork, &n->ev_join})
+    SG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  const int nl = (int)P.layers.size();
+  n->data.assign(nl, nullptr);
+  n->grad.assign(nl, nullptr);
+  n->scale.assign(nl, nullptr);
+  n->mask.assign(nl, nullptr);
+  n->ev_grad.resize(nl);
+  n->ev_upd.resize(nl);
+  n->upd_pending.assign(nl, 0);
+  n->fwd_done.assign(nl, 0);
+  n->bwd_done.assign(nl, 0);
+  for (int i = 0; i < nl; ++i) {
+    SG_CUDA(cudaEventCreateWithFlags(&n->ev_grad[i], cudaEventDisableTiming));
+    SG_CUDA(cudaEventCreateWithFlags(&n->ev_upd[i], cudaEventDisableTiming));
+  }
+  size_t ws = 1 << 16;
+  auto need = [&](size_t f) {
+    if (f > ws) ws = f;
+  };
+  for (int i = 0; i < nl; ++i) {
+    const LayerPlan& L = P.layers[i];
+    if (L.kind == SG_SOFTMAX_CE || L.kind == SG_EUCLIDEAN) continue;
+    SG_TRY(dalloc_t(n, (size_t)L.blob_floats(), &n->data[i]));
+    if (L.kind != SG_INPUT) SG_TRY(dalloc_t(n, (size_t)L.blob_floats(), &n->grad[i]));
+    if (L.kind == SG_POOL_MAX) SG_TRY(dalloc_t(n, (size_t)L.blob_floats(), &n->mask[i]));
+    if (L.kind == SG_LRN) SG_TRY(dalloc_t(n, (size_t)L.blob_floats(), &n->scale[i]));
+    if (L.kind == SG_CONV) {
+      const LayerPlan& S = P.layers[L.src];
+      const int Kg = L.kernel * L.kernel * S.c;
+      need(gemm_ws_floats((int)(L.rows * L.h * L.w), L.c, Kg));
+      need(gemm_ws_floats(Kg, L.c, (int)(L.rows * L.h * L.w)));
+      need(gemm_ws_floats((int)(L.rows * S.h * S.w), S.c, L.kernel * L.kernel * L.c));
+      need(colsum_ws_floats((int)(L.rows * L.h * L.w), L.c));
+    }
+    if (L.kind == SG_INNER_PRODUCT) {
+      need(gemm_ws_floats((int)L.rows, (int)L.nout, (int)L.kin));
+      need(gemm_ws_floats((int)L.kin, (int)L.nout, (int)L.rows));
+      need(gemm_ws_floats((int)L.rows, (int)L.kin, (int)L.nout));
+      need(colsum_ws_floats((int)L.rows, (int)L.nout));
+    }
+  }
+  // the input blob's source (input layer pad) is the user's x; gradients of the
+  // input layer are never formed.  The loss layer writes dz into its source's grad.
+  SG_TRY(dalloc_t(n, ws, &n->ws.ptr));
+  n->ws.floats = ws;
+  SG_TRY(dalloc_t(n, (size_t)std::max<int64_t>(P.loss_rows, 1), &n->row_loss));
+  n->data[P.loss] = n->row_loss;
+  SG_TRY(dalloc_t(n, 4, &n->loss_int));
+  SG_TRY(dalloc_t(n, 4, &n->lr_dev));
+  SG_TRY(dalloc_t(n, 4, &n->err));
+  SG_TRY(dalloc_t(n, (size_t)std::max<int64_t>(P.loss_rows, 1), &n->labels));
+  {
+    const LayerPlan& in = P.layers[0];
+    SG_TRY(dalloc_t(n, (size_t)(in.rows * in.feat), &n->x_stage));
+  }
+  for (const StorePlan& S : P.stores) {
+    float *w, *g, *v;
+    SG_TRY(dalloc_t(n, (size_t)S.padded, &w));
+    SG_TRY(dalloc_t(n, (size_t)S.padded, &g));
+    SG_TRY(dalloc_t(n, (size_t)(S.sharded ? S.padded / P.world : S.padded), &v));
+    n->sw.push_back(w);
+    n->sgr.push_back(g);
+    n->sv.push_back(v);
+  }
+  SG_CUDA(cudaDeviceSynchronize());
+  return SG_OK;
+}
+
+}  // namespace
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+// ------------------------------------------------------------------ cluster --
+SG_API sg_status sg_get_unique_id(uint8_t out[128]) {
+  SG_CHECK(out, SG_ERR_INVALID_ARG, "null output");
+  ncclUniqueId id;
+  SG_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(out, &id, 128);
+  return SG_OK;
+}
+
+SG_API sg_status sg_cluster_create(const sg_cluster_cfg* cfg, sg_cluster** out) {
+  SG_CHECK(cfg && out, SG_ERR_INVALID_ARG, "sg_cluster_create: null argument");
+  SG_CHECK(cfg->world_size >= 1 && cfg->rank >= 0 && cfg->rank < cfg->world_size, SG_ERR_INVALID_ARG,
+           "cluster: rank %d world %d", cfg->rank, cfg->world_size);
+  SG_CHECK(cfg->nworker_groups == 1 && cfg->nserver_groups == 1, SG_ERR_UNSUPPORTED,
+           "unsupported: %d worker groups / %d server groups (asynchronous frameworks are out of scope; "
+           "synchronous training uses 1 worker group and 1 server group, P:411-422)",
+           cfg->nworker_groups, cfg->nserver_groups);
+  SG_CHECK(cfg->workers_per_group == cfg->world_size && cfg->servers_per_group == cfg->world_size,
+           SG_ERR_UNSUPPORTED, "unsupported: %d workers / %d servers per group on %d ranks (AllReduce framework binds "
+           "one worker and one server per rank, P:419-422)",
+           cfg->workers_per_group, cfg->servers_per_group, cfg->world_size);
+  SG_CUDA(cudaSetDevice(cfg->device));
+  sg_cluster* c = new sg_cluster();
+  c->rank = cfg->rank;
+  c->world = cfg->world_size;
+  c->device = cfg->device;
+  if (c->world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm_act, c->world, id, c->rank);
+    if (r == ncclSuccess) r = ncclCommSplit(c->comm_act, 0, c->rank, &c->comm_par, nullptr);
+    if (r != ncclSuccess) {
+      delete c;
+      SG_FAIL(SG_ERR_NCCL, "NCCL communicator creation failed: %s", ncclGetErrorString(r));
+    }
+  }
+  *out = c;
+  return SG_OK;
+}
+
+SG_API sg_status sg_cluster_framework(const sg_cluster* c, const char** name) {
+  SG_CHECK(c && name, SG_ERR_INVALID_ARG, "null argument");
+  *name = "AllReduce";
+  return SG_OK;
+}
+
+SG_API sg_status sg_cluster_destroy(sg_cluster* c) {
+  if (!c) return SG_OK;
+  if (c->comm_par) ncclCommDestroy(c->comm_par);
+  if (c->comm_act) ncclCommDestroy(c->comm_act);
+  delete c;
+  return SG_OK;
+}
+
+// ---------------------------------------------------------------------- net --
+SG_API sg_status sg_net_create(sg_cluster* c, const sg_net_cfg* cfg, sg_net** out) {
+  SG_CHECK(c && cfg && out, SG_ERR_INVALID_ARG, "sg_net_create: null argument");
+  sg_net* n = new sg_net();
+  n->cl = c;
+  sg_status st = create_net(c, cfg, n);
+  if (st != SG_OK) {
+    std::string msg = get_error();
+    destroy_net(n);
+    set_error("%s", msg.c_str());
+    return st;
+  }
+  *out = n;
+  return SG_OK;
+}
+
+SG_API sg_status sg_net_destroy(sg_net* n) { return destroy_net(n); }
+
+SG_API sg_status sg_net_plan(const sg_net* n, const sg_plan** out) {
+  SG_CHECK(n && out, SG_ERR_INVALID_ARG, "null argument");
+  *out = &n->plan;
+  return SG_OK;
+}
+
+SG_API sg_status sg_param_set_value(sg_net* n, int32_t p, const float* user) {
+  SG_CHECK(n && user, SG_ERR_INVALID_ARG, "null argument");
+  const Plan& P = PL(n);
+  SG_CHECK(p >= 0 && p < (int)P.params.size(), SG_ERR_INVALID_ARG, "param index %d out of range", p);
+  const ParamPlan& q = P.params[p];
+  std::vector<float> h;
+  to_internal(P, q, user, h);
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  SG_CUDA(cudaStreamSynchronize(n->ps));
+  SG_CUDA(cudaStreamSynchronize(n->cs));
+  SG_CUDA(cudaMemcpy(n->sw[q.store] + q.store_off, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+  return SG_OK;
+}
+SG_API sg_status sg_param_get_value(sg_net* n, int32_t p, float* user) {
+  SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
+  return param_export(n, p, 0, user);
+}
+SG_API sg_status sg_param_get_grad(sg_net* n, int32_t p, float* user) {
+  SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
+  return param_export(n, p, 1, user);
+}
+SG_API sg_status sg_param_get_history(sg_net* n, int32_t p, float* user) {
+  SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
+  return param_export(n, p, 2, user);
+}
+
+SG_API sg_status sg_updater_create(sg_net* n, const sg_updater_cfg* cfg, sg_updater** out) {
+  SG_CHECK(n && cfg && out, SG_ERR_INVALID_ARG, "null argument");
+  SG_CHECK(cfg->base_lr >= 0.f && cfg->momentum >= 0.f && cfg->momentum < 1.f && cfg->weight_decay >= 0.f,
+           SG_ERR_CONFIG, "updater: base_lr=%g momentum=%g weight_decay=%g", (double)cfg->base_lr,
+           (double)cfg->momentum, (double)cfg->weight_decay);
+  SG_CHECK(cfg->lr_policy == 0 || (cfg->lr_policy == 1 && cfg->step_size > 0), SG_ERR_CONFIG,
+           "updater: lr_policy=%d step_size=%d", cfg->lr_policy, cfg->step_size);
+  sg_updater* u = new sg_updater();
+  u->cfg = *cfg;
+  u->s = cfg->grad_scale > 0.f ? cfg->grad_scale : PL(n).grad_scale;
+  *out = u;
+  return SG_OK;
+}
+SG_API sg_status sg_updater_destroy(sg_updater* u) {
+  delete u;
+  return SG_OK;
+}
+
+SG_API sg_status sg_net_set_input(sg_net* n, const float* x, const int32_t* labels, void* stream) {
+  SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
+  SG_TRY(enter(n, stream));
+  SG_TRY(set_input(n, x, labels));
+  return leave(n, stream);
+}
+
+SG_API sg_status sg_net_collect(sg_net* n, int32_t layer, void* stream) {
+  SG_CHECK(n && layer >= 0 && layer < (int)PL(n).layers.size(), SG_ERR_INVALID_ARG, "bad layer %d", layer);
+  SG_TRY(enter(n, stream));
+  SG_TRY(collect(n, layer));
+  return leave(n, stream);
+}
+
+SG_API sg_status sg_layer_compute_feature(sg_net* n, int32_t layer, void* stream) {
+  SG_CHECK(n && layer >= 0 && layer < (int)PL(n).layers.size(), SG_ERR_INVALID_ARG, "bad layer %d", layer);
+  const Plan& P = PL(n);
+  SG_CHECK(n->input_set, SG_ERR_SEQUENCE, "sequence error: ComputeFeature(%s) before sg_net_set_input",
+           P.layers[layer].name.c_str());
+  const int src = P.layers[layer].src;
+  SG_CHECK(src < 0 || n->fwd_done[src], SG_ERR_SEQUENCE,
+           "sequence error: ComputeFeature(%s) before ComputeFeature of its source %s", P.layers[layer].name.c_str(),
+           P.layers[src].name.c_str());
+  SG_TRY(enter(n, stream));
+  long long l0 = g_kernel_launches;
+  SG_TRY(forward(n, layer));
+  n->last_launches = g_kernel_launches - l0;
+  n->fwd_done[layer] = 1;
+  return leave(n, stream);
+}
+
+SG_API sg_status sg_layer_compute_gradient(sg_net* n, int32_t layer, void* stream) {
+  SG_CHECK(n && layer >= 0 && layer < (int)PL(n).layers.size(), SG_ERR_INVALID_ARG, "bad layer %d", layer);
+  const Plan& P = PL(n);
+  SG_CHECK(n->fwd_done[P.loss], SG_ERR_SEQUENCE,
+           "sequence error: ComputeGradient(%s) before the forward pass reached the loss",
+           P.layers[layer].name.c_str());
+  for (int j = layer + 1; j < (int)P.layers.size(); ++j)
+    if (P.layers[j].src == layer)
+      SG_CHECK(n->bwd_done[j] || P.layers[j].kind == SG_SOFTMAX_CE || P.layers[j].kind == SG_EUCLIDEAN,
+               SG_ERR_SEQUENCE, "sequence error: ComputeGradient(%s) before ComputeGradient of its consumer %s",
+               P.layers[layer].name.c_str(), P.layers[j].name.c_str());
+  SG_TRY(enter(n, stream));
+  SG_TRY(backward(n, layer));
+  n->bwd_done[layer] = 1;
+  return leave(n, stream);
+}
+
+SG_API sg_status sg_net_update(sg_net* n, sg_updater* u, int32_t layer, int64_t step, void* stream) {
+  SG_CHECK(n && u && layer >= 0 && layer < (int)PL(n).layers.size(), SG_ERR_INVALID_ARG, "bad argument");
+  SG_CHECK(n->bwd_done[layer] || PL(n).layers[layer].store < 0, SG_ERR_PROTOCOL,
+           "protocol error: Update(%s) before its ComputeGradient in this step", PL(n).layers[layer].name.c_str());
+  SG_TRY(enter(n, stream));
+  {
+    cudaError_t e = fill_scalar(n->lr_dev, lr_at(u->cfg, step), n->cs);
+    SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "update: %s", cudaGetErrorString(e));
+  }
+  SG_TRY(update(n, u, layer));
+  return leave(n, stream);
+}
+
+SG_API sg_status sg_net_loss(sg_net* n, float* loss_dev, void* stream) {
+  SG_CHECK(n && loss_dev, SG_ERR_INVALID_ARG, "null argument");
+  SG_TRY(enter(n, stream));
+  SG_TRY(loss_reduce(n));
+  SG_CUDA(cudaMemcpyAsync(loss_dev, n->loss_int, sizeof(float), cudaMemcpyDeviceToDevice, n->cs));
+  return leave(n, stream);
+}
+
+SG_API sg_status sg_train_one_batch(sg_net* n, sg_updater* u, int64_t step, const float* x, const int32_t* labels,
+                                    float* loss_dev, void* stream) {
+  SG_CHECK(n && u && x, SG_ERR_INVALID_ARG, "sg_train_one_batch: null argument");
+  const Plan& P = PL(n);
+  SG_TRY(enter(n, stream));
+  long long l0 = g_kernel_launches;
+  {
+    cudaError_t e = fill_scalar(n->lr_dev, lr_at(u->cfg, step), n->cs);
+    SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "train: %s", cudaGetErrorString(e));
+  }
+  if (n->graph_on) {
+    const LayerPlan& in = P.layers[0];
+    SG_CUDA(cudaMemcpyAsync(n->x_stage, x, (size_t)(in.rows * in.feat) * sizeof(float), cudaMemcpyDeviceToDevice,
+                            n->cs));
+    SG_TRY(set_input(n, n->x_stage, labels));
+    if (!n->gexec || n->graph_upd != u) {
+      if (n->gexec) cudaGraphExecDestroy(n->gexec), n->gexec = nullptr;
+      cudaGraph_t g;
+      long long c0 = g_kernel_launches;
+      SG_CUDA(cudaStreamBeginCapture(n->cs, cudaStreamCaptureModeThreadLocal));
+      sg_status st = step_body(n, u);
+      cudaError_t ce = cudaStreamEndCapture(n->cs, &g);
+      SG_TRY(st);
+      SG_CHECK(ce == cudaSuccess, SG_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+      ce = cudaGraphInstantiate(&n->gexec, g, 0);
+      cudaGraphDestroy(g);
+      SG_CHECK(ce == cudaSuccess, SG_ERR_CUDA, "graph instantiation failed: %s", cudaGetErrorString(ce));
+      n->graph_launches = g_kernel_launches - c0;
+      n->graph_upd = u;
+    }
+    SG_CUDA(cudaGraphLaunch(n->gexec, n->cs));
+    n->last_launches = (g_kernel_launches - l0) + n->graph_launches;
+  } else {
+    SG_TRY(set_input(n, x, labels));
+    SG_TRY(step_body(n, u));
+    n->last_launches = g_kernel_launches - l0;
+  }
+  if (loss_dev) SG_CUDA(cudaMemcpyAsync(loss_dev, n->loss_int, sizeof(float), cudaMemcpyDeviceToDevice, n->cs));
+  n->input_set = false;
+  return leave(n, stream);
+}
+
+SG_API sg_status sg_train_one_batch_host(sg_net* n, sg_updater* u, int64_t step, const float* x_host,
+                                         const int32_t* labels_host, float* loss_host, void* stream) {
+  SG_CHECK(n && u && x_host && loss_host, SG_ERR_INVALID_ARG, "sg_train_one_batch_host: null argument");
+  const Plan& P = PL(n);
+  const LayerPlan& in = P.layers[0];
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // host -> device staging of this step's inputs (part of the measured end-to-end path)
+  SG_CUDA(cudaMemcpyAsync(n->x_stage, x_host, (size_t)(in.rows * in.feat) * sizeof(float), cudaMemcpyHostToDevice,
+                          st));
+  const int32_t* ldev = nullptr;
+  if (labels_host && P.layers[P.loss].kind == SG_SOFTMAX_CE) {
+    SG_CUDA(cudaMemcpyAsync(n->labels, labels_host, (size_t)P.loss_rows * sizeof(int32_t), cudaMemcpyHostToDevice,
+                            st));
+    ldev = n->labels;
+  }
+  SG_TRY(sg_train_one_batch(n, u, step, n->x_stage, ldev, n->loss_int, stream));
+  SG_CUDA(cudaMemcpyAsync(loss_host, n->loss_int, sizeof(float), cudaMemcpyDeviceToHost, st));
+  SG_CUDA(cudaStreamSynchronize(st));
+  return SG_OK;
+}
+
+SG_API sg_status sg_net_sync(sg_net* n) {
+  SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  SG_CUDA(cudaStreamSynchronize(n->ps));
+  SG_CUDA(cudaStreamSynchronize(n->cs));
+  int flags = 0;
+  SG_CUDA(cudaMemcpy(&flags, n->err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flags) SG_CUDA(cudaMemset(n->err, 0, sizeof(int)));
+  SG_CHECK(!(flags & 1), SG_ERR_LABEL, "label error: a label is outside [0, %d)", PL(n).num_classes);
+  SG_CHECK(!(flags & 2), SG_ERR_DIVERGED, "diverged: non-finite loss");
+  return SG_OK;
+}
+
+SG_API sg_status sg_net_enable_graph(sg_net* n, int32_t enable) {
+  SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
+  n->graph_on = enable != 0;
+  if (!n->graph_on && n->gexec) {
+    cudaStreamSynchronize(n->cs);
+    cudaGraphExecDestroy(n->gexec);
+    n->gexec = nullptr;
+  }
+  return SG_OK;
+}
+
+SG_API sg_status sg_net_last_launch_count(const sg_net* n, int64_t* launches) {
+  SG_CHECK(n && launches, SG_ERR_INVALID_ARG, "null argument");
+  *launches = n->last_launches;
+  return SG_OK;
+}
+
+SG_API sg_status sg_blob_size(sg_net* n, int32_t layer, int32_t which, size_t* bytes) {
+  SG_CHECK(n && bytes && layer >= 0 && layer < (int)PL(n).layers.size() && which >= 0 && which <= 2,
+           SG_ERR_INVALID_ARG, "bad blob request layer=%d which=%d", layer, which);
+  const Plan& P = PL(n);
+  const LayerPlan& L = P.layers[layer];
+  *bytes = 0;
+  if (which == 0) {
+    *bytes = (L.kind == SG_SOFTMAX_CE || L.kind == SG_EUCLIDEAN) ? (size_t)P.loss_rows * 4 : L.blob_floats() * 4;
+  } else if (which == 1) {
+    if (L.src >= 0 && P.layers[L.src].kind != SG_INPUT) *bytes = P.layers[L.src].blob_floats() * 4;
+  } else if (L.kind == SG_POOL_MAX) {
+    *bytes = L.blob_floats() * 4;
+  }
+  return SG_OK;
+}
+
+SG_API sg_status sg_blob_get(sg_net* n, int32_t layer, int32_t which, void* dst, size_t bytes, void* stream) {
+  size_t need;
+  SG_TRY(sg_blob_size(n, layer, which, &need));
+  SG_CHECK(need > 0 && dst && bytes >= need, SG_ERR_INVALID_ARG, "blob %d/%d: %zu bytes needed, %zu given", layer,
+           which, need, bytes);
+  const Plan& P = PL(n);
+  const LayerPlan& L = P.layers[layer];
+  SG_TRY(enter(n, stream));
+  if (which == 0) {
+    SG_CUDA(cudaMemcpyAsync(dst, n->data[layer], need, cudaMemcpyDeviceToDevice, n->cs));
+  } else if (which == 1) {
+    SG_CUDA(cudaMemcpyAsync(dst, n->grad[L.src], need, cudaMemcpyDeviceToDevice, n->cs));
+  } else {
+    cudaError_t e = pool_argmax_expand(pool_shape(L, P.layers[L.src]), n->mask[layer], (int32_t*)dst, n->cs);
+    SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "argmax export: %s", cudaGetErrorString(e));
+  }
+  return leave(n, stream);
+}
+
+SG_API sg_status sg_blob_set(sg_net* n, int32_t layer, int32_t which, const void* src, size_t bytes, void* stream) {
+  size_t need;
+  SG_TRY(sg_blob_size(n, layer, which, &need));
+  SG_CHECK(which <= 1 && need > 0 && src && bytes == need, SG_ERR_INVALID_ARG,
+           "blob set %d/%d: %zu bytes expected, %zu given", layer, which, need, bytes);
+  const LayerPlan& L = PL(n).layers[layer];
+  SG_TRY(enter(n, stream));
+  SG_CUDA(cudaMemcpyAsync(which == 0 ? n->data[layer] : n->grad[L.src], src, need, cudaMemcpyDeviceToDevice, n->cs));
+  return leave(n, stream);
+}
+
+// ------------------------------------------------------ C5 server sync sweep --
+SG_API sg_status sg_server_sync(sg_cluster* c, const sg_updater_cfg* cfg, int64_t step, float* grad, float* w,
+                                float* v_shard, int64_t n, void* stream) {
+  SG_CHECK(c && cfg && grad && w && v_shard, SG_ERR_INVALID_ARG, "sg_server_sync: null argument");
+  SG_CHECK(n > 0 && n % (32LL * c->world) == 0, SG_ERR_PARTITION, "partition error: n=%lld not a multiple of 32*K=%d",
+           (long long)n, 32 * c->world);
+  SG_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t shard = n / c->world;
+  const float s = cfg->grad_scale > 0 ? cfg->grad_scale : 1.f / c->world;
+  if (c->world > 1)
+    SG_NCCL(ncclReduceScatter(grad, grad + c->rank * shard, (size_t)shard, ncclFloat, ncclSum, c->comm_par, st));
+  cudaError_t e = sgd_momentum(w + c->rank * shard, grad + c->rank * shard, v_shard, shard, lr_at(*cfg, step),
+                               cfg->momentum, cfg->weight_decay, s, st);
+  SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "server sync update: %s", cudaGetErrorString(e));
+  if (c->world > 1) SG_NCCL(ncclAllGather(w + c->rank * shard, w, (size_t)shard, ncclFloat, c->comm_par, st));
+  return SG_OK;
+}
+
+}  // extern "C"

@@ -314,6 +314,17 @@ SG_API sg_status sg_net_sync(sg_net* n);
 SG_API sg_status sg_net_enable_graph(sg_net* n, int32_t enable);
 /* Kernel launches issued by the last sg_train_one_batch (graph replay counts the captured kernels). */
 SG_API sg_status sg_net_last_launch_count(const sg_net* n, int64_t* launches);
+/* Per-operation device timing (CUDA events around every layer operation, also
+ * inside captured graphs).  enable != 0 arms it (a graph is re-captured).
+ * sg_net_op_times: after the stream has drained, accumulates the last step's
+ * event intervals and returns the running sums in ms, 4 slots per layer:
+ * [4*i + 0] ComputeFeature, [4*i + 1] ComputeGradient (weight gradient for
+ * conv / inner product), [4*i + 2] data gradient (conv / inner product),
+ * [4*i + 3] Update (parameter stream).  counts[] (may be NULL) = intervals
+ * summed per slot; reset != 0 clears the sums after reading. */
+SG_API sg_status sg_net_profile(sg_net* n, int32_t enable);
+SG_API sg_status sg_net_op_times(sg_net* n, double* ms, int64_t* counts, int32_t cap, int32_t* nslots,
+                                 int32_t reset);
 
 /* ---- Blob access for layer-isolated parity (this rank's local blob) ----
  * which: 0 data (layer output), 1 grad (gradient w.r.t. the layer's SOURCE

@@ -140,6 +140,8 @@ SIGS = {
     "sg_net_sync": [P],
     "sg_net_enable_graph": [P, I32],
     "sg_net_last_launch_count": [P, PI64],
+    "sg_net_profile": [P, I32],
+    "sg_net_op_times": [P, C.POINTER(C.c_double), PI64, I32, PI32, I32],
     "sg_blob_size": [P, I32, I32, C.POINTER(C.c_size_t)],
     "sg_blob_get": [P, I32, I32, P, C.c_size_t, P],
     "sg_blob_set": [P, I32, I32, P, C.c_size_t, P],

@@ -71,6 +71,12 @@ struct sg_net {
   sg_updater* graph_upd = nullptr;
   long long graph_launches = 0;
   long long last_launches = 0;
+  // per-operation event timing (sg_net_profile)
+  bool prof = false, capturing = false;
+  std::vector<cudaEvent_t> pev;  // 2 per slot, 4 slots per layer
+  std::vector<char> pused;
+  std::vector<double> pacc;
+  std::vector<long long> pcnt;
   std::vector<void*> allocs;
 };
 
@@ -133,8 +139,26 @@ PoolShape pool_shape(const LayerPlan& L, const LayerPlan& S) {
   return PoolShape{(int)L.rows, S.h, S.w, S.c, L.kernel, L.stride, L.pad, L.h, L.w};
 }
 
+// ---- per-operation event timing ----
+void prof_mark(sg_net* n, int slot, int end, cudaStream_t st) {
+  if (!n->prof) return;
+  cudaEvent_t e = n->pev[2 * slot + end];
+  if (n->capturing)
+    cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, st);
+  n->pused[slot] = 1;
+}
+
 // ---- ComputeFeature ----
+sg_status forward_impl(sg_net* n, int i);
 sg_status forward(sg_net* n, int i) {
+  prof_mark(n, 4 * i, 0, n->cs);
+  SG_TRY(forward_impl(n, i));
+  prof_mark(n, 4 * i, 1, n->cs);
+  return SG_OK;
+}
+sg_status forward_impl(sg_net* n, int i) {
   const Plan& P = PL(n);
   const LayerPlan& L = P.layers[i];
   cudaStream_t st = n->cs;
@@ -213,11 +237,18 @@ sg_status backward(sg_net* n, int i) {
   float* W = L.pW >= 0 ? n->sw[L.store] + P.params[L.pW].store_off : nullptr;
   float* dW = L.pW >= 0 ? n->sgr[L.store] + P.params[L.pW].store_off : nullptr;
   float* db = L.pb >= 0 ? n->sgr[L.store] + P.params[L.pb].store_off : nullptr;
+  const int s1 = 4 * i + 1, s2 = 4 * i + 2;
+  prof_mark(n, s1, 0, st);
   switch (L.kind) {
     case SG_CONV:
       SG_LCH(conv_wgrad(conv_shape(L, S), n->data[L.src], n->grad[i], dW, db, n->ws, st));
-      if (need_dx) SG_LCH(conv_dgrad(conv_shape(L, S), n->grad[i], W, n->grad[L.src], n->ws, st));
-      break;
+      prof_mark(n, s1, 1, st);
+      if (need_dx) {
+        prof_mark(n, s2, 0, st);
+        SG_LCH(conv_dgrad(conv_shape(L, S), n->grad[i], W, n->grad[L.src], n->ws, st));
+        prof_mark(n, s2, 1, st);
+      }
+      return SG_OK;
     case SG_POOL_MAX:
       if (need_dx) SG_LCH(maxpool_bwd(pool_shape(L, S), n->grad[i], n->mask[i], n->grad[L.src], st));
       break;
@@ -238,8 +269,13 @@ sg_status backward(sg_net* n, int i) {
     case SG_INNER_PRODUCT: {
       View2D dy = plain(n->grad[i], (int)L.rows, (int)L.nout, L.ld);
       SG_LCH(ip_wgrad(feat_view(S, n->data[L.src], L.kin), dy, (int)L.kin, (int)L.nout, dW, db, n->ws, st));
-      if (need_dx) SG_LCH(ip_dgrad(dy, W, (int)L.kin, (int)L.nout, feat_view(S, n->grad[L.src], L.kin), n->ws, st));
-      break;
+      prof_mark(n, s1, 1, st);
+      if (need_dx) {
+        prof_mark(n, s2, 0, st);
+        SG_LCH(ip_dgrad(dy, W, (int)L.kin, (int)L.nout, feat_view(S, n->grad[L.src], L.kin), n->ws, st));
+        prof_mark(n, s2, 1, st);
+      }
+      return SG_OK;
     }
     case SG_CONCAT:
       SG_NCCL(ncclReduceScatter(n->grad[i], n->grad[L.src], (size_t)(S.rows * S.ld), ncclFloat, ncclSum,
@@ -256,6 +292,7 @@ sg_status backward(sg_net* n, int i) {
       break;
     }
   }
+  prof_mark(n, s1, 1, st);
   return SG_OK;
 }
 
@@ -267,6 +304,7 @@ sg_status update(sg_net* n, sg_updater* u, int i) {
   const StorePlan& S = P.stores[L.store];
   SG_CUDA(cudaEventRecord(n->ev_grad[i], n->cs));
   SG_CUDA(cudaStreamWaitEvent(n->ps, n->ev_grad[i], 0));
+  prof_mark(n, 4 * i + 3, 0, n->ps);
   const float mu = u->cfg.momentum, wd = u->cfg.weight_decay * L.wd_scale;
   if (S.sharded) {
     const int64_t shard = S.padded / P.world;
@@ -280,6 +318,7 @@ sg_status update(sg_net* n, sg_updater* u, int i) {
     SG_LCH(sgd_momentum_dev(n->sw[L.store], n->sgr[L.store], n->sv[L.store], S.padded, n->lr_dev, L.lr_scale, mu, wd,
                             u->s, n->ps));
   }
+  prof_mark(n, 4 * i + 3, 1, n->ps);
   SG_CUDA(cudaEventRecord(n->ev_upd[i], n->ps));
   n->upd_pending[i] = 1;
   return SG_OK;
@@ -472,6 +511,7 @@ sg_status destroy_net(sg_net* n) {
   for (auto e : n->ev_upd) cudaEventDestroy(e);
   for (auto e : {n->ev_in, n->ev_out, n->ev_fork, n->ev_join})
     if (e) cudaEventDestroy(e);
+  for (auto e : n->pev) cudaEventDestroy(e);
   if (n->cs) cudaStreamDestroy(n->cs);
   if (n->ps) cudaStreamDestroy(n->ps);
   delete n;
@@ -772,7 +812,9 @@ SG_API sg_status sg_train_one_batch(sg_net* n, sg_updater* u, int64_t step, cons
       cudaGraph_t g;
       long long c0 = g_kernel_launches;
       SG_CUDA(cudaStreamBeginCapture(n->cs, cudaStreamCaptureModeThreadLocal));
+      n->capturing = true;
       sg_status st = step_body(n, u);
+      n->capturing = false;
       cudaError_t ce = cudaStreamEndCapture(n->cs, &g);
       SG_TRY(st);
       SG_CHECK(ce == cudaSuccess, SG_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
@@ -836,6 +878,56 @@ SG_API sg_status sg_net_enable_graph(sg_net* n, int32_t enable) {
     cudaStreamSynchronize(n->cs);
     cudaGraphExecDestroy(n->gexec);
     n->gexec = nullptr;
+  }
+  return SG_OK;
+}
+
+SG_API sg_status sg_net_profile(sg_net* n, int32_t enable) {
+  SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  const int slots = 4 * (int)PL(n).layers.size();
+  if (enable && n->pev.empty()) {
+    n->pev.resize(2 * slots);
+    for (auto& e : n->pev) SG_CUDA(cudaEventCreate(&e));
+    n->pused.assign(slots, 0);
+    n->pacc.assign(slots, 0.0);
+    n->pcnt.assign(slots, 0);
+  }
+  n->prof = enable != 0;
+  if (n->gexec) {  // re-capture with / without the timing events
+    SG_CUDA(cudaStreamSynchronize(n->cs));
+    cudaGraphExecDestroy(n->gexec);
+    n->gexec = nullptr;
+  }
+  return SG_OK;
+}
+
+SG_API sg_status sg_net_op_times(sg_net* n, double* ms, int64_t* counts, int32_t cap, int32_t* nslots,
+                                 int32_t reset) {
+  SG_CHECK(n && nslots, SG_ERR_INVALID_ARG, "null argument");
+  const int slots = 4 * (int)PL(n).layers.size();
+  *nslots = slots;
+  if (n->pev.empty()) return SG_OK;
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  SG_CUDA(cudaStreamSynchronize(n->ps));
+  SG_CUDA(cudaStreamSynchronize(n->cs));
+  for (int s = 0; s < slots; ++s) {
+    if (!n->pused[s]) continue;
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, n->pev[2 * s], n->pev[2 * s + 1]) == cudaSuccess) {
+      n->pacc[s] += t;
+      n->pcnt[s] += 1;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  for (int s = 0; s < slots && s < cap; ++s) {
+    if (ms) ms[s] = n->pacc[s];
+    if (counts) counts[s] = n->pcnt[s];
+  }
+  if (reset) {
+    std::fill(n->pacc.begin(), n->pacc.end(), 0.0);
+    std::fill(n->pcnt.begin(), n->pcnt.end(), 0);
   }
   return SG_OK;
 }

@@ -6,9 +6,9 @@
 //
 // One CTA computes a 128 x BN output tile (optionally one K-split of it):
 //   warps 0-3 : producers — gather 16-byte chunks with cp.async (zero-filled
-//               outside the operand) straight into the UMMA SWIZZLE_128B
-//               canonical layout, one stage of BK = 32 fp32 (128 B) per step;
-//               then the epilogue (TMEM -> registers -> global).
+//               outside the operand) straight into the UMMA canonical layouts,
+//               one stage of BK = 32 fp32 (128 B) per step; then the epilogue
+//               (TMEM -> registers -> global).
 //   warp 4    : TMEM allocation and the single MMA-issuing thread.
 // Operands are "loaders": each maps a (row, k) of the GEMM onto the layer's
 // native tensor (NHWC activations, KRSC / [d_v][d_h] weights), so the im2col
@@ -17,6 +17,15 @@
 // contiguous); tcgen05 kind::tf32 accepts both from shared memory
 // (instruction-descriptor bits 15/16); MN-major tf32 must use the
 // SWIZZLE_128B_BASE32B layout (32-byte swizzle granules, 4-line atoms).
+//
+// Every producer thread handles fixed tile rows (K-major) or a fixed MN chunk
+// (MN-major) for the whole K loop, so per-row / per-column address bases are
+// computed once (loader State) and a stage costs a few integer ops per chunk;
+// the remaining divisions use multiply-shift FastDiv.
+//
+// Bias gradients are fused into the weight-gradient GEMMs: the A operand gets
+// one extra "ones" row (index `ones_row`), whose output row is sum_k B(n, k) =
+// column sums of dy, routed by the epilogue to the bias-gradient buffer.
 #pragma once
 #include "sg_common.cuh"
 
@@ -26,6 +35,32 @@ constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 32;  // fp32 elements = 128 bytes = one swizzle row
 constexpr int GEMM_THREADS = 160;
 
+// {1, 0, 0, 0}: source of the ones-row chunk (global memory, cp.async source).
+__device__ __align__(16) static const float g_one4[4] = {1.f, 0.f, 0.f, 0.f};
+
+// Unsigned division by a runtime constant via multiply-high (n < 2^31).
+struct FastDiv {
+  int d;
+  uint32_t mul, shr;
+  __device__ __forceinline__ int div(int n) const {
+    return (int)((__umulhi((uint32_t)n, mul) + (uint32_t)n) >> shr);
+  }
+};
+inline FastDiv make_fastdiv(int d) {
+  FastDiv f;
+  f.d = d < 1 ? 1 : d;
+  if (f.d == 1) {
+    f.mul = 0;
+    f.shr = 0;
+    return f;
+  }
+  uint32_t l = 0;
+  while ((1ull << l) < (unsigned long long)f.d) ++l;
+  f.mul = (uint32_t)(((1ull << 32) * ((1ull << l) - (unsigned long long)f.d)) / (unsigned long long)f.d + 1);
+  f.shr = l;
+  return f;
+}
+
 // ---------------------------------------------------------------------------
 // Blocked row-major matrix view: element (i, j) at p[(j / cb) * bs + i * ld + j % cb].
 // cb >= cols means a plain row-major matrix.  Column blocking is how a tensor
@@ -34,40 +69,91 @@ struct MatView {
   const float* p;
   long long ld, bs;
   int cb, rows, cols;
-  __device__ __forceinline__ const float* at(int i, int j) const {
-    if (cb >= cols) return p + (long long)i * ld + j;
-    int blk = j / cb;
-    return p + (long long)blk * bs + (long long)i * ld + (j - blk * cb);
+  FastDiv fcb;  // divides by cb (blocked views)
+  __device__ __forceinline__ long long col_off(int j) const {
+    if (cb >= cols) return j;
+    int blk = fcb.div(j);
+    return (long long)blk * bs + (j - blk * cb);
   }
 };
 
+// Thread -> chunk mapping of one stage (see load_stage):
+//   K-major tile of T rows: thread t covers k-chunk (t & 7) of rows (t >> 3) + 16 i, i < T/16.
+//   MN-major tile of T rows: thread t covers row chunk (t % (T/4)) * 4 of k-lines
+//   t / (T/4) + (512/T) i, i < T/16.
+template <int T>
+struct MNMap {
+  static constexpr int CPR = T / 4;
+  static constexpr int KSTEP = 128 / CPR;
+  static __device__ __forceinline__ int mn(int tid) { return (tid % CPR) * 4; }
+  static __device__ __forceinline__ int kr(int tid, int i) { return tid / CPR + KSTEP * i; }
+};
+
+// ---------------------------------------------------------------- loaders --
 // K-major dense operand: op(r, k) = M(r, k).
 struct LdDenseK {
   static constexpr int kMN = 0;
   MatView m;
-  __device__ __forceinline__ const float* src(int r, int k, int& nbytes) const {
-    if (r < m.rows && k < m.cols) {
-      int nv = m.cols - k;
-      nbytes = (nv >= 4 ? 4 : nv) * 4;
-      return m.at(r, k);
+  template <int T>
+  struct State {
+    const float* base[T / 16];
+  };
+  template <int T>
+  __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
+#pragma unroll
+    for (int i = 0; i < T / 16; ++i) {
+      int r = row0 + (tid >> 3) + 16 * i;
+      s.base[i] = r < m.rows ? m.p + (long long)r * m.ld : nullptr;
     }
-    nbytes = 0;
-    return m.p;
+  }
+  template <int T>
+  __device__ __forceinline__ const float* src(const State<T>& s, int i, int k, int& nb) const {
+    // k is a multiple of 4; column blocks are multiples of 4 wide
+    if (!s.base[i] || k >= m.cols) {
+      nb = 0;
+      return m.p;
+    }
+    int nv = m.cols - k;
+    nb = (nv >= 4 ? 4 : nv) * 4;
+    return s.base[i] + m.col_off(k);
   }
 };
 
-// MN-major dense operand: op(r, k) = M(k, r)  (4 consecutive r contiguous).
+// MN-major dense operand: op(r, k) = M(k, r) (4 consecutive r contiguous).
+// ones_row >= 0 (a multiple of 4): rows ones_row.. read {1, 0, 0, 0}.
 struct LdDenseMN {
   static constexpr int kMN = 1;
   MatView m;
-  __device__ __forceinline__ const float* src(int r, int k, int& nbytes) const {
-    if (k < m.rows && r < m.cols) {
+  int ones_row;
+  template <int T>
+  struct State {
+    long long coff;
+    int nb;  // bytes of this thread's row chunk (0 = outside)
+    bool ones;
+  };
+  template <int T>
+  __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
+    int r = row0 + MNMap<T>::mn(tid);
+    s.ones = (r == ones_row);
+    s.nb = 0;
+    s.coff = 0;
+    if (r < m.cols) {
       int nv = m.cols - r;
-      nbytes = (nv >= 4 ? 4 : nv) * 4;
-      return m.at(k, r);
+      s.nb = (nv >= 4 ? 4 : nv) * 4;
+      s.coff = m.col_off(r);
+    } else if (s.ones) {
+      s.nb = 16;
     }
-    nbytes = 0;
-    return m.p;
+  }
+  template <int T>
+  __device__ __forceinline__ const float* src(const State<T>& s, int k, int& nb) const {
+    if (k >= m.rows || s.nb == 0) {
+      nb = 0;
+      return m.p;
+    }
+    nb = s.nb;
+    if (s.ones) return g_one4;
+    return m.p + (long long)k * m.ld + s.coff;
   }
 };
 
@@ -75,52 +161,130 @@ struct ConvGeom {
   int N, H, W, C;       // input (C multiple of 4)
   int Co, R, S;         // filter
   int Ho, Wo, st, pad;  // output
+  FastDiv fC, fS, fCo, fHoWo, fWo, fHW, fW;
 };
 
-// Convolution forward, A(m, k): m = (n, oh, ow), k = (r, s, c) ; x NHWC.
+// Convolution forward, A(m, k): m = (n, oh, ow), k = (r, s, c); x NHWC.
 struct LdConvFwdA {
   static constexpr int kMN = 0;
   const float* x;
   ConvGeom g;
-  __device__ __forceinline__ const float* src(int m, int k, int& nbytes) const {
-    nbytes = 0;
-    int HoWo = g.Ho * g.Wo;
-    if (m >= g.N * HoWo || k >= g.R * g.S * g.C) return x;
-    int n = m / HoWo, rem = m - n * HoWo;
-    int oh = rem / g.Wo, ow = rem - oh * g.Wo;
-    int rs = k / g.C, c = k - rs * g.C;
-    int r = rs / g.S, s = rs - r * g.S;
-    int h = oh * g.st - g.pad + r, w = ow * g.st - g.pad + s;
-    if ((unsigned)h >= (unsigned)g.H || (unsigned)w >= (unsigned)g.W) return x;
-    nbytes = 16;
-    return x + (((long long)n * g.H + h) * g.W + w) * g.C + c;
+  template <int T>
+  struct State {
+    const float* base[T / 16];  // x at (n, oh*st - p, ow*st - p, 0) (may point outside x)
+    int h0[T / 16], w0[T / 16];
+  };
+  template <int T>
+  __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
+    const int Mtot = g.N * g.Ho * g.Wo;
+#pragma unroll
+    for (int i = 0; i < T / 16; ++i) {
+      int m = row0 + (tid >> 3) + 16 * i;
+      if (m < Mtot) {
+        int n = g.fHoWo.div(m), rem = m - n * g.Ho * g.Wo;
+        int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
+        s.h0[i] = oh * g.st - g.pad;
+        s.w0[i] = ow * g.st - g.pad;
+        s.base[i] = x + (((long long)n * g.H + s.h0[i]) * g.W + s.w0[i]) * g.C;
+      } else {
+        s.h0[i] = -(1 << 28);
+        s.w0[i] = 0;
+        s.base[i] = x;
+      }
+    }
+  }
+  // per-stage tap of this thread's k chunk
+  struct Tap {
+    int r, s;
+    long long off;
+    bool ok;
+  };
+  __device__ __forceinline__ Tap tap(int k) const {
+    Tap t;
+    t.ok = k < g.R * g.S * g.C;
+    int rs = g.fC.div(k), c = k - rs * g.C;
+    t.r = g.fS.div(rs);
+    t.s = rs - t.r * g.S;
+    t.off = ((long long)t.r * g.W + t.s) * g.C + c;
+    return t;
+  }
+  template <int T>
+  __device__ __forceinline__ const float* src(const State<T>& s, int i, const Tap& t, int& nb) const {
+    int h = s.h0[i] + t.r, w = s.w0[i] + t.s;
+    if (t.ok && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W) {
+      nb = 16;
+      return s.base[i] + t.off;
+    }
+    nb = 0;
+    return x;
   }
 };
 
 // Convolution data gradient, A(m, k): m = (n, h, w) over the input,
-// k = (r, s, co);  value dy[n][(h+p-r)/st][(w+p-s)/st][co] when integral & in range.
+// k = (r, s, co); value dy[n][(h+p-r)/st][(w+p-s)/st][co] when integral & in range.
 struct LdConvDgradA {
   static constexpr int kMN = 0;
   const float* dy;
   ConvGeom g;
-  __device__ __forceinline__ const float* src(int m, int k, int& nbytes) const {
-    nbytes = 0;
-    int HW = g.H * g.W;
-    if (m >= g.N * HW || k >= g.R * g.S * g.Co) return dy;
-    int n = m / HW, rem = m - n * HW;
-    int h = rem / g.W, w = rem - h * g.W;
-    int rs = k / g.Co, co = k - rs * g.Co;
-    int r = rs / g.S, s = rs - r * g.S;
-    int oh = h + g.pad - r, ow = w + g.pad - s;
-    if (oh < 0 || ow < 0) return dy;
-    if (g.st > 1) {
-      if (oh % g.st || ow % g.st) return dy;
-      oh /= g.st;
-      ow /= g.st;
+  template <int T>
+  struct State {
+    const float* base[T / 16];  // stride 1: dy at (n, h+p, w+p, 0)
+    int hp[T / 16], wp[T / 16], n[T / 16];
+  };
+  template <int T>
+  __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
+    const int Mtot = g.N * g.H * g.W;
+#pragma unroll
+    for (int i = 0; i < T / 16; ++i) {
+      int m = row0 + (tid >> 3) + 16 * i;
+      if (m < Mtot) {
+        int n = g.fHW.div(m), rem = m - n * g.H * g.W;
+        int h = g.fW.div(rem), w = rem - h * g.W;
+        s.hp[i] = h + g.pad;
+        s.wp[i] = w + g.pad;
+        s.n[i] = n;
+        s.base[i] = dy + (((long long)n * g.Ho + s.hp[i]) * g.Wo + s.wp[i]) * g.Co;
+      } else {
+        s.hp[i] = -(1 << 28);
+        s.wp[i] = 0;
+        s.n[i] = 0;
+        s.base[i] = dy;
+      }
     }
+  }
+  struct Tap {
+    int r, s, co;
+    long long off;
+    bool ok;
+  };
+  __device__ __forceinline__ Tap tap(int k) const {
+    Tap t;
+    t.ok = k < g.R * g.S * g.Co;
+    int rs = g.fCo.div(k);
+    t.co = k - rs * g.Co;
+    t.r = g.fS.div(rs);
+    t.s = rs - t.r * g.S;
+    t.off = -((long long)t.r * g.Wo + t.s) * g.Co + t.co;
+    return t;
+  }
+  template <int T>
+  __device__ __forceinline__ const float* src(const State<T>& s, int i, const Tap& t, int& nb) const {
+    nb = 0;
+    if (!t.ok) return dy;
+    int oh = s.hp[i] - t.r, ow = s.wp[i] - t.s;
+    if (g.st == 1) {
+      if ((unsigned)oh < (unsigned)g.Ho && (unsigned)ow < (unsigned)g.Wo) {
+        nb = 16;
+        return s.base[i] + t.off;
+      }
+      return dy;
+    }
+    if (oh < 0 || ow < 0 || oh % g.st || ow % g.st) return dy;
+    oh /= g.st;
+    ow /= g.st;
     if (oh >= g.Ho || ow >= g.Wo) return dy;
-    nbytes = 16;
-    return dy + (((long long)n * g.Ho + oh) * g.Wo + ow) * g.Co + co;
+    nb = 16;
+    return dy + (((long long)s.n[i] * g.Ho + oh) * g.Wo + ow) * g.Co + t.co;
   }
 };
 
@@ -129,40 +293,92 @@ struct LdConvDgradB {
   static constexpr int kMN = 1;
   const float* Wt;
   ConvGeom g;
-  __device__ __forceinline__ const float* src(int c, int k, int& nbytes) const {
-    nbytes = 0;
-    if (c >= g.C || k >= g.R * g.S * g.Co) return Wt;
-    int rs = k / g.Co, co = k - rs * g.Co;
-    nbytes = 16;
-    return Wt + ((long long)co * g.R * g.S + rs) * g.C + c;
+  template <int T>
+  struct State {
+    int c;
+  };
+  template <int T>
+  __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
+    s.c = row0 + MNMap<T>::mn(tid);
+  }
+  template <int T>
+  __device__ __forceinline__ const float* src(const State<T>& s, int k, int& nb) const {
+    nb = 0;
+    if (s.c >= g.C || k >= g.R * g.S * g.Co) return Wt;
+    int rs = g.fCo.div(k), co = k - rs * g.Co;
+    nb = 16;
+    return Wt + ((long long)co * g.R * g.S + rs) * g.C + s.c;
   }
 };
 
 // Convolution weight gradient, A(kg, m) = x[n][oh*st-p+r][ow*st-p+s][c] with
 // kg = (r, s, c) the GEMM row and m = (n, oh, ow) the reduction index; MN-major.
+// Row ones_row (= R*S*C) is the ones row of the fused bias gradient.
 struct LdConvWgradA {
   static constexpr int kMN = 1;
   const float* x;
   ConvGeom g;
-  __device__ __forceinline__ const float* src(int kg, int m, int& nbytes) const {
-    nbytes = 0;
-    int HoWo = g.Ho * g.Wo;
-    if (kg >= g.R * g.S * g.C || m >= g.N * HoWo) return x;
-    int n = m / HoWo, rem = m - n * HoWo;
-    int oh = rem / g.Wo, ow = rem - oh * g.Wo;
-    int rs = kg / g.C, c = kg - rs * g.C;
-    int r = rs / g.S, s = rs - r * g.S;
-    int h = oh * g.st - g.pad + r, w = ow * g.st - g.pad + s;
-    if ((unsigned)h >= (unsigned)g.H || (unsigned)w >= (unsigned)g.W) return x;
-    nbytes = 16;
-    return x + (((long long)n * g.H + h) * g.W + w) * g.C + c;
+  int ones_row;
+  template <int T>
+  struct State {
+    int r, s;
+    long long off;  // (r*W + s)*C + c
+    int mode;       // 0 outside, 1 data, 2 ones
+  };
+  template <int T>
+  __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
+    int kg = row0 + MNMap<T>::mn(tid);
+    s.mode = 0;
+    s.r = s.s = 0;
+    s.off = 0;
+    if (kg < g.R * g.S * g.C) {
+      int rs = g.fC.div(kg), c = kg - rs * g.C;
+      s.r = g.fS.div(rs);
+      s.s = rs - s.r * g.S;
+      s.off = ((long long)s.r * g.W + s.s) * g.C + c;
+      s.mode = 1;
+    } else if (kg == ones_row) {
+      s.mode = 2;
+    }
   }
+  template <int T>
+  __device__ __forceinline__ const float* src(const State<T>& s, int m, int& nb) const {
+    nb = 0;
+    if (s.mode == 0 || m >= g.N * g.Ho * g.Wo) return x;
+    if (s.mode == 2) {
+      nb = 16;
+      return g_one4;
+    }
+    int n = g.fHoWo.div(m), rem = m - n * g.Ho * g.Wo;
+    int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
+    int h0 = oh * g.st - g.pad, w0 = ow * g.st - g.pad;
+    int h = h0 + s.r, w = w0 + s.s;
+    if ((unsigned)h >= (unsigned)g.H || (unsigned)w >= (unsigned)g.W) return x;
+    nb = 16;
+    return x + (((long long)n * g.H + h0) * g.W + w0) * g.C + s.off;
+  }
+};
+
+// Loaders whose K-major chunk address depends on a per-stage "tap" (filter offset).
+template <class L>
+struct requires_tap {
+  static constexpr bool value = false;
+};
+template <>
+struct requires_tap<LdConvFwdA> {
+  static constexpr bool value = true;
+};
+template <>
+struct requires_tap<LdConvDgradA> {
+  static constexpr bool value = true;
 };
 
 // ---------------------------------------------------------------------------
 // Epilogue parameters.  Output element (m, n) goes to out(m, n) (trans = 0) or
-// out(n, m) (trans = 1) of a blocked row-major view; with ws != nullptr the
-// CTA writes its raw K-split partial to ws[split][m][n] (ld = ws_ld) instead.
+// out(n, m) (trans = 1) of a blocked row-major view for m < mvalid; row
+// m == xrow goes to xout[n] (fused bias gradient); other rows are dropped.
+// With ws != nullptr the CTA writes its raw K-split partial to
+// ws[split][m][n] (ld = ws_ld) instead.
 struct EpiArgs {
   float* p;
   long long ld, bs;
@@ -170,6 +386,8 @@ struct EpiArgs {
   const float* bias;  // indexed by n (bias_on_m = 0) or by m
   int bias_on_m;
   int relu;
+  int mvalid, xrow;
+  float* xout;
   float* ws;
   long long ws_ld, ws_split_stride;
 };
@@ -190,33 +408,43 @@ struct GemmArgs {
 };
 
 // ---------------------------------------------------------------------------
-// Producer: write one operand tile (T rows x BK) of one stage.
+// Producer: one stage of an operand tile (T rows x BK) into shared memory.
 template <int T, class LD>
-__device__ __forceinline__ void load_tile(const LD& ld, uint32_t sm, int row0, int k0, int tid) {
+__device__ __forceinline__ void load_stage(const LD& ld, const typename LD::template State<T>& st, uint32_t sm,
+                                           int k0, int tid) {
   if constexpr (LD::kMN == 0) {
-    // K-major: row r at r*128 B (8-row groups of 1024 B), 16-byte chunk c stored at c ^ (r & 7).
+    // K-major SWIZZLE_128B: row r at (r >> 3) * 1024 + (r & 7) * 128, chunk c at c ^ (r & 7).
+    const int kc = tid & 7, r7 = (tid >> 3) & 7;
+    const uint32_t d0 = sm + ((tid >> 6) << 10) + (r7 << 7) + ((kc ^ r7) << 4);
+    const int k = k0 + kc * 4;
+    if constexpr (requires_tap<LD>::value) {
+      const auto t = ld.tap(k);
 #pragma unroll
-    for (int i = 0; i < T / 16; ++i) {
-      int q = tid + 128 * i;
-      int r = q >> 3, kc = q & 7;
-      int nb;
-      const float* g = ld.src(row0 + r, k0 + kc * 4, nb);
-      cp_async16(sm + (r >> 3) * 1024 + (r & 7) * 128 + ((kc ^ (r & 7)) << 4), g, nb);
+      for (int i = 0; i < T / 16; ++i) {
+        int nb;
+        const float* g = ld.src(st, i, t, nb);
+        cp_async16(d0 + i * 2048, g, nb);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < T / 16; ++i) {
+        int nb;
+        const float* g = ld.template src<T>(st, i, k, nb);
+        cp_async16(d0 + i * 2048, g, nb);
+      }
     }
   } else {
-    // MN-major (tf32 requires SWIZZLE_128B_BASE32B): 32 consecutive rows (128 B) per
-    // k-line; k-line kr of MN-atom a at a*(BK*128) + kr*128; within the line the
-    // 32-byte granule g sits at g ^ (kr & 3).  LBO = BK*128 (atom stride), SBO = 512
-    // (4 k-lines).
-    constexpr int CPR = T / 4;
+    // MN-major SWIZZLE_128B_BASE32B: k-line kr of MN-atom a at a*(BK*128) + kr*128;
+    // within the line the 32-byte granule g sits at g ^ (kr & 3).  LBO = BK*128, SBO = 512.
+    const int mn = MNMap<T>::mn(tid);
+    const uint32_t dmn = sm + (mn >> 5) * (GEMM_BK * 128) + ((mn & 4) << 2);
+    const int g32 = (mn & 31) >> 3;
 #pragma unroll
     for (int i = 0; i < T / 16; ++i) {
-      int q = tid + 128 * i;
-      int kr = q / CPR, mn = (q % CPR) * 4;
+      const int kr = MNMap<T>::kr(tid, i);
       int nb;
-      const float* g = ld.src(row0 + mn, k0 + kr, nb);
-      cp_async16(sm + (mn >> 5) * (GEMM_BK * 128) + kr * 128 + ((((mn & 31) >> 3) ^ (kr & 3)) << 5) + ((mn & 4) << 2),
-                 g, nb);
+      const float* g = ld.template src<T>(st, k0 + kr, nb);
+      cp_async16(dmn + kr * 128 + ((g32 ^ (kr & 3)) << 5), g, nb);
     }
   }
 }
@@ -278,14 +506,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
 
   if (warp < 4) {
     // ------------------------------ producers ------------------------------
+    typename LA::template State<GEMM_BM> sa_st;
+    typename LB::template State<BN> sb_st;
+    args.a.template init<GEMM_BM>(sa_st, m0, tid);
+    args.b.template init<BN>(sb_st, n0, tid);
     for (int it = 0; it < nkb; ++it) {
       const int s = it % STAGES;
       const int round = it / STAGES;
       if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
       const uint32_t sa = sbase + s * STAGE_BYTES;
       const int k0 = (kb_begin + it) * GEMM_BK;
-      load_tile<GEMM_BM>(args.a, sa, m0, k0, tid);
-      load_tile<BN>(args.b, sa + A_BYTES, n0, k0, tid);
+      load_stage<GEMM_BM>(args.a, sa_st, sa, k0, tid);
+      load_stage<BN>(args.b, sb_st, sa + A_BYTES, k0, tid);
       cp_async_commit();
       if (it >= LAG) {
         // this thread's copies for k-block it-LAG have landed: make them visible
@@ -324,6 +556,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
     const int row = m0 + warp * 32 + (tid & 31);
     const EpiArgs& e = args.epi;
     const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
+    const bool plain_vec = !e.trans && e.cb >= args.N && (e.ld & 3) == 0 && !e.bias_on_m;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
       if (n0 + c0 >= args.N) break;
@@ -348,6 +581,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
         }
         continue;
       }
+      if (row >= e.mvalid) {
+        if (row == e.xrow) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (n0 + c0 + i < args.N) e.xout[n0 + c0 + i] = v[i];
+        }
+        continue;
+      }
+      if (plain_vec && n0 + c0 + 15 < args.N) {
+        float* dst = e.p + (long long)row * e.ld + n0 + c0;
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          if (e.bias) {
+            o.x += e.bias[n0 + c0 + i];
+            o.y += e.bias[n0 + c0 + i + 1];
+            o.z += e.bias[n0 + c0 + i + 2];
+            o.w += e.bias[n0 + c0 + i + 3];
+          }
+          if (e.relu) {
+            o.x = fmaxf(o.x, 0.f);
+            o.y = fmaxf(o.y, 0.f);
+            o.z = fmaxf(o.z, 0.f);
+            o.w = fmaxf(o.w, 0.f);
+          }
+          *reinterpret_cast<float4*>(dst + i) = o;
+        }
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int col = n0 + c0 + i;
@@ -356,7 +618,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
         if (e.bias) o += e.bias_on_m ? e.bias[row] : e.bias[col];
         if (e.relu) o = fmaxf(o, 0.f);
         if (e.trans)
-          *out_at(e, col, row, args.M) = o;
+          *out_at(e, col, row, e.mvalid) = o;
         else
           *out_at(e, row, col, args.N) = o;
       }

@@ -636,6 +636,36 @@ SG_API sg_status sg_cluster_create(const sg_cluster_cfg* cfg, sg_cluster** out) 
       delete c;
       SG_FAIL(SG_ERR_NCCL, "NCCL communicator creation failed: %s", ncclGetErrorString(r));
     }
+    // Establish every connection now (one of each collective kind on both
+    // communicators, serialised), so no lazy connection setup can happen while
+    // kernels of the other communicator are in flight during a step.
+    float* buf = nullptr;
+    const size_t cnt = 1024;
+    cudaError_t ce = cudaMalloc(&buf, 2 * cnt * c->world * sizeof(float));
+    if (ce != cudaSuccess) {
+      delete c;
+      SG_FAIL(SG_ERR_OOM, "cluster warm-up buffer: %s", cudaGetErrorString(ce));
+    }
+    cudaMemset(buf, 0, 2 * cnt * c->world * sizeof(float));
+    for (ncclComm_t comm : {c->comm_act, c->comm_par}) {
+      if (r == ncclSuccess) r = ncclAllReduce(buf, buf, cnt, ncclFloat, ncclSum, comm, 0);
+      if (r == ncclSuccess) r = ncclAllGather(buf, buf + cnt * c->world, cnt, ncclFloat, comm, 0);
+      if (r == ncclSuccess) r = ncclReduceScatter(buf + cnt * c->world, buf, cnt, ncclFloat, ncclSum, comm, 0);
+      if (r == ncclSuccess) {
+        r = ncclGroupStart();
+        for (int j = 0; j < c->world && r == ncclSuccess; ++j) {
+          r = ncclSend(buf + j * cnt, cnt, ncclFloat, j, comm, 0);
+          if (r == ncclSuccess) r = ncclRecv(buf + cnt * c->world + j * cnt, cnt, ncclFloat, j, comm, 0);
+        }
+        ncclResult_t r2 = ncclGroupEnd();
+        if (r == ncclSuccess) r = r2;
+      }
+      if (cudaDeviceSynchronize() != cudaSuccess && r == ncclSuccess) r = ncclUnhandledCudaError;
+    }
+    cudaFree(buf);
+    if (r != ncclSuccess) {
+      SG_FAIL(SG_ERR_NCCL, "NCCL warm-up failed: %s", ncclGetErrorString(r));
+    }
   }
   *out = c;
   return SG_OK;

@@ -5,11 +5,12 @@
 //   D[m][n] = sum_k A(m, k) * B(n, k)      fp32 storage, TF32 operands, fp32 accumulate
 //
 // One CTA computes a 128 x BN output tile (optionally one K-split of it):
-//   warps 0-3 : producers — gather 16-byte chunks with cp.async (zero-filled
+//   warps 0-7 : producers — gather 16-byte chunks with cp.async (zero-filled
 //               outside the operand) straight into the UMMA canonical layouts,
 //               one stage of BK = 32 fp32 (128 B) per step; then the epilogue
-//               (TMEM -> registers -> global).
-//   warp 4    : TMEM allocation and the single MMA-issuing thread.
+//               (TMEM -> registers -> global; warp w reads TMEM lanes
+//               32*(w%4).. and column half w/4).
+//   warp 8    : TMEM allocation and the single MMA-issuing thread.
 // Operands are "loaders": each maps a (row, k) of the GEMM onto the layer's
 // native tensor (NHWC activations, KRSC / [d_v][d_h] weights), so the im2col
 // of the convolution is never materialised.  A loader is K-major (4
@@ -18,22 +19,26 @@
 // (instruction-descriptor bits 15/16); MN-major tf32 must use the
 // SWIZZLE_128B_BASE32B layout (32-byte swizzle granules, 4-line atoms).
 //
-// Every producer thread handles fixed tile rows (K-major) or a fixed MN chunk
-// (MN-major) for the whole K loop, so per-row / per-column address bases are
-// computed once (loader State) and a stage costs a few integer ops per chunk;
-// the remaining divisions use multiply-shift FastDiv.
+// Producer threads own fixed tile rows (K-major) or a fixed MN chunk
+// (MN-major) for the whole K loop, so address bases are computed once (loader
+// State); per stage a chunk costs a handful of integer ops.  In the weight
+// gradient the K index is the output pixel: each warp decomposes its 4 pixels
+// of the stage once (lanes 0-3) and broadcasts them with shuffles.
 //
 // Bias gradients are fused into the weight-gradient GEMMs: the A operand gets
 // one extra "ones" row (index `ones_row`), whose output row is sum_k B(n, k) =
 // column sums of dy, routed by the epilogue to the bias-gradient buffer.
 #pragma once
+#include <cuda.h>
+
 #include "sg_common.cuh"
 
 namespace sg {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 32;  // fp32 elements = 128 bytes = one swizzle row
-constexpr int GEMM_THREADS = 160;
+constexpr int GEMM_PRODUCERS = 256;
+constexpr int GEMM_THREADS = GEMM_PRODUCERS + 32;
 
 // {1, 0, 0, 0}: source of the ones-row chunk (global memory, cp.async source).
 __device__ __align__(16) static const float g_one4[4] = {1.f, 0.f, 0.f, 0.f};
@@ -77,83 +82,99 @@ struct MatView {
   }
 };
 
-// Thread -> chunk mapping of one stage (see load_stage):
-//   K-major tile of T rows: thread t covers k-chunk (t & 7) of rows (t >> 3) + 16 i, i < T/16.
-//   MN-major tile of T rows: thread t covers row chunk (t % (T/4)) * 4 of k-lines
-//   t / (T/4) + (512/T) i, i < T/16.
+// Chunk placement of one stage (T tile rows x BK).
+//   K-major (SWIZZLE_128B): thread t covers k-chunk (t & 7) of rows (t >> 3) + 32 i,
+//     i < T/32; row r at (r >> 3) * 1024 + (r & 7) * 128, chunk c at c ^ (r & 7).
+//   MN-major (SWIZZLE_128B_BASE32B): thread t covers row chunk (t % (T/4)) * 4 of
+//     k-lines t / (T/4) + (1024/T) i, i < T/32; k-line kr of MN-atom a at
+//     a*(BK*128) + kr*128, 32-byte granule g at g ^ (kr & 3) (LBO = BK*128, SBO = 512).
 template <int T>
-struct MNMap {
-  static constexpr int CPR = T / 4;
-  static constexpr int KSTEP = 128 / CPR;
+struct Place {
+  static constexpr int N = T / 32;          // chunks per thread per stage
+  static constexpr int CPR = T / 4;         // MN-major chunks per k-line
+  static constexpr int KSTEP = GEMM_PRODUCERS / CPR;
+  static __device__ __forceinline__ int krow(int tid, int i) { return (tid >> 3) + 32 * i; }
+  static __device__ __forceinline__ uint32_t kdst(uint32_t sm, int tid, int i) {
+    const int kc = tid & 7, r7 = (tid >> 3) & 7;
+    return sm + ((tid >> 6) << 10) + (r7 << 7) + ((kc ^ r7) << 4) + i * 4096;
+  }
   static __device__ __forceinline__ int mn(int tid) { return (tid % CPR) * 4; }
   static __device__ __forceinline__ int kr(int tid, int i) { return tid / CPR + KSTEP * i; }
+  static __device__ __forceinline__ uint32_t mdst(uint32_t sm, int tid, int i) {
+    const int m = mn(tid), k = kr(tid, i);
+    return sm + (m >> 5) * (GEMM_BK * 128) + ((m & 4) << 2) + k * 128 + ((((m & 31) >> 3) ^ (k & 3)) << 5);
+  }
 };
 
 // ---------------------------------------------------------------- loaders --
 // K-major dense operand: op(r, k) = M(r, k).
 struct LdDenseK {
   static constexpr int kMN = 0;
+  static constexpr bool kTMA = false;
   MatView m;
   template <int T>
   struct State {
-    const float* base[T / 16];
+    const float* base[Place<T>::N];
   };
   template <int T>
   __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
 #pragma unroll
-    for (int i = 0; i < T / 16; ++i) {
-      int r = row0 + (tid >> 3) + 16 * i;
+    for (int i = 0; i < Place<T>::N; ++i) {
+      int r = row0 + Place<T>::krow(tid, i);
       s.base[i] = r < m.rows ? m.p + (long long)r * m.ld : nullptr;
     }
   }
   template <int T>
-  __device__ __forceinline__ const float* src(const State<T>& s, int i, int k, int& nb) const {
-    // k is a multiple of 4; column blocks are multiples of 4 wide
-    if (!s.base[i] || k >= m.cols) {
-      nb = 0;
-      return m.p;
+  __device__ __forceinline__ void load(const State<T>& s, uint32_t sm, int k0, int tid) const {
+    const int k = k0 + (tid & 7) * 4;  // multiple of 4; column blocks are multiples of 4 wide
+    const int nv = m.cols - k;
+    const int nb = nv <= 0 ? 0 : (nv >= 4 ? 16 : nv * 4);
+    const long long off = nb ? m.col_off(k) : 0;
+#pragma unroll
+    for (int i = 0; i < Place<T>::N; ++i) {
+      const bool ok = nb && s.base[i];
+      cp_async16(Place<T>::kdst(sm, tid, i), ok ? s.base[i] + off : m.p, ok ? nb : 0);
     }
-    int nv = m.cols - k;
-    nb = (nv >= 4 ? 4 : nv) * 4;
-    return s.base[i] + m.col_off(k);
   }
 };
 
 // MN-major dense operand: op(r, k) = M(k, r) (4 consecutive r contiguous).
-// ones_row >= 0 (a multiple of 4): rows ones_row.. read {1, 0, 0, 0}.
+// ones_row >= 0 (a multiple of 4): that row chunk reads {1, 0, 0, 0}.
 struct LdDenseMN {
   static constexpr int kMN = 1;
+  static constexpr bool kTMA = false;
   MatView m;
   int ones_row;
   template <int T>
   struct State {
-    long long coff;
-    int nb;  // bytes of this thread's row chunk (0 = outside)
-    bool ones;
+    const float* col;  // &M(0, this thread's column chunk), or g_one4
+    long long ld;      // 0 for the ones chunk
+    int nb;
   };
   template <int T>
   __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
-    int r = row0 + MNMap<T>::mn(tid);
-    s.ones = (r == ones_row);
+    const int r = row0 + Place<T>::mn(tid);
     s.nb = 0;
-    s.coff = 0;
+    s.col = m.p;
+    s.ld = m.ld;
     if (r < m.cols) {
-      int nv = m.cols - r;
+      const int nv = m.cols - r;
       s.nb = (nv >= 4 ? 4 : nv) * 4;
-      s.coff = m.col_off(r);
-    } else if (s.ones) {
+      s.col = m.p + m.col_off(r);
+    } else if (r == ones_row) {
       s.nb = 16;
+      s.col = g_one4;
+      s.ld = 0;
     }
   }
   template <int T>
-  __device__ __forceinline__ const float* src(const State<T>& s, int k, int& nb) const {
-    if (k >= m.rows || s.nb == 0) {
-      nb = 0;
-      return m.p;
+  __device__ __forceinline__ void load(const State<T>& s, uint32_t sm, int k0, int tid) const {
+#pragma unroll
+    for (int i = 0; i < Place<T>::N; ++i) {
+      const int k = k0 + Place<T>::kr(tid, i);
+      const bool ok = s.nb && k < m.rows;
+      cp_async16(Place<T>::mdst(sm, tid, i), ok ? s.col + (long long)k * s.ld : m.p, ok ? s.nb : 0);
     }
-    nb = s.nb;
-    if (s.ones) return g_one4;
-    return m.p + (long long)k * m.ld + s.coff;
   }
 };
 
@@ -167,22 +188,23 @@ struct ConvGeom {
 // Convolution forward, A(m, k): m = (n, oh, ow), k = (r, s, c); x NHWC.
 struct LdConvFwdA {
   static constexpr int kMN = 0;
+  static constexpr bool kTMA = false;
   const float* x;
   ConvGeom g;
   template <int T>
   struct State {
-    const float* base[T / 16];  // x at (n, oh*st - p, ow*st - p, 0) (may point outside x)
-    int h0[T / 16], w0[T / 16];
+    const float* base[Place<T>::N];  // x at (n, oh*st - p, ow*st - p, 0) (may point outside x)
+    int h0[Place<T>::N], w0[Place<T>::N];
   };
   template <int T>
   __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
     const int Mtot = g.N * g.Ho * g.Wo;
 #pragma unroll
-    for (int i = 0; i < T / 16; ++i) {
-      int m = row0 + (tid >> 3) + 16 * i;
+    for (int i = 0; i < Place<T>::N; ++i) {
+      const int m = row0 + Place<T>::krow(tid, i);
       if (m < Mtot) {
-        int n = g.fHoWo.div(m), rem = m - n * g.Ho * g.Wo;
-        int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
+        const int n = g.fHoWo.div(m), rem = m - n * g.Ho * g.Wo;
+        const int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
         s.h0[i] = oh * g.st - g.pad;
         s.w0[i] = ow * g.st - g.pad;
         s.base[i] = x + (((long long)n * g.H + s.h0[i]) * g.W + s.w0[i]) * g.C;
@@ -193,30 +215,19 @@ struct LdConvFwdA {
       }
     }
   }
-  // per-stage tap of this thread's k chunk
-  struct Tap {
-    int r, s;
-    long long off;
-    bool ok;
-  };
-  __device__ __forceinline__ Tap tap(int k) const {
-    Tap t;
-    t.ok = k < g.R * g.S * g.C;
-    int rs = g.fC.div(k), c = k - rs * g.C;
-    t.r = g.fS.div(rs);
-    t.s = rs - t.r * g.S;
-    t.off = ((long long)t.r * g.W + t.s) * g.C + c;
-    return t;
-  }
   template <int T>
-  __device__ __forceinline__ const float* src(const State<T>& s, int i, const Tap& t, int& nb) const {
-    int h = s.h0[i] + t.r, w = s.w0[i] + t.s;
-    if (t.ok && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W) {
-      nb = 16;
-      return s.base[i] + t.off;
+  __device__ __forceinline__ void load(const State<T>& s, uint32_t sm, int k0, int tid) const {
+    const int k = k0 + (tid & 7) * 4;
+    const bool kok = k < g.R * g.S * g.C;
+    const int rs = g.fC.div(k), c = k - rs * g.C;
+    const int r = g.fS.div(rs), sc = rs - r * g.S;
+    const int off = (r * g.W + sc) * g.C + c;
+#pragma unroll
+    for (int i = 0; i < Place<T>::N; ++i) {
+      const int h = s.h0[i] + r, w = s.w0[i] + sc;
+      const bool ok = kok && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W;
+      cp_async16(Place<T>::kdst(sm, tid, i), ok ? s.base[i] + off : x, ok ? 16 : 0);
     }
-    nb = 0;
-    return x;
   }
 };
 
@@ -224,22 +235,23 @@ struct LdConvFwdA {
 // k = (r, s, co); value dy[n][(h+p-r)/st][(w+p-s)/st][co] when integral & in range.
 struct LdConvDgradA {
   static constexpr int kMN = 0;
+  static constexpr bool kTMA = false;
   const float* dy;
   ConvGeom g;
   template <int T>
   struct State {
-    const float* base[T / 16];  // stride 1: dy at (n, h+p, w+p, 0)
-    int hp[T / 16], wp[T / 16], n[T / 16];
+    const float* base[Place<T>::N];  // stride 1: dy at (n, h+p, w+p, 0)
+    int hp[Place<T>::N], wp[Place<T>::N], n[Place<T>::N];
   };
   template <int T>
   __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
     const int Mtot = g.N * g.H * g.W;
 #pragma unroll
-    for (int i = 0; i < T / 16; ++i) {
-      int m = row0 + (tid >> 3) + 16 * i;
+    for (int i = 0; i < Place<T>::N; ++i) {
+      const int m = row0 + Place<T>::krow(tid, i);
       if (m < Mtot) {
-        int n = g.fHW.div(m), rem = m - n * g.H * g.W;
-        int h = g.fW.div(rem), w = rem - h * g.W;
+        const int n = g.fHW.div(m), rem = m - n * g.H * g.W;
+        const int h = g.fW.div(rem), w = rem - h * g.W;
         s.hp[i] = h + g.pad;
         s.wp[i] = w + g.pad;
         s.n[i] = n;
@@ -252,45 +264,39 @@ struct LdConvDgradA {
       }
     }
   }
-  struct Tap {
-    int r, s, co;
-    long long off;
-    bool ok;
-  };
-  __device__ __forceinline__ Tap tap(int k) const {
-    Tap t;
-    t.ok = k < g.R * g.S * g.Co;
-    int rs = g.fCo.div(k);
-    t.co = k - rs * g.Co;
-    t.r = g.fS.div(rs);
-    t.s = rs - t.r * g.S;
-    t.off = -((long long)t.r * g.Wo + t.s) * g.Co + t.co;
-    return t;
-  }
   template <int T>
-  __device__ __forceinline__ const float* src(const State<T>& s, int i, const Tap& t, int& nb) const {
-    nb = 0;
-    if (!t.ok) return dy;
-    int oh = s.hp[i] - t.r, ow = s.wp[i] - t.s;
+  __device__ __forceinline__ void load(const State<T>& s, uint32_t sm, int k0, int tid) const {
+    const int k = k0 + (tid & 7) * 4;
+    const bool kok = k < g.R * g.S * g.Co;
+    const int rs = g.fCo.div(k), co = k - rs * g.Co;
+    const int r = g.fS.div(rs), sc = rs - r * g.S;
     if (g.st == 1) {
-      if ((unsigned)oh < (unsigned)g.Ho && (unsigned)ow < (unsigned)g.Wo) {
-        nb = 16;
-        return s.base[i] + t.off;
+      const int off = co - (r * g.Wo + sc) * g.Co;
+#pragma unroll
+      for (int i = 0; i < Place<T>::N; ++i) {
+        const int oh = s.hp[i] - r, ow = s.wp[i] - sc;
+        const bool ok = kok && (unsigned)oh < (unsigned)g.Ho && (unsigned)ow < (unsigned)g.Wo;
+        cp_async16(Place<T>::kdst(sm, tid, i), ok ? s.base[i] + off : dy, ok ? 16 : 0);
       }
-      return dy;
+    } else {
+#pragma unroll
+      for (int i = 0; i < Place<T>::N; ++i) {
+        int oh = s.hp[i] - r, ow = s.wp[i] - sc;
+        bool ok = kok && oh >= 0 && ow >= 0 && oh % g.st == 0 && ow % g.st == 0;
+        oh /= g.st;
+        ow /= g.st;
+        ok = ok && oh < g.Ho && ow < g.Wo;
+        cp_async16(Place<T>::kdst(sm, tid, i),
+                   ok ? dy + (((long long)s.n[i] * g.Ho + oh) * g.Wo + ow) * g.Co + co : dy, ok ? 16 : 0);
+      }
     }
-    if (oh < 0 || ow < 0 || oh % g.st || ow % g.st) return dy;
-    oh /= g.st;
-    ow /= g.st;
-    if (oh >= g.Ho || ow >= g.Wo) return dy;
-    nb = 16;
-    return dy + (((long long)s.n[i] * g.Ho + oh) * g.Wo + ow) * g.Co + t.co;
   }
 };
 
 // Convolution data gradient, B(c, k) = W[co][r][s][c] with k = (r, s, co); MN-major (c contiguous).
 struct LdConvDgradB {
   static constexpr int kMN = 1;
+  static constexpr bool kTMA = false;
   const float* Wt;
   ConvGeom g;
   template <int T>
@@ -299,15 +305,18 @@ struct LdConvDgradB {
   };
   template <int T>
   __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
-    s.c = row0 + MNMap<T>::mn(tid);
+    s.c = row0 + Place<T>::mn(tid);
   }
   template <int T>
-  __device__ __forceinline__ const float* src(const State<T>& s, int k, int& nb) const {
-    nb = 0;
-    if (s.c >= g.C || k >= g.R * g.S * g.Co) return Wt;
-    int rs = g.fCo.div(k), co = k - rs * g.Co;
-    nb = 16;
-    return Wt + ((long long)co * g.R * g.S + rs) * g.C + s.c;
+  __device__ __forceinline__ void load(const State<T>& s, uint32_t sm, int k0, int tid) const {
+    const int RS = g.R * g.S;
+#pragma unroll
+    for (int i = 0; i < Place<T>::N; ++i) {
+      const int k = k0 + Place<T>::kr(tid, i);
+      const bool ok = s.c < g.C && k < RS * g.Co;
+      const int rs = g.fCo.div(k), co = k - rs * g.Co;
+      cp_async16(Place<T>::mdst(sm, tid, i), ok ? Wt + ((long long)co * RS + rs) * g.C + s.c : Wt, ok ? 16 : 0);
+    }
   }
 };
 
@@ -316,61 +325,242 @@ struct LdConvDgradB {
 // Row ones_row (= R*S*C) is the ones row of the fused bias gradient.
 struct LdConvWgradA {
   static constexpr int kMN = 1;
+  static constexpr bool kTMA = false;
   const float* x;
   ConvGeom g;
   int ones_row;
   template <int T>
   struct State {
-    int r, s;
-    long long off;  // (r*W + s)*C + c
+    int r, s, off;  // off = (r*W + s)*C + c
     int mode;       // 0 outside, 1 data, 2 ones
   };
   template <int T>
   __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
-    int kg = row0 + MNMap<T>::mn(tid);
+    const int kg = row0 + Place<T>::mn(tid);
     s.mode = 0;
-    s.r = s.s = 0;
-    s.off = 0;
+    s.r = s.s = s.off = 0;
     if (kg < g.R * g.S * g.C) {
-      int rs = g.fC.div(kg), c = kg - rs * g.C;
+      const int rs = g.fC.div(kg), c = kg - rs * g.C;
       s.r = g.fS.div(rs);
       s.s = rs - s.r * g.S;
-      s.off = ((long long)s.r * g.W + s.s) * g.C + c;
+      s.off = (s.r * g.W + s.s) * g.C + c;
       s.mode = 1;
     } else if (kg == ones_row) {
       s.mode = 2;
     }
   }
   template <int T>
-  __device__ __forceinline__ const float* src(const State<T>& s, int m, int& nb) const {
-    nb = 0;
-    if (s.mode == 0 || m >= g.N * g.Ho * g.Wo) return x;
-    if (s.mode == 2) {
-      nb = 16;
-      return g_one4;
+  __device__ __forceinline__ void load(const State<T>& s, uint32_t sm, int k0, int tid) const {
+    // The k-lines (pixels) of this thread are warp-uniform when 32 | T/4 (T = 128):
+    // lanes 0..N-1 decompose pixel k0 + kr(tid, lane), the warp shares them.
+    static_assert(Place<T>::CPR % 32 == 0 || Place<T>::CPR < 32, "mapping");
+    const int Mtot = g.N * g.Ho * g.Wo;
+    const int lane = tid & 31;
+    if constexpr (Place<T>::CPR % 32 == 0) {
+      int poff = 0, ph0 = -(1 << 28), pw0 = 0;
+      if (lane < Place<T>::N) {
+        const int m = k0 + Place<T>::kr(tid - lane, lane);
+        if (m < Mtot) {
+          const int n = g.fHoWo.div(m), rem = m - n * g.Ho * g.Wo;
+          const int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
+          ph0 = oh * g.st - g.pad;
+          pw0 = ow * g.st - g.pad;
+          poff = ((n * g.H + ph0) * g.W + pw0) * g.C;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < Place<T>::N; ++i) {
+        const int off = __shfl_sync(0xffffffffu, poff, i);
+        const int h = __shfl_sync(0xffffffffu, ph0, i) + s.r;
+        const int w = __shfl_sync(0xffffffffu, pw0, i) + s.s;
+        bool ok = s.mode == 1 && (unsigned)h < (unsigned)g.H && (unsigned)w < (unsigned)g.W;
+        const float* src = x + off + s.off;
+        if (s.mode == 2) {
+          ok = k0 + Place<T>::kr(tid, i) < Mtot;
+          src = g_one4;
+        }
+        cp_async16(Place<T>::mdst(sm, tid, i), ok ? src : x, ok ? 16 : 0);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < Place<T>::N; ++i) {
+        const int m = k0 + Place<T>::kr(tid, i);
+        bool ok = m < Mtot && s.mode != 0;
+        const float* src = g_one4;
+        if (s.mode == 1) {
+          const int n = g.fHoWo.div(m), rem = m - n * g.Ho * g.Wo;
+          const int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
+          const int h0 = oh * g.st - g.pad, w0 = ow * g.st - g.pad;
+          ok = ok && (unsigned)(h0 + s.r) < (unsigned)g.H && (unsigned)(w0 + s.s) < (unsigned)g.W;
+          src = x + ((n * g.H + h0) * g.W + w0) * g.C + s.off;
+        }
+        cp_async16(Place<T>::mdst(sm, tid, i), ok ? src : x, ok ? 16 : 0);
+      }
     }
-    int n = g.fHoWo.div(m), rem = m - n * g.Ho * g.Wo;
-    int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
-    int h0 = oh * g.st - g.pad, w0 = ow * g.st - g.pad;
-    int h = h0 + s.r, w = w0 + s.s;
-    if ((unsigned)h >= (unsigned)g.H || (unsigned)w >= (unsigned)g.W) return x;
-    nb = 16;
-    return x + (((long long)n * g.H + h0) * g.W + w0) * g.C + s.off;
   }
 };
 
-// Loaders whose K-major chunk address depends on a per-stage "tap" (filter offset).
-template <class L>
-struct requires_tap {
-  static constexpr bool value = false;
+// ------------------------------------------------------------ TMA loaders --
+// One elected producer thread issues cp.async.bulk.tensor per operand per stage
+// (tensor maps encoded on the host after the tile shape is chosen; layouts
+// validated by tools/tma_test.cu).  Whole MN atoms past the data (`valid`) are
+// constant: prefilled once per stage buffer with zeros and the ones row.
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+// Constant MN atoms: rows [valid, ...) are zero, except row ones_row (= 1).
+template <int T>
+__device__ __forceinline__ void prefill_const_atoms(uint32_t sm, int row0, int valid, int ones_row, int tid) {
+  float* base = nullptr;
+  (void)base;
+#pragma unroll 1
+  for (int a = 0; a < T / 32; ++a) {
+    const int r0 = row0 + 32 * a;
+    if (r0 + 32 <= valid || (r0 < valid)) continue;
+    // 32 k-lines x 128 B; the ones row sits at MN position (ones_row - r0)
+    for (int i = tid; i < 32 * 32; i += GEMM_PRODUCERS) {
+      const int kr = i >> 5, mn = i & 31;
+      const float v = (r0 + mn == ones_row) ? 1.f : 0.f;
+      const uint32_t addr = sm + a * (GEMM_BK * 128) + kr * 128 + ((((mn >> 3) ^ (kr & 3))) << 5) + (mn & 7) * 4;
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+    }
+  }
+}
+
+// K-major tile of a (possibly column-blocked) row-major matrix; box {32, T}.
+struct TmaK {
+  static constexpr int kMN = 0;
+  static constexpr bool kTMA = true;
+  CUtensorMap map;
+  int blocked, cb;  // blocked: 3-D map {cb, rows, nblk}
+  template <int T>
+  __device__ __forceinline__ void prefill(uint32_t, int, int) const {}
+  template <int T>
+  __device__ __forceinline__ void issue(uint32_t sm, int row0, int k0, uint32_t bar) const {
+    mbar_expect_tx(bar, T * 128);
+    if (blocked)
+      tma_load_3d(sm, &map, k0 % cb, row0, k0 / cb, bar);
+    else
+      tma_load_2d(sm, &map, k0, row0, bar);
+  }
 };
-template <>
-struct requires_tap<LdConvFwdA> {
-  static constexpr bool value = true;
+
+// MN-major tile of M(k, mn) (mn contiguous), one {32 mn, 32 k} box per MN atom.
+struct TmaMN {
+  static constexpr int kMN = 1;
+  static constexpr bool kTMA = true;
+  CUtensorMap map;
+  int blocked, cb;      // blocked along mn: 3-D map {cb, rows, nblk}
+  int valid, ones_row;  // atoms starting at >= valid are constant (prefilled)
+  int atoms;            // whole tile in one box: 3-D view {32, rows, cols/32}, box {32, 32, T/32}
+  template <int T>
+  __device__ __forceinline__ void prefill(uint32_t sm, int row0, int tid) const {
+    if (!atoms) prefill_const_atoms<T>(sm, row0, valid, ones_row, tid);
+  }
+  template <int T>
+  __device__ __forceinline__ void issue(uint32_t sm, int mn0, int k0, uint32_t bar) const {
+    if (atoms) {
+      mbar_expect_tx(bar, T * 128);
+      tma_load_3d(sm, &map, 0, k0, mn0 >> 5, bar);
+      return;
+    }
+    int n = 0;
+#pragma unroll
+    for (int a = 0; a < T / 32; ++a) n += (mn0 + 32 * a < valid);
+    mbar_expect_tx(bar, n * 32 * 128);
+#pragma unroll
+    for (int a = 0; a < T / 32; ++a) {
+      const int mn = mn0 + 32 * a;
+      if (mn >= valid) continue;
+      if (blocked)
+        tma_load_3d(sm + a * (GEMM_BK * 128), &map, mn % cb, k0, mn / cb, bar);
+      else
+        tma_load_2d(sm + a * (GEMM_BK * 128), &map, mn, k0, bar);
+    }
+  }
 };
-template <>
-struct requires_tap<LdConvDgradA> {
-  static constexpr bool value = true;
+
+// im2col A operand of the convolution forward (fwd) or data gradient (dgrad,
+// stride 1, taps flipped): 128 pixels of the walk x 32 channels at one tap.
+struct TmaIm2col {
+  static constexpr int kMN = 0;
+  static constexpr bool kTMA = true;
+  CUtensorMap map;
+  int C, R, S, gH, gW;  // channels of the mapped tensor; walk grid gH x gW
+  int st, lo;           // window origin of walk pixel (y, x): (y*st + lo, x*st + lo)
+  int flip;
+  FastDiv fC, fS, fHW, fW;
+  template <int T>
+  __device__ __forceinline__ void prefill(uint32_t, int, int) const {}
+  template <int T>
+  __device__ __forceinline__ void issue(uint32_t sm, int m0, int k0, uint32_t bar) const {
+    const int rs = fC.div(k0), c0 = k0 - rs * C;
+    int r = fS.div(rs), s = rs - r * S;
+    if (flip) {
+      r = R - 1 - r;
+      s = S - 1 - s;
+    }
+    const int n = fHW.div(m0), rem = m0 - n * gH * gW;
+    const int y = fW.div(rem), x = rem - y * gW;
+    mbar_expect_tx(bar, 128 * 128);
+    tma_load_im2col(sm, &map, c0, x * st + lo, y * st + lo, n, s, r, bar);
+  }
+};
+
+// Data-gradient B(c, k = (rs, co)) = W[co][rs][c]: 3-D map {C, RS, Co}, box {32, 1, 32}.
+struct TmaDgradB {
+  static constexpr int kMN = 1;
+  static constexpr bool kTMA = true;
+  CUtensorMap map;
+  int C, Co;
+  FastDiv fCo;
+  template <int T>
+  __device__ __forceinline__ void prefill(uint32_t, int, int) const {}
+  template <int T>
+  __device__ __forceinline__ void issue(uint32_t sm, int c0, int k0, uint32_t bar) const {
+    const int rs = fCo.div(k0), co0 = k0 - rs * Co;
+    int n = 0;
+#pragma unroll
+    for (int a = 0; a < T / 32; ++a) n += (c0 + 32 * a < C);
+    mbar_expect_tx(bar, n * 32 * 128);
+#pragma unroll
+    for (int a = 0; a < T / 32; ++a)
+      if (c0 + 32 * a < C) tma_load_3d(sm + a * (GEMM_BK * 128), &map, c0 + 32 * a, rs, co0, bar);
+  }
+};
+
+// Weight-gradient A(kg = (rs, c), m = pixel): im2col map with 32-pixel x
+// 32-channel boxes (one per MN atom of 32 kg), C % 32 == 0; kg >= valid constant.
+struct TmaWgradA {
+  static constexpr int kMN = 1;
+  static constexpr bool kTMA = true;
+  CUtensorMap map;
+  int C, S, Ho, Wo, st, pad;
+  int valid, ones_row;
+  FastDiv fC, fS, fHoWo, fWo;
+  template <int T>
+  __device__ __forceinline__ void prefill(uint32_t sm, int row0, int tid) const {
+    prefill_const_atoms<T>(sm, row0, valid, ones_row, tid);
+  }
+  template <int T>
+  __device__ __forceinline__ void issue(uint32_t sm, int kg0, int k0, uint32_t bar) const {
+    const int n = fHoWo.div(k0), rem = k0 - n * Ho * Wo;
+    const int oh = fWo.div(rem), ow = rem - oh * Wo;
+    int cnt = 0;
+#pragma unroll
+    for (int a = 0; a < T / 32; ++a) cnt += (kg0 + 32 * a < valid);
+    mbar_expect_tx(bar, cnt * 32 * 128);
+#pragma unroll
+    for (int a = 0; a < T / 32; ++a) {
+      const int kg = kg0 + 32 * a;
+      if (kg >= valid) continue;
+      const int rs = fC.div(kg), c0 = kg - rs * C;
+      const int r = fS.div(rs), s = rs - r * S;
+      tma_load_im2col(sm + a * (GEMM_BK * 128), &map, c0, ow * st - pad, oh * st - pad, n, s, r, bar);
+    }
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -407,48 +597,6 @@ struct GemmArgs {
   EpiArgs epi;
 };
 
-// ---------------------------------------------------------------------------
-// Producer: one stage of an operand tile (T rows x BK) into shared memory.
-template <int T, class LD>
-__device__ __forceinline__ void load_stage(const LD& ld, const typename LD::template State<T>& st, uint32_t sm,
-                                           int k0, int tid) {
-  if constexpr (LD::kMN == 0) {
-    // K-major SWIZZLE_128B: row r at (r >> 3) * 1024 + (r & 7) * 128, chunk c at c ^ (r & 7).
-    const int kc = tid & 7, r7 = (tid >> 3) & 7;
-    const uint32_t d0 = sm + ((tid >> 6) << 10) + (r7 << 7) + ((kc ^ r7) << 4);
-    const int k = k0 + kc * 4;
-    if constexpr (requires_tap<LD>::value) {
-      const auto t = ld.tap(k);
-#pragma unroll
-      for (int i = 0; i < T / 16; ++i) {
-        int nb;
-        const float* g = ld.src(st, i, t, nb);
-        cp_async16(d0 + i * 2048, g, nb);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < T / 16; ++i) {
-        int nb;
-        const float* g = ld.template src<T>(st, i, k, nb);
-        cp_async16(d0 + i * 2048, g, nb);
-      }
-    }
-  } else {
-    // MN-major SWIZZLE_128B_BASE32B: k-line kr of MN-atom a at a*(BK*128) + kr*128;
-    // within the line the 32-byte granule g sits at g ^ (kr & 3).  LBO = BK*128, SBO = 512.
-    const int mn = MNMap<T>::mn(tid);
-    const uint32_t dmn = sm + (mn >> 5) * (GEMM_BK * 128) + ((mn & 4) << 2);
-    const int g32 = (mn & 31) >> 3;
-#pragma unroll
-    for (int i = 0; i < T / 16; ++i) {
-      const int kr = MNMap<T>::kr(tid, i);
-      int nb;
-      const float* g = ld.template src<T>(st, k0 + kr, nb);
-      cp_async16(dmn + kr * 128 + ((g32 ^ (kr & 3)) << 5), g, nb);
-    }
-  }
-}
-
 template <int T, int MN>
 __device__ __forceinline__ uint64_t tile_desc(uint32_t sm, int kk) {
   if constexpr (MN == 0) {
@@ -456,6 +604,11 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t sm, int kk) {
   } else {
     return umma_desc_mn_sw128_32b(sm + kk * 8 * 128, GEMM_BK * 128, 512);
   }
+}
+
+template <int BN>
+constexpr int gemm_stages() {
+  return BN <= 32 ? 8 : BN <= 64 ? 7 : BN <= 128 ? 6 : 4;
 }
 
 template <int BN, int STAGES>
@@ -470,7 +623,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
   constexpr int LAG = STAGES > 2 ? STAGES - 2 : 1;
+  constexpr int MMA_WARP = GEMM_PRODUCERS / 32;
   static_assert(BN % 32 == 0 && BN <= 256, "BN");
+  static_assert(LA::kTMA == LB::kTMA, "both operands TMA or both cp.async");
+  constexpr bool TMA = LA::kTMA;
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -492,73 +648,114 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(bar_base + 8 * s, 128);                // one arrive per producer thread
+      mbar_init(bar_base + 8 * s, TMA ? 1 : GEMM_PRODUCERS);  // TMA thread / every producer thread
       mbar_init(bar_base + 8 * (STAGES + s), 1);       // tcgen05.commit
     }
     mbar_init(accum_bar, 1);
     fence_barrier_init();
   }
-  if (warp == 4) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == MMA_WARP) tmem_alloc<TMEM_COLS>(tmem_slot);
+  if constexpr (TMA) {
+    if (warp < MMA_WARP) {
+      for (int s = 0; s < STAGES; ++s) {
+        args.a.template prefill<GEMM_BM>(sbase + s * STAGE_BYTES, m0, tid);
+        args.b.template prefill<BN>(sbase + s * STAGE_BYTES + A_BYTES, n0, tid);
+      }
+      fence_proxy_async_smem();
+    }
+    if (tid == 0) {
+      prefetch_tmap(&args.a.map);
+      prefetch_tmap(&args.b.map);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
 
-  if (warp < 4) {
-    // ------------------------------ producers ------------------------------
-    typename LA::template State<GEMM_BM> sa_st;
-    typename LB::template State<BN> sb_st;
-    args.a.template init<GEMM_BM>(sa_st, m0, tid);
-    args.b.template init<BN>(sb_st, n0, tid);
-    for (int it = 0; it < nkb; ++it) {
-      const int s = it % STAGES;
-      const int round = it / STAGES;
-      if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
-      const uint32_t sa = sbase + s * STAGE_BYTES;
-      const int k0 = (kb_begin + it) * GEMM_BK;
-      load_stage<GEMM_BM>(args.a, sa_st, sa, k0, tid);
-      load_stage<BN>(args.b, sb_st, sa + A_BYTES, k0, tid);
-      cp_async_commit();
-      if (it >= LAG) {
-        // this thread's copies for k-block it-LAG have landed: make them visible
-        // to the tensor-core (async) proxy, then release the stage.
-        cp_async_wait<LAG>();
-        fence_proxy_async_smem();
-        mbar_arrive(bar_base + 8 * ((it - LAG) % STAGES));
+  const int lane = tid & 31;
+  if (warp < MMA_WARP) {
+    if constexpr (TMA) {
+      if (warp == 0) {
+        // ----------------- TMA producer: warp 0, lane 0 issues (warp-uniform waits) -----------------
+        for (int it = 0; it < nkb; ++it) {
+          const int s = it % STAGES;
+          const int round = it / STAGES;
+          if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
+          if (lane == 0) {
+            const uint32_t sa = sbase + s * STAGE_BYTES;
+            const uint32_t full = bar_base + 8 * s;
+            const int k0 = (kb_begin + it) * GEMM_BK;
+            args.a.template issue<GEMM_BM>(sa, m0, k0, full);
+            args.b.template issue<BN>(sa + A_BYTES, n0, k0, full);
+            mbar_arrive(full);
+          }
+          __syncwarp();
+        }
       }
+    } else {
+      // --------------------------- cp.async producers ---------------------------
+      typename LA::template State<GEMM_BM> sa_st;
+      typename LB::template State<BN> sb_st;
+      args.a.template init<GEMM_BM>(sa_st, m0, tid);
+      args.b.template init<BN>(sb_st, n0, tid);
+      for (int it = 0; it < nkb; ++it) {
+        const int s = it % STAGES;
+        const int round = it / STAGES;
+        if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
+        const uint32_t sa = sbase + s * STAGE_BYTES;
+        const int k0 = (kb_begin + it) * GEMM_BK;
+        args.a.template load<GEMM_BM>(sa_st, sa, k0, tid);
+        args.b.template load<BN>(sb_st, sa + A_BYTES, k0, tid);
+        cp_async_commit();
+        if (it >= LAG) {
+          // this thread's copies for k-block it-LAG have landed: make them visible
+          // to the tensor-core (async) proxy, then release the stage.
+          cp_async_wait<LAG>();
+          fence_proxy_async_smem();
+          mbar_arrive(bar_base + 8 * ((it - LAG) % STAGES));
+        }
+      }
+      cp_async_wait<0>();
+      fence_proxy_async_smem();
+      for (int j = (nkb > LAG ? nkb - LAG : 0); j < nkb; ++j) mbar_arrive(bar_base + 8 * (j % STAGES));
     }
-    cp_async_wait<0>();
-    fence_proxy_async_smem();
-    for (int j = (nkb > LAG ? nkb - LAG : 0); j < nkb; ++j) mbar_arrive(bar_base + 8 * (j % STAGES));
-  } else if (tid == 128) {
-    // ------------------------------ MMA issuer -----------------------------
+  } else {
+    // ------------- MMA issuer: the whole warp waits, lane 0 issues -------------
     constexpr uint32_t idesc = idesc_tf32(GEMM_BM, BN, LA::kMN, LB::kMN);
     for (int it = 0; it < nkb; ++it) {
       const int s = it % STAGES;
       mbar_wait(bar_base + 8 * s, (it / STAGES) & 1);
       tc_fence_after();
-      const uint32_t sa = sbase + s * STAGE_BYTES;
+      if (lane == 0) {
+        const uint32_t sa = sbase + s * STAGE_BYTES;
 #pragma unroll
-      for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
-        uint64_t ad = tile_desc<GEMM_BM, LA::kMN>(sa, kk);
-        uint64_t bd = tile_desc<BN, LB::kMN>(sa + A_BYTES, kk);
-        mma_tf32(tmem, ad, bd, idesc, (it | kk) ? 1u : 0u);
+        for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
+          uint64_t ad = tile_desc<GEMM_BM, LA::kMN>(sa, kk);
+          uint64_t bd = tile_desc<BN, LB::kMN>(sa + A_BYTES, kk);
+          mma_tf32(tmem, ad, bd, idesc, (it | kk) ? 1u : 0u);
+        }
+        mma_commit(bar_base + 8 * (STAGES + s));
       }
-      mma_commit(bar_base + 8 * (STAGES + s));
+      __syncwarp();
     }
-    mma_commit(accum_bar);
+    if (lane == 0) mma_commit(accum_bar);
+    __syncwarp();
   }
 
   // -------------------------------- epilogue --------------------------------
-  if (warp < 4) {
+  if (warp < MMA_WARP) {
     if (nkb > 0) mbar_wait(accum_bar, 0);
     tc_fence_after();
-    const int row = m0 + warp * 32 + (tid & 31);
+    const int lg = warp & 3;                 // TMEM lane group this warp may access
+    const int row = m0 + lg * 32 + (tid & 31);
     const EpiArgs& e = args.epi;
-    const uint32_t tbase = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t tbase = tmem + ((uint32_t)(lg * 32) << 16);
     const bool plain_vec = !e.trans && e.cb >= args.N && (e.ld & 3) == 0 && !e.bias_on_m;
+    constexpr int HALF = BN / 2;
+    const int cbeg = (warp >> 2) * HALF;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = cbeg; c0 < cbeg + HALF; c0 += 16) {
       if (n0 + c0 >= args.N) break;
       float v[16];
       if (nkb > 0) {
@@ -626,7 +823,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == MMA_WARP) {
     tc_fence_after();
     tmem_dealloc<TMEM_COLS>(tmem);
   }

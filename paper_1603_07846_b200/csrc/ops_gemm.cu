@@ -2,7 +2,10 @@
 // gradient / weight gradient (+ fused bias gradient) and inner-product forward /
 // data gradient / weight gradient (§4.1.2, §5.4.1; SURVEY
 // §8(a) a3, a8, a10, a15), deterministic split-K reduction and column sums.
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm_tc.cuh"
 #include "ops.h"
@@ -24,9 +27,13 @@ inline long long pad4(int n) { return (n + 3) & ~3; }
 
 Plan plan_gemm(int M, int N, int K, size_t ws_floats_avail) {
   Plan p;
+  static const int big_bn = getenv("SG_BN_BIG") ? atoi(getenv("SG_BN_BIG")) : 1;
   p.bn = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
   p.mt = (M + GEMM_BM - 1) / GEMM_BM;
-  if (p.bn == 256 && p.mt * ((N + 255) / 256) < kNumSMs) p.bn = 128;
+  const int nkb0 = (K + GEMM_BK - 1) / GEMM_BK;
+  // wide tiles halve the operand bytes per MMA; keep them when split-K can fill the machine
+  const bool can_split = nkb0 >= 2 * kMinKbPerSplit * ((kNumSMs + p.mt - 1) / p.mt);
+  if (p.bn == 256 && p.mt * ((N + 255) / 256) < kNumSMs && !(big_bn && can_split)) p.bn = 128;
   p.nt = (N + p.bn - 1) / p.bn;
   const int nkb = (K + GEMM_BK - 1) / GEMM_BK;
   const int tiles = p.mt * p.nt;
@@ -43,37 +50,42 @@ Plan plan_gemm(int M, int N, int K, size_t ws_floats_avail) {
   return p;
 }
 
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, long long split_stride, int M, int N,
-                                     EpiArgs e) {
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)M * N) return;
-  int m, n;
-  if (e.trans) {  // consecutive threads -> consecutive m (coalesced store)
-    n = (int)(idx / M);
-    m = (int)(idx - (long long)n * M);
-  } else {
-    m = (int)(idx / N);
-    n = (int)(idx - (long long)m * N);
-  }
-  if (m >= e.mvalid && m != e.xrow) return;
+// Fixed-order split-K reduction: a block owns 32 consecutive outputs (row-major
+// m*N + n); its 8 warps sum the splits g, g+8, g+16, ... for every output, then
+// warp 0 adds the 8 partial sums in ascending g.  Deterministic.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits,
+                                                            long long split_stride, int M, int N, EpiArgs e) {
+  __shared__ float part[8][32];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const long long idx = (long long)blockIdx.x * 32 + lane;
+  const bool in = idx < (long long)M * N;
+  const int m = in ? (int)(idx / N) : 0, n = in ? (int)(idx - (long long)m * N) : 0;
   float acc = 0.f;
-  const float* p = ws + (long long)m * ((N + 3) & ~3) + n;
-  for (int s = 0; s < splits; ++s) acc += p[s * split_stride];
-  if (m == e.xrow) {
-    e.xout[n] = acc;
+  if (in) {
+    const float* p = ws + (long long)m * ((N + 3) & ~3) + n;
+    for (int s = g; s < splits; s += 8) acc += p[s * split_stride];
+  }
+  part[g][lane] = acc;
+  __syncthreads();
+  if (g != 0 || !in) return;
+  float t = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) t += part[j][lane];
+  if (m >= e.mvalid) {
+    if (m == e.xrow) e.xout[n] = t;
     return;
   }
-  if (e.bias) acc += e.bias_on_m ? e.bias[m] : e.bias[n];
-  if (e.relu) acc = fmaxf(acc, 0.f);
+  if (e.bias) t += e.bias_on_m ? e.bias[m] : e.bias[n];
+  if (e.relu) t = fmaxf(t, 0.f);
   if (e.trans)
-    *out_at(e, n, m, e.mvalid) = acc;
+    *out_at(e, n, m, e.mvalid) = t;
   else
-    *out_at(e, m, n, N) = acc;
+    *out_at(e, m, n, N) = t;
 }
 
 template <int BN, class LA, class LB>
 cudaError_t launch_bn(const GemmArgs<LA, LB>& args, const Plan& p, cudaStream_t st) {
-  constexpr int STAGES = BN >= 256 ? 3 : 4;
+  constexpr int STAGES = gemm_stages<BN>();
   constexpr int SMEM = gemm_smem_bytes<BN, STAGES>();
   auto kern = gemm_tc_kernel<BN, STAGES, LA, LB>;
   static bool configured = false;
@@ -88,9 +100,9 @@ cudaError_t launch_bn(const GemmArgs<LA, LB>& args, const Plan& p, cudaStream_t 
 }
 
 template <class LA, class LB>
-cudaError_t run_gemm(const LA& a, const LB& b, int M, int N, int K, EpiArgs epi, Workspace ws, cudaStream_t st) {
+cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int N, int K, EpiArgs epi, Workspace ws,
+                             cudaStream_t st) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  Plan p = plan_gemm(M, N, K, ws.floats);
   GemmArgs<LA, LB> args{a, b, M, N, K, p.kb_per_split, epi};
   if (p.splits > 1) {
     args.epi.ws = ws.ptr;
@@ -108,9 +120,146 @@ cudaError_t run_gemm(const LA& a, const LB& b, int M, int N, int K, EpiArgs epi,
   }
   if (e != cudaSuccess || p.splits == 1) return e;
   long long total = (long long)M * N;
-  splitk_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(ws.ptr, p.splits, (long long)M * pad4(N), M,
-                                                                         N, epi);
+  splitk_reduce_kernel<<<(unsigned)((total + 31) / 32), 256, 0, st>>>(ws.ptr, p.splits, (long long)M * pad4(N), M, N,
+                                                                       epi);
   return launched();
+}
+
+template <class LA, class LB>
+cudaError_t run_gemm(const LA& a, const LB& b, int M, int N, int K, EpiArgs epi, Workspace ws, cudaStream_t st) {
+  return run_gemm_planned(a, b, plan_gemm(M, N, K, ws.floats), M, N, K, epi, ws, st);
+}
+
+// TMA operands: the tensor maps' boxes depend on the tile chosen by the plan.
+template <class MA, class MB>
+cudaError_t run_gemm_mk(MA mkA, MB mkB, int M, int N, int K, EpiArgs epi, Workspace ws, cudaStream_t st) {
+  const Plan p = plan_gemm(M, N, K, ws.floats);
+  return run_gemm_planned(mkA(GEMM_BM), mkB(p.bn), p, M, N, K, epi, ws, st);
+}
+
+// ------------------------------------------------------- tensor-map encode --
+PFN_cuTensorMapEncodeTiled_v12000 g_enc_tiled = nullptr;
+PFN_cuTensorMapEncodeIm2col_v12000 g_enc_im2col = nullptr;
+
+// TMA operand paths per operation (measured: TMA wins for the im2col conv
+// forward / data gradient, cp.async for the rest; SG_TMA_OPS overrides):
+// bit 0 conv fwd, 1 conv dgrad, 2 conv wgrad, 3 inner product, 4 plain GEMM.
+int tma_ops() {
+  static int ops = -1;
+  if (ops < 0) {
+    const char* env = getenv("SG_TMA_OPS");
+    ops = env ? atoi(env) : 0x1f;
+  }
+  return ops;
+}
+bool tma_on_impl();
+bool tma_on(int op_bit) { return (tma_ops() >> op_bit & 1) && tma_on_impl(); }
+
+bool tma_on_impl() {
+  static int state = -1;
+  if (state < 0) {
+    const char* env = getenv("SG_TMA");
+    state = 0;
+    if (!(env && env[0] == '0')) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&g_enc_tiled, cudaEnableDefault, &q) ==
+              cudaSuccess &&
+          cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", (void**)&g_enc_im2col, cudaEnableDefault, &q) ==
+              cudaSuccess &&
+          g_enc_tiled && g_enc_im2col)
+        state = 1;
+    }
+  }
+  return state == 1;
+}
+
+bool aligned16p(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// rank-2/3 tiled fp32 map; dims innermost first, strides in bytes for dims 1..
+CUtensorMap enc_tiled(const void* p, int rank, const cuuint64_t* dims, const cuuint64_t* strides_b,
+                      const cuuint32_t* box, CUtensorMapSwizzle sw, bool* ok) {
+  CUtensorMap m;
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_enc_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(p), dims, strides_b, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  *ok = *ok && r == CUDA_SUCCESS;
+  return m;
+}
+
+CUtensorMap enc_im2col(const void* x, int N, int H, int W, int C, int lo_w, int lo_h, int up_w, int up_h,
+                       int channels, int pixels, int st, CUtensorMapSwizzle sw, bool* ok) {
+  CUtensorMap m;
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4};
+  int lower[2] = {lo_w, lo_h}, upper[2] = {up_w, up_h};
+  cuuint32_t es[4] = {1, (cuuint32_t)st, (cuuint32_t)st, 1};
+  CUresult r = g_enc_im2col(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(x), dims, strides, lower, upper,
+                            channels, pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  // driver <= 13.1 quirk for small tensors (as in CUTLASS's im2col descriptor builder)
+  if ((size_t)N * H * W * C * 4 < 131072) reinterpret_cast<uint64_t*>(&m)[1] &= ~(1llu << 21);
+  *ok = *ok && r == CUDA_SUCCESS && lo_w >= -128 && lo_w <= 127 && lo_h >= -128 && lo_h <= 127 && up_w >= -128 &&
+        up_w <= 127 && up_h >= -128 && up_h <= 127;
+  return m;
+}
+
+// K-major tile of a row-major [rows][cols] matrix (ld elements), optionally column-blocked.
+TmaK tma_k(const View2D& v, int box_rows, bool* ok) {
+  TmaK t{};
+  const bool blocked = v.cb > 0 && v.cb < v.cols;
+  t.blocked = blocked;
+  t.cb = blocked ? v.cb : v.cols;
+  if (blocked) {
+    *ok = *ok && v.cb % 32 == 0 && (v.bs * 4) % 16 == 0;
+    cuuint64_t dims[3] = {(cuuint64_t)v.cb, (cuuint64_t)v.rows, (cuuint64_t)((v.cols + v.cb - 1) / v.cb)};
+    cuuint64_t strides[2] = {(cuuint64_t)v.ld * 4, (cuuint64_t)v.bs * 4};
+    cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+    t.map = enc_tiled(v.p, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, ok);
+  } else {
+    cuuint64_t dims[2] = {(cuuint64_t)v.cols, (cuuint64_t)v.rows};
+    cuuint64_t strides[1] = {(cuuint64_t)v.ld * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    t.map = enc_tiled(v.p, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, ok);
+  }
+  *ok = *ok && aligned16p(v.p) && (v.ld * 4) % 16 == 0 && box_rows <= 256;
+  return t;
+}
+
+// MN-major tile of M(k, mn) = v(row = k, col = mn); valid / ones_row as TmaMN.
+// A plain matrix with 32 | cols and no constant atoms is loaded as ONE box per
+// stage through the 3-D view {32, rows, cols/32} (atom stride 128 B).
+TmaMN tma_mn(const View2D& v, int valid, int ones_row, int box_rows, bool* ok) {
+  TmaMN t{};
+  const bool blocked = v.cb > 0 && v.cb < v.cols;
+  t.blocked = blocked;
+  t.cb = blocked ? v.cb : v.cols;
+  t.valid = valid;
+  t.ones_row = ones_row;
+  t.atoms = !blocked && ones_row < 0 && v.cols % 32 == 0 && valid == v.cols;
+  if (t.atoms) {
+    cuuint64_t dims[3] = {32, (cuuint64_t)v.rows, (cuuint64_t)(v.cols / 32)};
+    cuuint64_t strides[2] = {(cuuint64_t)v.ld * 4, 128};
+    cuuint32_t box[3] = {32, 32, (cuuint32_t)(box_rows / 32)};
+    t.map = enc_tiled(v.p, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, ok);
+  } else if (blocked) {
+    *ok = *ok && v.cb % 32 == 0 && (v.bs * 4) % 16 == 0;
+    cuuint64_t dims[3] = {(cuuint64_t)v.cb, (cuuint64_t)v.rows, (cuuint64_t)((v.cols + v.cb - 1) / v.cb)};
+    cuuint64_t strides[2] = {(cuuint64_t)v.ld * 4, (cuuint64_t)v.bs * 4};
+    cuuint32_t box[3] = {32, 32, 1};
+    t.map = enc_tiled(v.p, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, ok);
+  } else {
+    cuuint64_t dims[2] = {(cuuint64_t)v.cols, (cuuint64_t)v.rows};
+    cuuint64_t strides[1] = {(cuuint64_t)v.ld * 4};
+    cuuint32_t box[2] = {32, 32};
+    t.map = enc_tiled(v.p, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, ok);
+  }
+  *ok = *ok && aligned16p(v.p) && (v.ld * 4) % 16 == 0;
+  return t;
+}
+
+View2D vplain(const float* p, int rows, int cols, long long ld) {
+  return View2D{const_cast<float*>(p), ld, 0, cols, rows, cols};
 }
 
 MatView mv(const float* p, int rows, int cols, long long ld, long long bs = 0, int cb = 0) {
@@ -228,48 +377,150 @@ size_t colsum_ws_floats(int M, int N) { return (size_t)((M + CS_ROWS_PER_BLOCK -
 cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const float* b, float* y, int relu,
                      Workspace ws, cudaStream_t st) {
   const int M = s.N * s.Ho * s.Wo, N = s.Co, K = s.R * s.S * s.C;
+  const EpiArgs e = epi_plain(y, s.Co, 0, b, 0, relu, M);
+  if (tma_on(0) && s.C % 32 == 0 && aligned16p(x)) {
+    bool ok = true;
+    TmaIm2col a{};
+    a.map = enc_im2col(x, s.N, s.H, s.W, s.C, -s.pad, -s.pad, s.pad - (s.S - 1), s.pad - (s.R - 1), 32, GEMM_BM,
+                       s.st, CU_TENSOR_MAP_SWIZZLE_128B, &ok);
+    a.C = s.C;
+    a.R = s.R;
+    a.S = s.S;
+    a.gH = s.Ho;
+    a.gW = s.Wo;
+    a.st = s.st;
+    a.lo = -s.pad;
+    a.flip = 0;
+    a.fC = make_fastdiv(s.C);
+    a.fS = make_fastdiv(s.S);
+    a.fHW = make_fastdiv(s.Ho * s.Wo);
+    a.fW = make_fastdiv(s.Wo);
+    const Plan p = plan_gemm(M, N, K, ws.floats);
+    TmaK bw = tma_k(vplain(W, s.Co, K, K), p.bn, &ok);
+    if (ok) return run_gemm_planned(a, bw, p, M, N, K, e, ws, st);
+  }
   LdConvFwdA a{x, geom(s)};
   LdDenseK bw{mv(W, s.Co, K, K)};
-  return run_gemm(a, bw, M, N, K, epi_plain(y, s.Co, 0, b, 0, relu, M), ws, st);
+  return run_gemm(a, bw, M, N, K, e, ws, st);
 }
 
 cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* W, float* dx, Workspace ws,
                        cudaStream_t st) {
   const int M = s.N * s.H * s.W, N = s.C, K = s.R * s.S * s.Co;
+  const EpiArgs e = epi_plain(dx, s.C, 0, nullptr, 0, 0, M);
+  if (tma_on(1) && s.st == 1 && s.Co % 32 == 0 && s.C % 32 == 0 && aligned16p(dy) && aligned16p(W)) {
+    bool ok = true;
+    const int lo = s.pad - (s.R - 1);
+    TmaIm2col a{};
+    a.map = enc_im2col(dy, s.N, s.Ho, s.Wo, s.Co, lo, lo, lo + (s.W - s.Wo), lo + (s.H - s.Ho), 32, GEMM_BM, 1,
+                       CU_TENSOR_MAP_SWIZZLE_128B, &ok);
+    a.C = s.Co;
+    a.R = s.R;
+    a.S = s.S;
+    a.gH = s.H;
+    a.gW = s.W;
+    a.st = 1;
+    a.lo = lo;
+    a.flip = 1;
+    a.fC = make_fastdiv(s.Co);
+    a.fS = make_fastdiv(s.S);
+    a.fHW = make_fastdiv(s.H * s.W);
+    a.fW = make_fastdiv(s.W);
+    TmaDgradB bw{};
+    cuuint64_t dims[3] = {(cuuint64_t)s.C, (cuuint64_t)(s.R * s.S), (cuuint64_t)s.Co};
+    cuuint64_t strides[2] = {(cuuint64_t)s.C * 4, (cuuint64_t)s.R * s.S * s.C * 4};
+    cuuint32_t box[3] = {32, 1, 32};
+    bw.map = enc_tiled(W, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, &ok);
+    bw.C = s.C;
+    bw.Co = s.Co;
+    bw.fCo = make_fastdiv(s.Co);
+    if (ok) return run_gemm(a, bw, M, N, K, e, ws, st);
+  }
   LdConvDgradA a{dy, geom(s)};
   LdConvDgradB bw{W, geom(s)};
-  return run_gemm(a, bw, M, N, K, epi_plain(dx, s.C, 0, nullptr, 0, 0, M), ws, st);
+  return run_gemm(a, bw, M, N, K, e, ws, st);
 }
 
 cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dW, float* db, Workspace ws,
                        cudaStream_t st) {
   const int Kg = s.R * s.S * s.C, Mtot = s.N * s.Ho * s.Wo;
-  LdConvWgradA a{x, geom(s), db ? Kg : -1};
-  LdDenseMN bd{mv(dy, Mtot, s.Co, s.Co), -1};
   // D[kg][co] stored transposed into dW[co][kg]; row Kg (ones) = db
   EpiArgs e = epi_plain(dW, Kg, 1, nullptr, 0, 0, Kg);
   if (db) {
     e.xrow = Kg;
     e.xout = db;
   }
-  return run_gemm(a, bd, db ? Kg + 1 : Kg, s.Co, Mtot, e, ws, st);
+  const int M = db ? Kg + 1 : Kg;
+  if (tma_on(2) && s.C % 32 == 0 && aligned16p(x) && aligned16p(dy)) {
+    bool ok = true;
+    TmaWgradA a{};
+    a.map = enc_im2col(x, s.N, s.H, s.W, s.C, -s.pad, -s.pad, s.pad - (s.S - 1), s.pad - (s.R - 1), 32, GEMM_BK, s.st,
+                       CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, &ok);
+    a.C = s.C;
+    a.S = s.S;
+    a.Ho = s.Ho;
+    a.Wo = s.Wo;
+    a.st = s.st;
+    a.pad = s.pad;
+    a.valid = Kg;
+    a.ones_row = db ? Kg : -1;
+    a.fC = make_fastdiv(s.C);
+    a.fS = make_fastdiv(s.S);
+    a.fHoWo = make_fastdiv(s.Ho * s.Wo);
+    a.fWo = make_fastdiv(s.Wo);
+    const Plan p = plan_gemm(M, s.Co, Mtot, ws.floats);
+    TmaMN bd = tma_mn(vplain(dy, Mtot, s.Co, s.Co), s.Co, -1, p.bn, &ok);
+    if (ok) return run_gemm_planned(a, bd, p, M, s.Co, Mtot, e, ws, st);
+  }
+  LdConvWgradA a{x, geom(s), db ? Kg : -1};
+  LdDenseMN bd{mv(dy, Mtot, s.Co, s.Co), -1};
+  return run_gemm(a, bd, M, s.Co, Mtot, e, ws, st);
 }
 
 // ---------------------------------------------------------- inner product ----
 cudaError_t ip_fwd(View2D x, const float* W, int dv, int dh, const float* b, View2D y, int relu, Workspace ws,
                    cudaStream_t st) {
+  const EpiArgs e = epi_view(y, b, relu);
+  if (tma_on(3)) {
+    bool ok = true;
+    const Plan p = plan_gemm(x.rows, dh, dv, ws.floats);
+    TmaK a = tma_k(x, GEMM_BM, &ok);
+    TmaMN bw = tma_mn(vplain(W, dv, dh, dh), dh, -1, p.bn, &ok);  // op(n, k) = W(k, n)
+    if (ok) return run_gemm_planned(a, bw, p, x.rows, dh, dv, e, ws, st);
+  }
   LdDenseK a{mv(x)};
-  LdDenseMN bw{mv(W, dv, dh, dh), -1};  // op(n, k) = W(k, n)
-  return run_gemm(a, bw, x.rows, dh, dv, epi_view(y, b, relu), ws, st);
+  LdDenseMN bw{mv(W, dv, dh, dh), -1};
+  return run_gemm(a, bw, x.rows, dh, dv, e, ws, st);
 }
 
 cudaError_t ip_dgrad(View2D dy, const float* W, int dv, int dh, View2D dx, Workspace ws, cudaStream_t st) {
+  const EpiArgs e = epi_view(dx, nullptr, 0);
+  if (tma_on(3)) {
+    bool ok = true;
+    TmaK a = tma_k(dy, GEMM_BM, &ok);
+    const Plan p = plan_gemm(dy.rows, dv, dh, ws.floats);
+    TmaK bw = tma_k(vplain(W, dv, dh, dh), p.bn, &ok);  // op(n = v, k = h) = W(v, h)
+    if (ok) return run_gemm_planned(a, bw, p, dy.rows, dv, dh, e, ws, st);
+  }
   LdDenseK a{mv(dy)};
-  LdDenseK bw{mv(W, dv, dh, dh)};   // op(n = v, k = h) = W(v, h)
-  return run_gemm(a, bw, dy.rows, dv, dh, epi_view(dx, nullptr, 0), ws, st);
+  LdDenseK bw{mv(W, dv, dh, dh)};
+  return run_gemm(a, bw, dy.rows, dv, dh, e, ws, st);
 }
 
 cudaError_t ip_wgrad(View2D x, View2D dy, int dv, int dh, float* dW, float* db, Workspace ws, cudaStream_t st) {
+  if (tma_on(3)) {
+    bool ok = true;
+    const int dv32 = (dv + 31) & ~31;  // the ones row starts its own (prefilled) MN atom
+    const Plan p = plan_gemm(db ? dv32 + 1 : dv, dh, x.rows, ws.floats);
+    TmaMN a = tma_mn(x, dv, db ? dv32 : -1, GEMM_BM, &ok);
+    TmaMN bd = tma_mn(dy, dh, -1, p.bn, &ok);
+    EpiArgs e = epi_plain(dW, dh, 0, nullptr, 0, 0, dv);
+    if (db) {
+      e.xrow = dv32;
+      e.xout = db;
+    }
+    if (ok) return run_gemm_planned(a, bd, p, db ? dv32 + 1 : dv, dh, x.rows, e, ws, st);
+  }
   const int dv4 = (dv + 3) & ~3;
   LdDenseMN a{mv(x), db ? dv4 : -1};   // op(m = v, k = row) = x(row, v); row dv4 = ones
   LdDenseMN bd{mv(dy), -1};            // op(n = h, k = row) = dy(row, h)
@@ -284,6 +535,27 @@ cudaError_t ip_wgrad(View2D x, View2D dy, int dv, int dh, float* dW, float* db, 
 cudaError_t gemm_plain(const float* A, int ta, const float* B, int tb, float* C, int M, int N, int K, Workspace ws,
                        cudaStream_t st) {
   EpiArgs e = epi_plain(C, N, 0, nullptr, 0, 0, M);
+  if (tma_on(4)) {
+    bool ok = true;
+    const Plan p = plan_gemm(M, N, K, ws.floats);
+    if (!ta && !tb) {
+      TmaK a = tma_k(vplain(A, M, K, K), GEMM_BM, &ok);
+      TmaMN b = tma_mn(vplain(B, K, N, N), N, -1, p.bn, &ok);
+      if (ok) return run_gemm_planned(a, b, p, M, N, K, e, ws, st);
+    } else if (!ta && tb) {
+      TmaK a = tma_k(vplain(A, M, K, K), GEMM_BM, &ok);
+      TmaK b = tma_k(vplain(B, N, K, K), p.bn, &ok);
+      if (ok) return run_gemm_planned(a, b, p, M, N, K, e, ws, st);
+    } else if (ta && !tb) {
+      TmaMN a = tma_mn(vplain(A, K, M, M), M, -1, GEMM_BM, &ok);
+      TmaMN b = tma_mn(vplain(B, K, N, N), N, -1, p.bn, &ok);
+      if (ok) return run_gemm_planned(a, b, p, M, N, K, e, ws, st);
+    } else {
+      TmaMN a = tma_mn(vplain(A, K, M, M), M, -1, GEMM_BM, &ok);
+      TmaK b = tma_k(vplain(B, N, K, K), p.bn, &ok);
+      if (ok) return run_gemm_planned(a, b, p, M, N, K, e, ws, st);
+    }
+  }
   if (!ta && !tb) return run_gemm(LdDenseK{mv(A, M, K, K)}, LdDenseMN{mv(B, K, N, N), -1}, M, N, K, e, ws, st);
   if (!ta && tb) return run_gemm(LdDenseK{mv(A, M, K, K)}, LdDenseK{mv(B, N, K, K)}, M, N, K, e, ws, st);
   if (ta && !tb)

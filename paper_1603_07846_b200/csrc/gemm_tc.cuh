@@ -597,12 +597,20 @@ struct GemmArgs {
   EpiArgs epi;
 };
 
-template <int T, int MN>
+// Shared-memory descriptor of the kk-th K=8 step of a stage tile, per operand
+// layout: 0 K-major SWIZZLE_128B, 1 MN-major SWIZZLE_128B_BASE32B, 2 K-major
+// no-swizzle (16-byte K chunks of T rows at 2 KB), 3 MN-major no-swizzle
+// (16-byte MN chunks of 32 k-lines at 512 B).
+template <int T, int LAYOUT>
 __device__ __forceinline__ uint64_t tile_desc(uint32_t sm, int kk) {
-  if constexpr (MN == 0) {
+  if constexpr (LAYOUT == 0) {
     return umma_desc_sw128(sm + kk * 32, 16, 1024);
-  } else {
+  } else if constexpr (LAYOUT == 1) {
     return umma_desc_mn_sw128_32b(sm + kk * 8 * 128, GEMM_BK * 128, 512);
+  } else if constexpr (LAYOUT == 2) {
+    return umma_desc_noswz(sm + kk * 2 * (T * 16), T * 16, 128);
+  } else {
+    return umma_desc_noswz(sm + kk * 128, 128, GEMM_BK * 16);
   }
 }
 
@@ -722,7 +730,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
     }
   } else {
     // ------------- MMA issuer: the whole warp waits, lane 0 issues -------------
-    constexpr uint32_t idesc = idesc_tf32(GEMM_BM, BN, LA::kMN, LB::kMN);
+    constexpr uint32_t idesc = idesc_tf32(GEMM_BM, BN, LA::kMN & 1, LB::kMN & 1);
     for (int it = 0; it < nkb; ++it) {
       const int s = it % STAGES;
       mbar_wait(bar_base + 8 * s, (it / STAGES) & 1);
@@ -732,7 +740,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
 #pragma unroll
         for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
           uint64_t ad = tile_desc<GEMM_BM, LA::kMN>(sa, kk);
-          uint64_t bd = tile_desc<BN, LB::kMN>(sa + A_BYTES, kk);
+          uint64_t bd = tile_desc<BN, LB::kMN>(sa + A_BYTES, kk);  // kMN also names the smem layout
           mma_tf32(tmem, ad, bd, idesc, (it | kk) ? 1u : 0u);
         }
         mma_commit(bar_base + 8 * (STAGES + s));

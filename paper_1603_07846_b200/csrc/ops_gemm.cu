@@ -51,11 +51,11 @@ Plan plan_gemm(int M, int N, int K, size_t ws_floats_avail) {
 }
 
 // Fixed-order split-K reduction: a block owns 32 consecutive outputs (row-major
-// m*N + n); its 8 warps sum the splits g, g+8, g+16, ... for every output, then
-// warp 0 adds the 8 partial sums in ascending g.  Deterministic.
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits,
+// m*N + n); its 16 warps sum the splits g, g+16, g+32, ... for every output,
+// then warp 0 adds the 16 partial sums in ascending g.  Deterministic.
+__global__ void __launch_bounds__(512) splitk_reduce_kernel(const float* __restrict__ ws, int splits,
                                                             long long split_stride, int M, int N, EpiArgs e) {
-  __shared__ float part[8][32];
+  __shared__ float part[16][32];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const long long idx = (long long)blockIdx.x * 32 + lane;
   const bool in = idx < (long long)M * N;
@@ -63,14 +63,14 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
   float acc = 0.f;
   if (in) {
     const float* p = ws + (long long)m * ((N + 3) & ~3) + n;
-    for (int s = g; s < splits; s += 8) acc += p[s * split_stride];
+    _Pragma("unroll 4") for (int s = g; s < splits; s += 16) acc += p[s * split_stride];
   }
   part[g][lane] = acc;
   __syncthreads();
   if (g != 0 || !in) return;
   float t = 0.f;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) t += part[j][lane];
+  for (int j = 0; j < 16; ++j) t += part[j][lane];
   if (m >= e.mvalid) {
     if (m == e.xrow) e.xout[n] = t;
     return;
@@ -120,7 +120,7 @@ cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int
   }
   if (e != cudaSuccess || p.splits == 1) return e;
   long long total = (long long)M * N;
-  splitk_reduce_kernel<<<(unsigned)((total + 31) / 32), 256, 0, st>>>(ws.ptr, p.splits, (long long)M * pad4(N), M, N,
+  splitk_reduce_kernel<<<(unsigned)((total + 31) / 32), 512, 0, st>>>(ws.ptr, p.splits, (long long)M * pad4(N), M, N,
                                                                        epi);
   return launched();
 }

@@ -67,6 +67,12 @@ struct sg_net {
   bool input_set = false;
   // graph
   bool graph_on = false;
+  // conv / inner-product -> ReLU fusion: the producer's epilogue applies the
+  // ReLU and writes the ReLU layer's blob (its own data blob aliases it)
+  bool fuse = true;
+  std::vector<float*> data_own;
+  std::vector<int> relu_of;     // producer i -> fused ReLU layer (or -1)
+  std::vector<char> fused_away; // ReLU layer whose forward is done by its producer
   cudaGraphExec_t gexec = nullptr;
   sg_updater* graph_upd = nullptr;
   long long graph_launches = 0;
@@ -175,7 +181,7 @@ sg_status forward_impl(sg_net* n, int i) {
         SG_LCH(copy2d(n->x_src, L.feat, n->data[i], L.ld, (int)L.rows, (int)L.feat, st));
       break;
     case SG_CONV:
-      SG_LCH(conv_fwd(conv_shape(L, *S), n->data[L.src], W, b, n->data[i], 0, n->ws, st));
+      SG_LCH(conv_fwd(conv_shape(L, *S), n->data[L.src], W, b, n->data[i], n->relu_of[i] >= 0, n->ws, st));
       break;
     case SG_POOL_MAX:
       SG_LCH(maxpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], n->mask[i], st));
@@ -188,14 +194,14 @@ sg_status forward_impl(sg_net* n, int i) {
                      n->data[i], n->scale[i], st));
       break;
     case SG_RELU:
-      SG_LCH(relu_fwd(n->data[L.src], n->data[i], L.blob_floats(), st));
+      if (!n->fused_away[i]) SG_LCH(relu_fwd(n->data[L.src], n->data[i], L.blob_floats(), st));
       break;
     case SG_SIGMOID:
       SG_LCH(sigmoid_fwd(n->data[L.src], n->data[i], L.blob_floats(), st));
       break;
     case SG_INNER_PRODUCT:
       SG_LCH(ip_fwd(feat_view(*S, n->data[L.src], L.kin), W, (int)L.kin, (int)L.nout, b,
-                    plain(n->data[i], (int)L.rows, (int)L.nout, L.ld), 0, n->ws, st));
+                    plain(n->data[i], (int)L.rows, (int)L.nout, L.ld), n->relu_of[i] >= 0, n->ws, st));
       break;
     case SG_CONCAT:
       SG_NCCL(ncclAllGather(n->data[L.src], n->data[i], (size_t)(S->rows * S->ld), ncclFloat, n->cl->comm_act, st));
@@ -500,6 +506,26 @@ sg_status param_export(sg_net* n, int p, int which, float* user) {
   return SG_OK;
 }
 
+void apply_fusion(sg_net* n) {
+  const Plan& P = PL(n);
+  const int nl = (int)P.layers.size();
+  n->data = n->data_own;
+  n->relu_of.assign(nl, -1);
+  n->fused_away.assign(nl, 0);
+  if (!n->fuse) return;
+  for (int j = 0; j < nl; ++j) {
+    const LayerPlan& R = P.layers[j];
+    if (R.kind != SG_RELU || R.src < 0) continue;
+    const int i = R.src;
+    const LayerPlan& L = P.layers[i];
+    if (L.kind != SG_CONV && L.kind != SG_INNER_PRODUCT) continue;
+    if (L.blob_floats() != R.blob_floats() || L.ld != R.ld || L.nblocks != R.nblocks) continue;
+    n->relu_of[i] = j;
+    n->fused_away[j] = 1;
+    n->data[i] = n->data[j];
+  }
+}
+
 sg_status destroy_net(sg_net* n) {
   if (!n) return SG_OK;
   cudaSetDevice(n->cl ? n->cl->device : 0);
@@ -589,6 +615,8 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
     n->sgr.push_back(g);
     n->sv.push_back(v);
   }
+  n->data_own = n->data;
+  apply_fusion(n);
   SG_CUDA(cudaDeviceSynchronize());
   return SG_OK;
 }
@@ -958,6 +986,19 @@ SG_API sg_status sg_net_op_times(sg_net* n, double* ms, int64_t* counts, int32_t
   if (reset) {
     std::fill(n->pacc.begin(), n->pacc.end(), 0.0);
     std::fill(n->pcnt.begin(), n->pcnt.end(), 0);
+  }
+  return SG_OK;
+}
+
+SG_API sg_status sg_net_set_fusion(sg_net* n, int32_t enable) {
+  SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  SG_CUDA(cudaStreamSynchronize(n->cs));
+  n->fuse = enable != 0;
+  apply_fusion(n);
+  if (n->gexec) {
+    cudaGraphExecDestroy(n->gexec);
+    n->gexec = nullptr;
   }
   return SG_OK;
 }

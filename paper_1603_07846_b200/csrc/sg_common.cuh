@@ -137,6 +137,12 @@ __device__ __forceinline__ uint64_t umma_desc_mn_sw128_32b(uint32_t saddr, uint3
   return (d & ~((uint64_t)7 << 61)) | ((uint64_t)1 << 61);
 }
 
+// No-swizzle (interleaved core matrices) descriptor, layout type 0.
+__device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = umma_desc_sw128(saddr, lbo, sbo);
+  return d & ~((uint64_t)7 << 61);
+}
+
 // Instruction descriptor: kind::tf32, fp32 accumulator, M = 128.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn_major, int b_mn_major) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn_major << 15) | ((uint32_t)b_mn_major << 16) |

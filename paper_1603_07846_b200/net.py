@@ -221,6 +221,9 @@ class Net:
     def sync(self):
         L.sg_net_sync(self.h)
 
+    def set_fusion(self, on=True):
+        L.sg_net_set_fusion(self.h, 1 if on else 0)
+
     def enable_graph(self, on=True):
         L.sg_net_enable_graph(self.h, 1 if on else 0)
 

@@ -89,6 +89,7 @@ def local_blob(run, i, which=0):
 
 def run_layer_isolated(net, b, steps=1):
     run = Run(net, b)
+    run.n.set_fusion(False)   # every layer's own output blob is materialised
     try:
         x, lab = generate.batch(net, b, 0)
         run.step(0, x, lab)
@@ -320,3 +321,20 @@ def test_alg1_layer_by_layer_api_matches_train_one_batch():
     finally:
         a.close()
         c.close()
+
+
+def test_relu_fusion_bit_exact():
+    net = configs.alexnet(hybrid=False)
+    b = 2
+    runs = [Run(net, b), Run(net, b)]
+    runs[1].n.set_fusion(False)
+    try:
+        for t in range(2):
+            x, lab = generate.batch(net, b, t)
+            assert runs[0].step(t, x, lab) == runs[1].step(t, x, lab)
+        pa, pb = runs[0].n.get_params(shapes_of(runs[0].p0)), runs[1].n.get_params(shapes_of(runs[1].p0))
+        for k in pa:
+            assert np.array_equal(pa[k], pb[k]), k
+    finally:
+        for r in runs:
+            r.close()

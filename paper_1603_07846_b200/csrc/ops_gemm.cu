@@ -141,8 +141,9 @@ cudaError_t run_gemm_mk(MA mkA, MB mkB, int M, int N, int K, EpiArgs epi, Worksp
 PFN_cuTensorMapEncodeTiled_v12000 g_enc_tiled = nullptr;
 PFN_cuTensorMapEncodeIm2col_v12000 g_enc_im2col = nullptr;
 
-// TMA operand paths per operation (measured: TMA wins for the im2col conv
-// forward / data gradient, cp.async for the rest; SG_TMA_OPS overrides):
+// TMA operand paths per operation (default all; an operation falls back to the
+// cp.async gather when its shapes do not fit TMA, e.g. 4-channel first layers;
+// SG_TMA_OPS overrides for A/B measurements):
 // bit 0 conv fwd, 1 conv dgrad, 2 conv wgrad, 3 inner product, 4 plain GEMM.
 int tma_ops() {
   static int ops = -1;

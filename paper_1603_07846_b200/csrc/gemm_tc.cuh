@@ -38,7 +38,6 @@ namespace sg {
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 32;  // fp32 elements = 128 bytes = one swizzle row
 constexpr int GEMM_PRODUCERS = 256;
-constexpr int GEMM_THREADS = GEMM_PRODUCERS + 32;
 
 // {1, 0, 0, 0}: source of the ones-row chunk (global memory, cp.async source).
 __device__ __align__(16) static const float g_one4[4] = {1.f, 0.f, 0.f, 0.f};
@@ -412,15 +411,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 
 // Constant MN atoms: rows [valid, ...) are zero, except row ones_row (= 1).
 template <int T>
-__device__ __forceinline__ void prefill_const_atoms(uint32_t sm, int row0, int valid, int ones_row, int tid) {
-  float* base = nullptr;
-  (void)base;
+__device__ __forceinline__ void prefill_const_atoms(uint32_t sm, int row0, int valid, int ones_row, int t, int nt) {
 #pragma unroll 1
   for (int a = 0; a < T / 32; ++a) {
     const int r0 = row0 + 32 * a;
-    if (r0 + 32 <= valid || (r0 < valid)) continue;
+    if (r0 < valid) continue;
     // 32 k-lines x 128 B; the ones row sits at MN position (ones_row - r0)
-    for (int i = tid; i < 32 * 32; i += GEMM_PRODUCERS) {
+    for (int i = t; i < 32 * 32; i += nt) {
       const int kr = i >> 5, mn = i & 31;
       const float v = (r0 + mn == ones_row) ? 1.f : 0.f;
       const uint32_t addr = sm + a * (GEMM_BK * 128) + kr * 128 + ((((mn >> 3) ^ (kr & 3))) << 5) + (mn & 7) * 4;
@@ -436,7 +433,11 @@ struct TmaK {
   CUtensorMap map;
   int blocked, cb;  // blocked: 3-D map {cb, rows, nblk}
   template <int T>
-  __device__ __forceinline__ void prefill(uint32_t, int, int) const {}
+  __device__ __forceinline__ bool needs_prefill(int) const {
+    return false;
+  }
+  template <int T>
+  __device__ __forceinline__ void prefill(uint32_t, int, int, int) const {}
   template <int T>
   __device__ __forceinline__ void issue(uint32_t sm, int row0, int k0, uint32_t bar) const {
     mbar_expect_tx(bar, T * 128);
@@ -456,8 +457,12 @@ struct TmaMN {
   int valid, ones_row;  // atoms starting at >= valid are constant (prefilled)
   int atoms;            // whole tile in one box: 3-D view {32, rows, cols/32}, box {32, 32, T/32}
   template <int T>
-  __device__ __forceinline__ void prefill(uint32_t sm, int row0, int tid) const {
-    if (!atoms) prefill_const_atoms<T>(sm, row0, valid, ones_row, tid);
+  __device__ __forceinline__ bool needs_prefill(int row0) const {
+    return !atoms && row0 + T > valid;
+  }
+  template <int T>
+  __device__ __forceinline__ void prefill(uint32_t sm, int row0, int t, int nt) const {
+    prefill_const_atoms<T>(sm, row0, valid, ones_row, t, nt);
   }
   template <int T>
   __device__ __forceinline__ void issue(uint32_t sm, int mn0, int k0, uint32_t bar) const {
@@ -493,7 +498,11 @@ struct TmaIm2col {
   int flip;
   FastDiv fC, fS, fHW, fW;
   template <int T>
-  __device__ __forceinline__ void prefill(uint32_t, int, int) const {}
+  __device__ __forceinline__ bool needs_prefill(int) const {
+    return false;
+  }
+  template <int T>
+  __device__ __forceinline__ void prefill(uint32_t, int, int, int) const {}
   template <int T>
   __device__ __forceinline__ void issue(uint32_t sm, int m0, int k0, uint32_t bar) const {
     const int rs = fC.div(k0), c0 = k0 - rs * C;
@@ -517,7 +526,11 @@ struct TmaDgradB {
   int C, Co;
   FastDiv fCo;
   template <int T>
-  __device__ __forceinline__ void prefill(uint32_t, int, int) const {}
+  __device__ __forceinline__ bool needs_prefill(int) const {
+    return false;
+  }
+  template <int T>
+  __device__ __forceinline__ void prefill(uint32_t, int, int, int) const {}
   template <int T>
   __device__ __forceinline__ void issue(uint32_t sm, int c0, int k0, uint32_t bar) const {
     const int rs = fCo.div(k0), co0 = k0 - rs * Co;
@@ -541,8 +554,12 @@ struct TmaWgradA {
   int valid, ones_row;
   FastDiv fC, fS, fHoWo, fWo;
   template <int T>
-  __device__ __forceinline__ void prefill(uint32_t sm, int row0, int tid) const {
-    prefill_const_atoms<T>(sm, row0, valid, ones_row, tid);
+  __device__ __forceinline__ bool needs_prefill(int row0) const {
+    return row0 + T > valid;
+  }
+  template <int T>
+  __device__ __forceinline__ void prefill(uint32_t sm, int row0, int t, int nt) const {
+    prefill_const_atoms<T>(sm, row0, valid, ones_row, t, nt);
   }
   template <int T>
   __device__ __forceinline__ void issue(uint32_t sm, int kg0, int k0, uint32_t bar) const {
@@ -624,14 +641,36 @@ constexpr int gemm_smem_bytes() {
   return STAGES * (GEMM_BM * GEMM_BK * 4 + BN * GEMM_BK * 4) + 1024 /*align*/ + 256 /*barriers*/;
 }
 
+// Persistent warp-specialised kernel.  Work items = (M tile, N tile, K split),
+// strided over the CTAs; the operand pipeline runs across work items without
+// draining, and the accumulator is double-buffered in TMEM so the epilogue of
+// one item overlaps the main loop of the next.
+//   warps 0-7  : producers (cp.async: all 256 threads; TMA: warp 0, lane 0 issues)
+//   warp 8     : MMA issuer (lane 0)
+//   warps 9-16 : epilogue (TMEM lane group warp % 4; column half (warp - 9) / 4)
+constexpr int GEMM_EPI_WARPS = 8;
+constexpr int GEMM_ALL_THREADS = GEMM_PRODUCERS + 32 + GEMM_EPI_WARPS * 32;
+
+struct WorkDecode {
+  int mt, nt, splits;
+  __device__ __forceinline__ void get(int w, int& mi, int& ni, int& si) const {
+    // M tile fastest: CTAs running side by side share the B tile (and its L2 lines)
+    mi = w % mt;
+    const int r = w / mt;
+    ni = r % nt;
+    si = r / nt;
+  }
+};
+
 template <int BN, int STAGES, class LA, class LB>
-__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs<LA, LB> args) {
+__global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs<LA, LB> args) {
   constexpr int A_BYTES = GEMM_BM * GEMM_BK * 4;
   constexpr int B_BYTES = BN * GEMM_BK * 4;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   constexpr int LAG = STAGES > 2 ? STAGES - 2 : 1;
   constexpr int MMA_WARP = GEMM_PRODUCERS / 32;
+  constexpr int EPI_WARP0 = MMA_WARP + 1;
   static_assert(BN % 32 == 0 && BN <= 256, "BN");
   static_assert(LA::kTMA == LB::kTMA, "both operands TMA or both cp.async");
   constexpr bool TMA = LA::kTMA;
@@ -639,38 +678,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t bar_base = sbase + STAGES * STAGE_BYTES;
-  // full[s] at bar_base + 8s, empty[s] at +8(STAGES+s), accum at +16 STAGES, tmem slot after.
-  const uint32_t accum_bar = bar_base + 16 * STAGES;
-  const uint32_t tmem_slot = accum_bar + 8;
+  // full[s] at bar_base + 8s, empty[s] at +8(STAGES+s), tfull[b] at +16 STAGES + 8b,
+  // tempty[b] at +16 STAGES + 16 + 8b, tmem slot after.
+  const uint32_t tfull_bar = bar_base + 16 * STAGES;
+  const uint32_t tempty_bar = tfull_bar + 16;
+  const uint32_t tmem_slot = tempty_bar + 16;
   uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const int m0 = blockIdx.x * GEMM_BM;
-  const int n0 = blockIdx.y * BN;
+  const int warp = tid >> 5, lane = tid & 31;
   const int nkb_total = (args.K + GEMM_BK - 1) / GEMM_BK;
-  const int kb_begin = blockIdx.z * args.kb_per_split;
-  int kb_end = kb_begin + args.kb_per_split;
-  if (kb_end > nkb_total) kb_end = nkb_total;
-  const int nkb = kb_end - kb_begin;
+  const WorkDecode wd{(args.M + GEMM_BM - 1) / GEMM_BM, (args.N + BN - 1) / BN,
+                      (nkb_total + args.kb_per_split - 1) / (args.kb_per_split > 0 ? args.kb_per_split : 1)};
+  const int nwork = wd.mt * wd.nt * (wd.splits > 0 ? wd.splits : 1);
+  auto kb_range = [&](int si, int& kb0, int& nkb) {
+    kb0 = si * args.kb_per_split;
+    int e = kb0 + args.kb_per_split;
+    if (e > nkb_total) e = nkb_total;
+    nkb = e - kb0;
+  };
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(bar_base + 8 * s, TMA ? 1 : GEMM_PRODUCERS);  // TMA thread / every producer thread
-      mbar_init(bar_base + 8 * (STAGES + s), 1);       // tcgen05.commit
+      mbar_init(bar_base + 8 * (STAGES + s), 1);              // tcgen05.commit
     }
-    mbar_init(accum_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull_bar + 8 * b, 1);                        // tcgen05.commit
+      mbar_init(tempty_bar + 8 * b, GEMM_EPI_WARPS * 32);     // every epilogue thread
+    }
     fence_barrier_init();
   }
   if (warp == MMA_WARP) tmem_alloc<TMEM_COLS>(tmem_slot);
   if constexpr (TMA) {
-    if (warp < MMA_WARP) {
-      for (int s = 0; s < STAGES; ++s) {
-        args.a.template prefill<GEMM_BM>(sbase + s * STAGE_BYTES, m0, tid);
-        args.b.template prefill<BN>(sbase + s * STAGE_BYTES + A_BYTES, n0, tid);
-      }
-      fence_proxy_async_smem();
-    }
     if (tid == 0) {
       prefetch_tmap(&args.a.map);
       prefetch_tmap(&args.b.map);
@@ -681,152 +721,212 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_tc_kernel(const __grid_c
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
 
-  const int lane = tid & 31;
   if (warp < MMA_WARP) {
+    // ------------------------------- producers -------------------------------
     if constexpr (TMA) {
       if (warp == 0) {
-        // ----------------- TMA producer: warp 0, lane 0 issues (warp-uniform waits) -----------------
-        for (int it = 0; it < nkb; ++it) {
-          const int s = it % STAGES;
-          const int round = it / STAGES;
-          if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
-          if (lane == 0) {
+        int it = 0;
+        int tagA[STAGES], tagB[STAGES];  // row0 the stage's constant atoms were written for
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) tagA[s] = tagB[s] = -1;
+        for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+          int mi, ni, si, kb0, nkb;
+          wd.get(w, mi, ni, si);
+          kb_range(si, kb0, nkb);
+          const int m0 = mi * GEMM_BM, n0 = ni * BN;
+          for (int j = 0; j < nkb; ++j, ++it) {
+            const int s = it % STAGES;
+            const int round = it / STAGES;
+            if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
             const uint32_t sa = sbase + s * STAGE_BYTES;
-            const uint32_t full = bar_base + 8 * s;
-            const int k0 = (kb_begin + it) * GEMM_BK;
-            args.a.template issue<GEMM_BM>(sa, m0, k0, full);
-            args.b.template issue<BN>(sa + A_BYTES, n0, k0, full);
-            mbar_arrive(full);
+            // constant operand atoms (zeros / the bias ones-row) are written by the warp
+            bool wrote = false;
+#pragma unroll
+            for (int q = 0; q < STAGES; ++q) {
+              if (q != s) continue;
+              // (a tag names the row0 whose constant atoms the stage holds; a tile
+              // without constant atoms lets TMA overwrite them, clearing the tag)
+              if (!args.a.template needs_prefill<GEMM_BM>(m0)) {
+                tagA[q] = -1;
+              } else if (tagA[q] != m0) {
+                args.a.template prefill<GEMM_BM>(sa, m0, lane, 32);
+                tagA[q] = m0;
+                wrote = true;
+              }
+              if (!args.b.template needs_prefill<BN>(n0)) {
+                tagB[q] = -1;
+              } else if (tagB[q] != n0) {
+                args.b.template prefill<BN>(sa + A_BYTES, n0, lane, 32);
+                tagB[q] = n0;
+                wrote = true;
+              }
+            }
+            if (wrote) {
+              fence_proxy_async_smem();
+              __syncwarp();
+            }
+            if (lane == 0) {
+              const uint32_t full = bar_base + 8 * s;
+              const int k0 = (kb0 + j) * GEMM_BK;
+              args.a.template issue<GEMM_BM>(sa, m0, k0, full);
+              args.b.template issue<BN>(sa + A_BYTES, n0, k0, full);
+              mbar_arrive(full);
+            }
+            __syncwarp();
           }
-          __syncwarp();
         }
       }
     } else {
-      // --------------------------- cp.async producers ---------------------------
-      typename LA::template State<GEMM_BM> sa_st;
-      typename LB::template State<BN> sb_st;
-      args.a.template init<GEMM_BM>(sa_st, m0, tid);
-      args.b.template init<BN>(sb_st, n0, tid);
-      for (int it = 0; it < nkb; ++it) {
-        const int s = it % STAGES;
-        const int round = it / STAGES;
-        if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
-        const uint32_t sa = sbase + s * STAGE_BYTES;
-        const int k0 = (kb_begin + it) * GEMM_BK;
-        args.a.template load<GEMM_BM>(sa_st, sa, k0, tid);
-        args.b.template load<BN>(sb_st, sa + A_BYTES, k0, tid);
-        cp_async_commit();
-        if (it >= LAG) {
-          // this thread's copies for k-block it-LAG have landed: make them visible
-          // to the tensor-core (async) proxy, then release the stage.
-          cp_async_wait<LAG>();
-          fence_proxy_async_smem();
-          mbar_arrive(bar_base + 8 * ((it - LAG) % STAGES));
+      int it = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        int mi, ni, si, kb0, nkb;
+        wd.get(w, mi, ni, si);
+        kb_range(si, kb0, nkb);
+        typename LA::template State<GEMM_BM> sa_st;
+        typename LB::template State<BN> sb_st;
+        args.a.template init<GEMM_BM>(sa_st, mi * GEMM_BM, tid);
+        args.b.template init<BN>(sb_st, ni * BN, tid);
+        for (int j = 0; j < nkb; ++j, ++it) {
+          const int s = it % STAGES;
+          const int round = it / STAGES;
+          if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
+          const uint32_t sa = sbase + s * STAGE_BYTES;
+          const int k0 = (kb0 + j) * GEMM_BK;
+          args.a.template load<GEMM_BM>(sa_st, sa, k0, tid);
+          args.b.template load<BN>(sb_st, sa + A_BYTES, k0, tid);
+          cp_async_commit();
+          if (it >= LAG) {
+            // this thread's copies of stage it-LAG have landed: make them visible
+            // to the tensor-core (async) proxy, then release the stage.
+            cp_async_wait<LAG>();
+            fence_proxy_async_smem();
+            mbar_arrive(bar_base + 8 * ((it - LAG) % STAGES));
+          }
         }
       }
       cp_async_wait<0>();
       fence_proxy_async_smem();
-      for (int j = (nkb > LAG ? nkb - LAG : 0); j < nkb; ++j) mbar_arrive(bar_base + 8 * (j % STAGES));
+      for (int j = (it > LAG ? it - LAG : 0); j < it; ++j) mbar_arrive(bar_base + 8 * (j % STAGES));
     }
-  } else {
-    // ------------- MMA issuer: the whole warp waits, lane 0 issues -------------
+  } else if (warp == MMA_WARP) {
+    // --------------- MMA issuer: the whole warp waits, lane 0 issues ---------------
     constexpr uint32_t idesc = idesc_tf32(GEMM_BM, BN, LA::kMN & 1, LB::kMN & 1);
-    for (int it = 0; it < nkb; ++it) {
-      const int s = it % STAGES;
-      mbar_wait(bar_base + 8 * s, (it / STAGES) & 1);
+    int it = 0, local = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++local) {
+      int mi, ni, si, kb0, nkb;
+      wd.get(w, mi, ni, si);
+      kb_range(si, kb0, nkb);
+      const int b = local & 1;
+      const int use = local >> 1;  // how many times buffer b was used before
+      if (use > 0) mbar_wait(tempty_bar + 8 * b, (use - 1) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t sa = sbase + s * STAGE_BYTES;
+      const uint32_t acc = tmem + b * BN;
+      for (int j = 0; j < nkb; ++j, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(bar_base + 8 * s, (it / STAGES) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = sbase + s * STAGE_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
-          uint64_t ad = tile_desc<GEMM_BM, LA::kMN>(sa, kk);
-          uint64_t bd = tile_desc<BN, LB::kMN>(sa + A_BYTES, kk);  // kMN also names the smem layout
-          mma_tf32(tmem, ad, bd, idesc, (it | kk) ? 1u : 0u);
+          for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
+            uint64_t ad = tile_desc<GEMM_BM, LA::kMN>(sa, kk);
+            uint64_t bd = tile_desc<BN, LB::kMN>(sa + A_BYTES, kk);  // kMN also names the smem layout
+            mma_tf32(acc, ad, bd, idesc, (j | kk) ? 1u : 0u);
+          }
+          mma_commit(bar_base + 8 * (STAGES + s));
         }
-        mma_commit(bar_base + 8 * (STAGES + s));
+        __syncwarp();
       }
+      if (lane == 0) mma_commit(tfull_bar + 8 * b);
       __syncwarp();
     }
-    if (lane == 0) mma_commit(accum_bar);
-    __syncwarp();
-  }
-
-  // -------------------------------- epilogue --------------------------------
-  if (warp < MMA_WARP) {
-    if (nkb > 0) mbar_wait(accum_bar, 0);
-    tc_fence_after();
-    const int lg = warp & 3;                 // TMEM lane group this warp may access
-    const int row = m0 + lg * 32 + (tid & 31);
-    const EpiArgs& e = args.epi;
-    const uint32_t tbase = tmem + ((uint32_t)(lg * 32) << 16);
-    const bool plain_vec = !e.trans && e.cb >= args.N && (e.ld & 3) == 0 && !e.bias_on_m;
+  } else {
+    // ---------------------------------- epilogue ----------------------------------
+    const int lg = warp & 3;  // TMEM lane group this warp may access
     constexpr int HALF = BN / 2;
-    const int cbeg = (warp >> 2) * HALF;
+    const int cbeg = ((warp - EPI_WARP0) >> 2) * HALF;
+    const EpiArgs& e = args.epi;
+    const bool plain_vec = !e.trans && e.cb >= args.N && (e.ld & 3) == 0 && !e.bias_on_m;
+    int local = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++local) {
+      int mi, ni, si, kb0, nkb;
+      wd.get(w, mi, ni, si);
+      kb_range(si, kb0, nkb);
+      const int b = local & 1;
+      mbar_wait(tfull_bar + 8 * b, (local >> 1) & 1);
+      tc_fence_after();
+      const int m0 = mi * GEMM_BM, n0 = ni * BN;
+      const int row = m0 + lg * 32 + lane;
+      const uint32_t tb = tmem + b * BN + ((uint32_t)(lg * 32) << 16);
 #pragma unroll 1
-    for (int c0 = cbeg; c0 < cbeg + HALF; c0 += 16) {
-      if (n0 + c0 >= args.N) break;
-      float v[16];
-      if (nkb > 0) {
-        tmem_ld16(tbase + c0, v);
-      } else {
+      for (int c0 = cbeg; c0 < cbeg + HALF; c0 += 16) {
+        if (n0 + c0 >= args.N) break;
+        float v[16];
+        if (nkb > 0) {
+          tmem_ld16(tb + c0, v);
+        } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.f;
-      }
-      if (row >= args.M) continue;
-      if (e.ws) {
-        float* dst = e.ws + blockIdx.z * e.ws_split_stride + (long long)row * e.ws_ld + n0 + c0;
-#pragma unroll
-        for (int i = 0; i < 16; i += 4) {
-          if (n0 + c0 + i + 3 < args.N) {
-            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          } else {
-            for (int t = 0; t < 4; ++t)
-              if (n0 + c0 + i + t < args.N) dst[i + t] = v[i + t];
-          }
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
         }
-        continue;
-      }
-      if (row >= e.mvalid) {
-        if (row == e.xrow) {
+        if (row >= args.M) continue;
+        if (e.ws) {
+          float* dst = e.ws + (long long)si * e.ws_split_stride + (long long)row * e.ws_ld + n0 + c0;
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (n0 + c0 + i < args.N) e.xout[n0 + c0 + i] = v[i];
-        }
-        continue;
-      }
-      if (plain_vec && n0 + c0 + 15 < args.N) {
-        float* dst = e.p + (long long)row * e.ld + n0 + c0;
-#pragma unroll
-        for (int i = 0; i < 16; i += 4) {
-          float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          if (e.bias) {
-            o.x += e.bias[n0 + c0 + i];
-            o.y += e.bias[n0 + c0 + i + 1];
-            o.z += e.bias[n0 + c0 + i + 2];
-            o.w += e.bias[n0 + c0 + i + 3];
+          for (int i = 0; i < 16; i += 4) {
+            if (n0 + c0 + i + 3 < args.N) {
+              *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            } else {
+              for (int t = 0; t < 4; ++t)
+                if (n0 + c0 + i + t < args.N) dst[i + t] = v[i + t];
+            }
           }
-          if (e.relu) {
-            o.x = fmaxf(o.x, 0.f);
-            o.y = fmaxf(o.y, 0.f);
-            o.z = fmaxf(o.z, 0.f);
-            o.w = fmaxf(o.w, 0.f);
-          }
-          *reinterpret_cast<float4*>(dst + i) = o;
+          continue;
         }
-        continue;
-      }
+        if (row >= e.mvalid) {
+          if (row == e.xrow) {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int col = n0 + c0 + i;
-        if (col >= args.N) break;
-        float o = v[i];
-        if (e.bias) o += e.bias_on_m ? e.bias[row] : e.bias[col];
-        if (e.relu) o = fmaxf(o, 0.f);
-        if (e.trans)
-          *out_at(e, col, row, e.mvalid) = o;
-        else
-          *out_at(e, row, col, args.N) = o;
+            for (int i = 0; i < 16; ++i)
+              if (n0 + c0 + i < args.N) e.xout[n0 + c0 + i] = v[i];
+          }
+          continue;
+        }
+        if (plain_vec && n0 + c0 + 15 < args.N) {
+          float* dst = e.p + (long long)row * e.ld + n0 + c0;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            if (e.bias) {
+              o.x += e.bias[n0 + c0 + i];
+              o.y += e.bias[n0 + c0 + i + 1];
+              o.z += e.bias[n0 + c0 + i + 2];
+              o.w += e.bias[n0 + c0 + i + 3];
+            }
+            if (e.relu) {
+              o.x = fmaxf(o.x, 0.f);
+              o.y = fmaxf(o.y, 0.f);
+              o.z = fmaxf(o.z, 0.f);
+              o.w = fmaxf(o.w, 0.f);
+            }
+            *reinterpret_cast<float4*>(dst + i) = o;
+          }
+          continue;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int col = n0 + c0 + i;
+          if (col >= args.N) break;
+          float o = v[i];
+          if (e.bias) o += e.bias_on_m ? e.bias[row] : e.bias[col];
+          if (e.relu) o = fmaxf(o, 0.f);
+          if (e.trans)
+            *out_at(e, col, row, e.mvalid) = o;
+          else
+            *out_at(e, row, col, args.N) = o;
+        }
       }
+      // this buffer's accumulator has been read: release it to the MMA warp
+      tc_fence_before();
+      mbar_arrive(tempty_bar + 8 * b);
     }
   }
   tc_fence_before();

@@ -50,27 +50,12 @@ Plan plan_gemm(int M, int N, int K, size_t ws_floats_avail) {
   return p;
 }
 
-// Fixed-order split-K reduction: a block owns 32 consecutive outputs (row-major
-// m*N + n); its 16 warps sum the splits g, g+16, g+32, ... for every output,
-// then warp 0 adds the 16 partial sums in ascending g.  Deterministic.
-__global__ void __launch_bounds__(512) splitk_reduce_kernel(const float* __restrict__ ws, int splits,
-                                                            long long split_stride, int M, int N, EpiArgs e) {
-  __shared__ float part[16][32];
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const long long idx = (long long)blockIdx.x * 32 + lane;
-  const bool in = idx < (long long)M * N;
-  const int m = in ? (int)(idx / N) : 0, n = in ? (int)(idx - (long long)m * N) : 0;
-  float acc = 0.f;
-  if (in) {
-    const float* p = ws + (long long)m * ((N + 3) & ~3) + n;
-    _Pragma("unroll 4") for (int s = g; s < splits; s += 16) acc += p[s * split_stride];
-  }
-  part[g][lane] = acc;
-  __syncthreads();
-  if (g != 0 || !in) return;
-  float t = 0.f;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) t += part[j][lane];
+// Fixed-order split-K reduction.  A block of G warps owns 128 consecutive
+// entries of the padded workspace row space (m * pad4(N) + n, one float4 per
+// lane); warp g sums the splits g, g+G, g+2G, ... in ascending order, then warp 0
+// adds the G partial sums in ascending g.  G = min(16, splits) depends on the
+// shape only, so the result is deterministic.
+__device__ __forceinline__ void reduce_store(const EpiArgs& e, int m, int n, int N, float t) {
   if (m >= e.mvalid) {
     if (m == e.xrow) e.xout[n] = t;
     return;
@@ -81,6 +66,63 @@ __global__ void __launch_bounds__(512) splitk_reduce_kernel(const float* __restr
     *out_at(e, n, m, e.mvalid) = t;
   else
     *out_at(e, m, n, N) = t;
+}
+
+__global__ void __launch_bounds__(512) splitk_reduce_kernel(const float* __restrict__ ws, int splits,
+                                                            long long split_stride, int M, int N, EpiArgs e) {
+  __shared__ float4 part[16][32];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5, G = blockDim.x >> 5;
+  const int ldw = (N + 3) & ~3;
+  const long long q = ((long long)blockIdx.x * 32 + lane) * 4;  // first padded entry of this lane
+  const bool in = q < (long long)M * ldw;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (in) {
+    const float* p = ws + q;
+#pragma unroll 4
+    for (int s = g; s < splits; s += G) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p + s * split_stride));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+  }
+  if (G > 1) {
+    part[g][lane] = acc;
+    __syncthreads();
+    if (g != 0) return;
+    acc = part[0][lane];
+    for (int j = 1; j < G; ++j) {
+      const float4 v = part[j][lane];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+  }
+  if (!in) return;
+  const int m = (int)(q / ldw), n = (int)(q - (long long)m * ldw);
+  const float r[4] = {acc.x, acc.y, acc.z, acc.w};
+  if (!e.trans && e.cb >= N && !e.bias_on_m && m < e.mvalid && n + 3 < N && (e.ld & 3) == 0) {
+    float4 o = acc;
+    if (e.bias) {
+      o.x += e.bias[n];
+      o.y += e.bias[n + 1];
+      o.z += e.bias[n + 2];
+      o.w += e.bias[n + 3];
+    }
+    if (e.relu) {
+      o.x = fmaxf(o.x, 0.f);
+      o.y = fmaxf(o.y, 0.f);
+      o.z = fmaxf(o.z, 0.f);
+      o.w = fmaxf(o.w, 0.f);
+    }
+    *reinterpret_cast<float4*>(e.p + (long long)m * e.ld + n) = o;
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (n + i < N) reduce_store(e, m, n + i, N, r[i]);
 }
 
 template <int BN, class LA, class LB>
@@ -94,8 +136,8 @@ cudaError_t launch_bn(const GemmArgs<LA, LB>& args, const Plan& p, cudaStream_t 
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(p.mt, p.nt, p.splits);
-  kern<<<grid, GEMM_THREADS, SMEM, st>>>(args);
+  const int nwork = p.mt * p.nt * p.splits;
+  kern<<<std::min(nwork, kNumSMs), GEMM_ALL_THREADS, SMEM, st>>>(args);
   return launched();
 }
 
@@ -119,9 +161,10 @@ cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int
     default: e = launch_bn<256>(args, p, st); break;
   }
   if (e != cudaSuccess || p.splits == 1) return e;
-  long long total = (long long)M * N;
-  splitk_reduce_kernel<<<(unsigned)((total + 31) / 32), 512, 0, st>>>(ws.ptr, p.splits, (long long)M * pad4(N), M, N,
-                                                                       epi);
+  const long long total4 = (long long)M * pad4(N) / 4;
+  const int G = std::min(16, p.splits);
+  splitk_reduce_kernel<<<(unsigned)((total4 + 31) / 32), 32 * G, 0, st>>>(ws.ptr, p.splits, (long long)M * pad4(N),
+                                                                         M, N, epi);
   return launched();
 }
 

@@ -720,6 +720,8 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot_ptr;
+  // the prologue above overlapped the previous kernel; its outputs are read below
+  pdl_entry();
 
   if (warp < MMA_WARP) {
     // ------------------------------- producers -------------------------------

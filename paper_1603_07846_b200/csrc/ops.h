@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 namespace sg {
 
 // Number of kernels launched by this library (all launchers bump it).
@@ -12,6 +14,29 @@ extern long long g_kernel_launches;
 inline cudaError_t launched() {
   ++g_kernel_launches;
   return cudaGetLastError();
+}
+
+// Programmatic dependent launch on/off (SG_PDL, default on).
+bool pdl_enabled();
+
+// Launch `k` on `st` with programmatic stream serialisation, so its prologue
+// overlaps the tail of the previous kernel (every kernel of this library starts
+// with pdl_wait(); see sg_common.cuh).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+  ++g_kernel_launches;
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // Scratch for deterministic split-K partials (owned by the caller).

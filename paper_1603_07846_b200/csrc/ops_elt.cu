@@ -7,6 +7,7 @@
 #include <cstdint>
 
 #include "ops.h"
+#include "sg_common.cuh"
 
 namespace sg {
 
@@ -21,6 +22,7 @@ inline unsigned blocks_for(long long n, int per_block) {
 // ------------------------------------------------------------ elementwise --
 template <class F>
 __global__ void map1_kernel(const float* __restrict__ x, float* __restrict__ y, long long n, F f) {
+  pdl_entry();
   long long n4 = n >> 2;
   const float4* x4 = reinterpret_cast<const float4*>(x);
   float4* y4 = reinterpret_cast<float4*>(y);
@@ -36,6 +38,7 @@ __global__ void map1_kernel(const float* __restrict__ x, float* __restrict__ y, 
 template <class F>
 __global__ void map2_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ y,
                             long long n, F f) {
+  pdl_entry();
   long long n4 = n >> 2;
   const float4* a4 = reinterpret_cast<const float4*>(a);
   const float4* b4 = reinterpret_cast<const float4*>(b);
@@ -72,15 +75,13 @@ template <class F>
 cudaError_t launch_map1(const float* x, float* y, long long n, F f, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (!aligned16(x) || !aligned16(y)) return cudaErrorMisalignedAddress;
-  map1_kernel<<<blocks_for(n / 4 + 1, 256), 256, 0, st>>>(x, y, n, f);
-  return launched();
+  return launch_k(map1_kernel<F>, blocks_for(n / 4 + 1, 256), 256, 0, st, x, y, n, f);
 }
 template <class F>
 cudaError_t launch_map2(const float* a, const float* b, float* y, long long n, F f, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (!aligned16(a) || !aligned16(b) || !aligned16(y)) return cudaErrorMisalignedAddress;
-  map2_kernel<<<blocks_for(n / 4 + 1, 256), 256, 0, st>>>(a, b, y, n, f);
-  return launched();
+  return launch_k(map2_kernel<F>, blocks_for(n / 4 + 1, 256), 256, 0, st, a, b, y, n, f);
 }
 
 // ---------------------------------------------------------------- pooling --
@@ -88,6 +89,7 @@ cudaError_t launch_map2(const float* a, const float* b, float* y, long long n, F
 // the argmax is stored as the uint8 offset (h - h0)*k + (w - w0).
 __global__ void maxpool_fwd_kernel(PoolShape s, const float* __restrict__ x, float* __restrict__ y,
                                    uint8_t* __restrict__ arg) {
+  pdl_entry();
   const int C4 = s.C >> 2;
   long long total = (long long)s.N * s.Ho * s.Wo * C4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -120,6 +122,7 @@ __global__ void maxpool_fwd_kernel(PoolShape s, const float* __restrict__ x, flo
 // of every window whose argmax is this element, windows in ascending (oh, ow).
 __global__ void maxpool_bwd_kernel(PoolShape s, const float* __restrict__ dy, const uint8_t* __restrict__ arg,
                                    float* __restrict__ dx) {
+  pdl_entry();
   const int C4 = s.C >> 2;
   long long total = (long long)s.N * s.H * s.W * C4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -150,6 +153,7 @@ __global__ void maxpool_bwd_kernel(PoolShape s, const float* __restrict__ dy, co
 }
 
 __global__ void avgpool_fwd_kernel(PoolShape s, const float* __restrict__ x, float* __restrict__ y) {
+  pdl_entry();
   const int C4 = s.C >> 2;
   long long total = (long long)s.N * s.Ho * s.Wo * C4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -174,6 +178,7 @@ __global__ void avgpool_fwd_kernel(PoolShape s, const float* __restrict__ x, flo
 }
 
 __global__ void avgpool_bwd_kernel(PoolShape s, const float* __restrict__ dy, float* __restrict__ dx) {
+  pdl_entry();
   const int C4 = s.C >> 2;
   long long total = (long long)s.N * s.H * s.W * C4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -203,6 +208,7 @@ __global__ void avgpool_bwd_kernel(PoolShape s, const float* __restrict__ dy, fl
 }
 
 __global__ void argmax_expand_kernel(PoolShape s, const uint8_t* __restrict__ arg, int32_t* __restrict__ out) {
+  pdl_entry();
   long long total = (long long)s.N * s.Ho * s.Wo * s.C;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     long long t = i / s.C;
@@ -219,6 +225,7 @@ __device__ __forceinline__ float pow_neg(float base, float beta) { return exp2f(
 
 __global__ void lrn_fwd_kernel(LrnShape s, const float* __restrict__ x, float* __restrict__ y,
                                float* __restrict__ scale) {
+  pdl_entry();
   long long total = s.pixels * s.C;
   const int half = s.n / 2;
   const float an = s.alpha / (float)s.n;
@@ -236,6 +243,7 @@ __global__ void lrn_fwd_kernel(LrnShape s, const float* __restrict__ x, float* _
 
 __global__ void lrn_bwd_kernel(LrnShape s, const float* __restrict__ x, const float* __restrict__ y,
                                const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ dx) {
+  pdl_entry();
   long long total = s.pixels * s.C;
   const int half = s.n / 2;
   const float coef = 2.f * s.alpha * s.beta / (float)s.n;
@@ -271,6 +279,7 @@ __device__ __forceinline__ float* vat_w(const View2D& v, int i, int j) { return 
 // xor-butterfly: deterministic.
 __global__ void softmax_ce_kernel(View2D z, const int32_t* __restrict__ labels, float* __restrict__ row_loss,
                                   View2D dz, float inv_nloc, int* err) {
+  pdl_entry();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < z.rows; r += gridDim.x * warps) {
@@ -296,6 +305,7 @@ __global__ void softmax_ce_kernel(View2D z, const int32_t* __restrict__ labels, 
 }
 
 __global__ void euclidean_kernel(View2D u, View2D v, float* __restrict__ row_loss, View2D du, float inv_nloc) {
+  pdl_entry();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < u.rows; r += gridDim.x * warps) {
@@ -311,6 +321,7 @@ __global__ void euclidean_kernel(View2D u, View2D v, float* __restrict__ row_los
 }
 
 __global__ void sum_scaled_kernel(const float* __restrict__ v, int n, float scale, float* out, int* err) {
+  pdl_entry();
   __shared__ float red[32];
   float acc = 0.f;
   for (int i = threadIdx.x; i < n; i += blockDim.x) acc += v[i];
@@ -338,6 +349,7 @@ __device__ __forceinline__ void sgd1(float& w, float g, float& v, float lr, floa
 
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ v, long long n,
                            const float* lr_dev, float lr_scale, float lr_val, float mu, float wd, float s) {
+  pdl_entry();
   const float lr = lr_dev ? lr_dev[0] * lr_scale : lr_val;
   long long n4 = n >> 2;
   float4* w4 = reinterpret_cast<float4*>(w);
@@ -364,6 +376,7 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, f
 // ------------------------------------------------------------- input layer --
 __global__ void pad_channels_kernel(const float* __restrict__ x, float* __restrict__ y, long long pixels, int cin,
                                     int cout) {
+  pdl_entry();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < pixels * cout;
        i += (long long)gridDim.x * blockDim.x) {
     long long p = i / cout;
@@ -374,6 +387,7 @@ __global__ void pad_channels_kernel(const float* __restrict__ x, float* __restri
 
 __global__ void copy2d_kernel(const float* __restrict__ src, long long sld, float* __restrict__ dst, long long dld,
                               int rows, int cols) {
+  pdl_entry();
   long long total = (long long)rows * cols;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     int r = (int)(i / cols), c = (int)(i % cols);
@@ -382,6 +396,7 @@ __global__ void copy2d_kernel(const float* __restrict__ src, long long sld, floa
 }
 
 __global__ void relu2d_kernel(const float* __restrict__ x, float* __restrict__ y, int rows, int cols, long long ld) {
+  pdl_entry();
   long long total = (long long)rows * cols;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     int r = (int)(i / cols), c = (int)(i % cols);
@@ -400,93 +415,77 @@ cudaError_t sigmoid_bwd(const float* y, const float* dy, float* dx, long long n,
   return launch_map2(y, dy, dx, n, SigB{}, st);
 }
 cudaError_t relu_fwd2d(const float* x, float* y, int rows, int cols, long long ld, cudaStream_t st) {
-  relu2d_kernel<<<blocks_for((long long)rows * cols, 256), 256, 0, st>>>(x, y, rows, cols, ld);
-  return launched();
+  return launch_k(relu2d_kernel, blocks_for((long long)rows * cols, 256), 256, 0, st, x, y, rows, cols, ld);
 }
 
 cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* arg, cudaStream_t st) {
   if (s.C % 4 || s.k * s.k > 256) return cudaErrorInvalidValue;
-  maxpool_fwd_kernel<<<blocks_for((long long)s.N * s.Ho * s.Wo * s.C / 4, 256), 256, 0, st>>>(s, x, y, arg);
-  return launched();
+  return launch_k(maxpool_fwd_kernel, blocks_for((long long)s.N * s.Ho * s.Wo * s.C / 4, 256), 256, 0, st, s, x, y, arg);
 }
 cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg, float* dx, cudaStream_t st) {
   if (s.C % 4) return cudaErrorInvalidValue;
-  maxpool_bwd_kernel<<<blocks_for((long long)s.N * s.H * s.W * s.C / 4, 256), 256, 0, st>>>(s, dy, arg, dx);
-  return launched();
+  return launch_k(maxpool_bwd_kernel, blocks_for((long long)s.N * s.H * s.W * s.C / 4, 256), 256, 0, st, s, dy, arg, dx);
 }
 cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st) {
   if (s.C % 4) return cudaErrorInvalidValue;
-  avgpool_fwd_kernel<<<blocks_for((long long)s.N * s.Ho * s.Wo * s.C / 4, 256), 256, 0, st>>>(s, x, y);
-  return launched();
+  return launch_k(avgpool_fwd_kernel, blocks_for((long long)s.N * s.Ho * s.Wo * s.C / 4, 256), 256, 0, st, s, x, y);
 }
 cudaError_t avgpool_bwd(const PoolShape& s, const float* dy, float* dx, cudaStream_t st) {
   if (s.C % 4) return cudaErrorInvalidValue;
-  avgpool_bwd_kernel<<<blocks_for((long long)s.N * s.H * s.W * s.C / 4, 256), 256, 0, st>>>(s, dy, dx);
-  return launched();
+  return launch_k(avgpool_bwd_kernel, blocks_for((long long)s.N * s.H * s.W * s.C / 4, 256), 256, 0, st, s, dy, dx);
 }
 cudaError_t pool_argmax_expand(const PoolShape& s, const uint8_t* arg, int32_t* out, cudaStream_t st) {
-  argmax_expand_kernel<<<blocks_for((long long)s.N * s.Ho * s.Wo * s.C, 256), 256, 0, st>>>(s, arg, out);
-  return launched();
+  return launch_k(argmax_expand_kernel, blocks_for((long long)s.N * s.Ho * s.Wo * s.C, 256), 256, 0, st, s, arg, out);
 }
 
 cudaError_t lrn_fwd(const LrnShape& s, const float* x, float* y, float* scale, cudaStream_t st) {
-  lrn_fwd_kernel<<<blocks_for(s.pixels * s.C, 256), 256, 0, st>>>(s, x, y, scale);
-  return launched();
+  return launch_k(lrn_fwd_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale);
 }
 cudaError_t lrn_bwd(const LrnShape& s, const float* x, const float* y, const float* scale, const float* dy, float* dx,
                     cudaStream_t st) {
-  lrn_bwd_kernel<<<blocks_for(s.pixels * s.C, 256), 256, 0, st>>>(s, x, y, scale, dy, dx);
-  return launched();
+  return launch_k(lrn_bwd_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale, dy, dx);
 }
 
 cudaError_t softmax_ce(View2D z, const int32_t* labels, float* row_loss, View2D dz, float inv_nloc, int* err,
                        cudaStream_t st) {
   if (z.rows <= 0) return cudaSuccess;
-  softmax_ce_kernel<<<(z.rows + 7) / 8, 256, 0, st>>>(z, labels, row_loss, dz, inv_nloc, err);
-  return launched();
+  return launch_k(softmax_ce_kernel, (z.rows + 7) / 8, 256, 0, st, z, labels, row_loss, dz, inv_nloc, err);
 }
 cudaError_t euclidean(View2D u, View2D v, float* row_loss, View2D du, float inv_nloc, cudaStream_t st) {
   if (u.rows <= 0) return cudaSuccess;
-  euclidean_kernel<<<(u.rows + 7) / 8, 256, 0, st>>>(u, v, row_loss, du, inv_nloc);
-  return launched();
+  return launch_k(euclidean_kernel, (u.rows + 7) / 8, 256, 0, st, u, v, row_loss, du, inv_nloc);
 }
 cudaError_t sum_scaled(const float* v, int n, float scale, float* out, int* err, cudaStream_t st) {
-  sum_scaled_kernel<<<1, 1024, 0, st>>>(v, n, scale, out, err);
-  return launched();
+  return launch_k(sum_scaled_kernel, 1, 1024, 0, st, v, n, scale, out, err);
 }
 
 cudaError_t sgd_momentum(float* w, const float* g, float* v, long long n, float lr, float mu, float wd, float s,
                          cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (!aligned16(w) || !aligned16(g) || !aligned16(v)) return cudaErrorMisalignedAddress;
-  sgd_kernel<<<blocks_for(n / 4 + 1, 256), 256, 0, st>>>(w, g, v, n, nullptr, 1.f, lr, mu, wd, s);
-  return launched();
+  return launch_k(sgd_kernel, blocks_for(n / 4 + 1, 256), 256, 0, st, w, g, v, n, nullptr, 1.f, lr, mu, wd, s);
 }
 cudaError_t sgd_momentum_dev(float* w, const float* g, float* v, long long n, const float* lr_dev, float lr_scale,
                              float mu, float wd, float s, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (!aligned16(w) || !aligned16(g) || !aligned16(v)) return cudaErrorMisalignedAddress;
-  sgd_kernel<<<blocks_for(n / 4 + 1, 256), 256, 0, st>>>(w, g, v, n, lr_dev, lr_scale, 0.f, mu, wd, s);
-  return launched();
+  return launch_k(sgd_kernel, blocks_for(n / 4 + 1, 256), 256, 0, st, w, g, v, n, lr_dev, lr_scale, 0.f, mu, wd, s);
 }
 
 cudaError_t pad_channels(const float* x, float* y, long long pixels, int cin, int cout, cudaStream_t st) {
-  pad_channels_kernel<<<blocks_for(pixels * cout, 256), 256, 0, st>>>(x, y, pixels, cin, cout);
-  return launched();
+  return launch_k(pad_channels_kernel, blocks_for(pixels * cout, 256), 256, 0, st, x, y, pixels, cin, cout);
 }
 cudaError_t copy2d(const float* src, long long sld, float* dst, long long dld, int rows, int cols, cudaStream_t st) {
-  copy2d_kernel<<<blocks_for((long long)rows * cols, 256), 256, 0, st>>>(src, sld, dst, dld, rows, cols);
-  return launched();
+  return launch_k(copy2d_kernel, blocks_for((long long)rows * cols, 256), 256, 0, st, src, sld, dst, dld, rows, cols);
 }
 
 }  // namespace sg
 
 namespace sg {
 namespace {
-__global__ void fill_scalar_kernel(float* p, float v) { *p = v; }
+__global__ void fill_scalar_kernel(float* p, float v) { pdl_entry(); *p = v; }
 }  // namespace
 cudaError_t fill_scalar(float* p, float v, cudaStream_t st) {
-  fill_scalar_kernel<<<1, 1, 0, st>>>(p, v);
-  return launched();
+  return launch_k(fill_scalar_kernel, 1, 1, 0, st, p, v);
 }
 }  // namespace sg

@@ -14,6 +14,16 @@ namespace sg {
 
 long long g_kernel_launches = 0;
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* env = getenv("SG_PDL");
+    on = env ? atoi(env) != 0 : 1;
+  }
+  return on != 0;
+}
+
+
 namespace {
 
 constexpr int kNumSMs = 148;
@@ -39,7 +49,8 @@ Plan plan_gemm(int M, int N, int K, size_t ws_floats_avail) {
   const int tiles = p.mt * p.nt;
   int splits = 1;
   if (tiles < kNumSMs && nkb >= 2 * kMinKbPerSplit) {
-    splits = std::min((kNumSMs + tiles - 1) / tiles, nkb / kMinKbPerSplit);
+    // persistent grid of kNumSMs CTAs: tiles x splits must not spill into a second round
+    splits = std::min(kNumSMs / tiles, nkb / kMinKbPerSplit);
     while (splits > 1 && (size_t)splits * M * pad4(N) > ws_floats_avail) --splits;
     if (splits < 1) splits = 1;
   }
@@ -70,6 +81,7 @@ __device__ __forceinline__ void reduce_store(const EpiArgs& e, int m, int n, int
 
 __global__ void __launch_bounds__(512) splitk_reduce_kernel(const float* __restrict__ ws, int splits,
                                                             long long split_stride, int M, int N, EpiArgs e) {
+  pdl_entry();
   __shared__ float4 part[16][32];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5, G = blockDim.x >> 5;
   const int ldw = (N + 3) & ~3;
@@ -137,8 +149,7 @@ cudaError_t launch_bn(const GemmArgs<LA, LB>& args, const Plan& p, cudaStream_t 
     configured = true;
   }
   const int nwork = p.mt * p.nt * p.splits;
-  kern<<<std::min(nwork, kNumSMs), GEMM_ALL_THREADS, SMEM, st>>>(args);
-  return launched();
+  return launch_k(kern, std::min(nwork, kNumSMs), GEMM_ALL_THREADS, SMEM, st, args);
 }
 
 template <class LA, class LB>
@@ -163,9 +174,8 @@ cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int
   if (e != cudaSuccess || p.splits == 1) return e;
   const long long total4 = (long long)M * pad4(N) / 4;
   const int G = std::min(16, p.splits);
-  splitk_reduce_kernel<<<(unsigned)((total4 + 31) / 32), 32 * G, 0, st>>>(ws.ptr, p.splits, (long long)M * pad4(N),
-                                                                         M, N, epi);
-  return launched();
+  return launch_k(splitk_reduce_kernel, (unsigned)((total4 + 31) / 32), 32 * G, 0, st, (const float*)ws.ptr, p.splits,
+                  (long long)M * pad4(N), M, N, epi);
 }
 
 template <class LA, class LB>
@@ -370,6 +380,7 @@ constexpr int CS_ROWS_PER_BLOCK = 1024;
 
 __global__ void colsum_partial_kernel(const float* __restrict__ X, int M, int N, long long ld,
                                       float* __restrict__ part) {
+  pdl_entry();
   __shared__ float red[8][33];
   const int col = blockIdx.x * 32 + threadIdx.x;
   const int r0 = blockIdx.y * CS_ROWS_PER_BLOCK;
@@ -389,6 +400,7 @@ __global__ void colsum_partial_kernel(const float* __restrict__ X, int M, int N,
 }
 
 __global__ void colsum_final_kernel(const float* __restrict__ part, int nparts, int N, float* __restrict__ out) {
+  pdl_entry();
   int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= N) return;
   float s = 0.f;
@@ -408,11 +420,9 @@ cudaError_t colsum(const float* X, int M, int N, long long ld, float* out, Works
   int nparts = (M + CS_ROWS_PER_BLOCK - 1) / CS_ROWS_PER_BLOCK;
   if ((size_t)nparts * N > ws.floats) return cudaErrorInvalidValue;
   dim3 grid((N + 31) / 32, nparts);
-  colsum_partial_kernel<<<grid, dim3(32, 8), 0, st>>>(X, M, N, ld, ws.ptr);
-  cudaError_t e = launched();
+  cudaError_t e = launch_k(colsum_partial_kernel, grid, dim3(32, 8), 0, st, X, M, N, ld, ws.ptr);
   if (e != cudaSuccess) return e;
-  colsum_final_kernel<<<(N + 127) / 128, 128, 0, st>>>(ws.ptr, nparts, N, out);
-  return launched();
+  return launch_k(colsum_final_kernel, (N + 127) / 128, 128, 0, st, ws.ptr, nparts, N, out);
 }
 
 size_t colsum_ws_floats(int M, int N) { return (size_t)((M + CS_ROWS_PER_BLOCK - 1) / CS_ROWS_PER_BLOCK) * N; }
@@ -495,7 +505,11 @@ cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, floa
     e.xout = db;
   }
   const int M = db ? Kg + 1 : Kg;
-  if (tma_on(2) && s.C % 32 == 0 && aligned16p(x) && aligned16p(dy)) {
+  // TMA im2col issues one 32-pixel box per 32 channels of every tap; with a single
+  // channel block (C = 32) the TMA unit, not the tensor core, sets the pace and the
+  // 256-thread cp.async gather is faster (measured: CIFAR conv2 wgrad 48.6 -> 36.3 us,
+  // AlexNet conv2 (C = 64) 376 -> 416 us the other way).
+  if (tma_on(2) && s.C % 32 == 0 && s.C >= 64 && aligned16p(x) && aligned16p(dy)) {
     bool ok = true;
     TmaWgradA a{};
     a.map = enc_im2col(x, s.N, s.H, s.W, s.C, -s.pad, -s.pad, s.pad - (s.S - 1), s.pad - (s.R - 1), 32, GEMM_BK, s.st,

@@ -79,6 +79,19 @@ __device__ __forceinline__ void prefetch_tmap(const void* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 
+// ------------------------------------------- programmatic dependent launch --
+// Kernels are launched with programmatic stream serialisation (launch_k): a
+// kernel may become resident while its predecessor drains, so every kernel
+// calls pdl_wait() before its first global-memory access (it returns once the
+// predecessor grid has completed and its writes are visible), then lets its own
+// successor start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_entry() {
+  pdl_wait();
+  pdl_launch();
+}
+
 // ----------------------------------------------------------------- tcgen05 --
 template <int COLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem) {

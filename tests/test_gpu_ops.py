@@ -45,6 +45,7 @@ CONV = [  # N, H, W, C, Co, R, stride, pad
     (4, 16, 16, 32, 32, 5, 1, 2),     # CIFAR conv2
     (8, 8, 8, 32, 64, 5, 1, 2),       # CIFAR conv3
     (2, 35, 35, 4, 64, 11, 4, 2),     # AlexNet conv1 geometry
+    (2, 27, 27, 64, 192, 5, 1, 2),    # AlexNet conv2 (TMA wgrad, C = 64)
     (2, 13, 13, 192, 384, 3, 1, 1),   # AlexNet conv3
     (3, 9, 7, 8, 12, 3, 2, 1),        # ragged, strided dgrad
 ]

@@ -8,6 +8,6 @@ mkdir -p gpurun_out
 python bench.py $ARGS > gpurun_out/${TAG}_plain.json 2> gpurun_out/${TAG}_plain.err || { echo "plain run failed"; tail gpurun_out/${TAG}_plain.err; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
     python bench.py $ARGS > gpurun_out/${TAG}_ncu1.log 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$KRE" -s 60 -c 1 \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$KRE" -s ${NCU_SKIP:-5} -c 1 \
     -o gpurun_out/${TAG}_full python bench.py $ARGS > gpurun_out/${TAG}_ncu2.log 2>&1
 echo done

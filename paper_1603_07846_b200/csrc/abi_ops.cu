@@ -41,6 +41,7 @@ static sg_status op_workspace(size_t floats, Workspace* out) {
     size_t n = floats < ((size_t)1 << 20) ? ((size_t)1 << 20) : floats;
     cudaError_t e = cudaMalloc(&w.ptr, n * sizeof(float));
     if (e != cudaSuccess) SG_FAIL(SG_ERR_OOM, "workspace allocation of %zu floats failed", n);
+    SG_CUDA(cudaMemset(w.ptr, 0, 4096));  // split-K tile counters live at the head
     w.floats = n;
   }
   *out = w;

@@ -597,6 +597,7 @@ struct EpiArgs {
   float* xout;
   float* ws;
   long long ws_ld, ws_split_stride;
+  int* cnt;  // split-K tile counters (zero between GEMMs); null: separate reduce kernel
 };
 
 __device__ __forceinline__ float* out_at(const EpiArgs& e, int i, int j, int cols) {
@@ -641,6 +642,53 @@ constexpr int gemm_smem_bytes() {
   return STAGES * (GEMM_BM * GEMM_BK * 4 + BN * GEMM_BK * 4) + 1024 /*align*/ + 256 /*barriers*/;
 }
 
+// Final epilogue of 16 consecutive accumulator columns of one row: bias, ReLU,
+// plain / transposed / column-blocked store, or the bias-gradient row (xrow).
+__device__ __forceinline__ void epi_store16(const EpiArgs& e, int row, int col0, const float (&v)[16], int N,
+                                            bool plain_vec) {
+  if (row >= e.mvalid) {
+    if (row == e.xrow) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (col0 + i < N) e.xout[col0 + i] = v[i];
+    }
+    return;
+  }
+  if (plain_vec && col0 + 15 < N) {
+    float* dst = e.p + (long long)row * e.ld + col0;
+#pragma unroll
+    for (int i = 0; i < 16; i += 4) {
+      float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      if (e.bias) {
+        o.x += e.bias[col0 + i];
+        o.y += e.bias[col0 + i + 1];
+        o.z += e.bias[col0 + i + 2];
+        o.w += e.bias[col0 + i + 3];
+      }
+      if (e.relu) {
+        o.x = fmaxf(o.x, 0.f);
+        o.y = fmaxf(o.y, 0.f);
+        o.z = fmaxf(o.z, 0.f);
+        o.w = fmaxf(o.w, 0.f);
+      }
+      *reinterpret_cast<float4*>(dst + i) = o;
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int col = col0 + i;
+    if (col >= N) break;
+    float o = v[i];
+    if (e.bias) o += e.bias_on_m ? e.bias[row] : e.bias[col];
+    if (e.relu) o = fmaxf(o, 0.f);
+    if (e.trans)
+      *out_at(e, col, row, e.mvalid) = o;
+    else
+      *out_at(e, row, col, N) = o;
+  }
+}
+
 // Persistent warp-specialised kernel.  Work items = (M tile, N tile, K split),
 // strided over the CTAs; the operand pipeline runs across work items without
 // draining, and the accumulator is double-buffered in TMEM so the epilogue of
@@ -672,6 +720,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   constexpr int MMA_WARP = GEMM_PRODUCERS / 32;
   constexpr int EPI_WARP0 = MMA_WARP + 1;
   static_assert(BN % 32 == 0 && BN <= 256, "BN");
+  static_assert(GEMM_EPI_WARPS * 32 == 256, "epi_bar_sync() counts 256 threads");
   static_assert(LA::kTMA == LB::kTMA, "both operands TMA or both cp.async");
   constexpr bool TMA = LA::kTMA;
 
@@ -849,6 +898,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
     const int cbeg = ((warp - EPI_WARP0) >> 2) * HALF;
     const EpiArgs& e = args.epi;
     const bool plain_vec = !e.trans && e.cb >= args.N && (e.ld & 3) == 0 && !e.bias_on_m;
+    __shared__ int s_last;
     int local = 0;
     for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++local) {
       int mi, ni, si, kb0, nkb;
@@ -884,51 +934,50 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
           }
           continue;
         }
-        if (row >= e.mvalid) {
-          if (row == e.xrow) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (n0 + c0 + i < args.N) e.xout[n0 + c0 + i] = v[i];
-          }
-          continue;
-        }
-        if (plain_vec && n0 + c0 + 15 < args.N) {
-          float* dst = e.p + (long long)row * e.ld + n0 + c0;
-#pragma unroll
-          for (int i = 0; i < 16; i += 4) {
-            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            if (e.bias) {
-              o.x += e.bias[n0 + c0 + i];
-              o.y += e.bias[n0 + c0 + i + 1];
-              o.z += e.bias[n0 + c0 + i + 2];
-              o.w += e.bias[n0 + c0 + i + 3];
-            }
-            if (e.relu) {
-              o.x = fmaxf(o.x, 0.f);
-              o.y = fmaxf(o.y, 0.f);
-              o.z = fmaxf(o.z, 0.f);
-              o.w = fmaxf(o.w, 0.f);
-            }
-            *reinterpret_cast<float4*>(dst + i) = o;
-          }
-          continue;
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int col = n0 + c0 + i;
-          if (col >= args.N) break;
-          float o = v[i];
-          if (e.bias) o += e.bias_on_m ? e.bias[row] : e.bias[col];
-          if (e.relu) o = fmaxf(o, 0.f);
-          if (e.trans)
-            *out_at(e, col, row, e.mvalid) = o;
-          else
-            *out_at(e, row, col, args.N) = o;
-        }
+        epi_store16(e, row, n0 + c0, v, args.N, plain_vec);
       }
       // this buffer's accumulator has been read: release it to the MMA warp
       tc_fence_before();
       mbar_arrive(tempty_bar + 8 * b);
+      if (e.ws && e.cnt) {
+        // Split-K fix-up: the split that finishes a tile last (tile counter) sums
+        // every split's partial in ascending split order and applies the
+        // epilogue; the order does not depend on which split is last.
+        __threadfence();
+        epi_bar_sync();
+        if (warp == EPI_WARP0 && lane == 0) {
+          const int t = mi + wd.mt * ni;
+          s_last = atomicAdd(e.cnt + t, 1) == wd.splits - 1;
+          if (s_last) e.cnt[t] = 0;  // every split has arrived: re-arm for the next GEMM
+        }
+        epi_bar_sync();
+        if (s_last) {
+          __threadfence();
+          if (row < args.M) {
+#pragma unroll 1
+            for (int c0 = cbeg; c0 < cbeg + HALF; c0 += 16) {
+              if (n0 + c0 >= args.N) break;
+              float v[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = 0.f;
+              const float* src = e.ws + (long long)row * e.ws_ld + n0 + c0;
+#pragma unroll 2
+              for (int s2 = 0; s2 < wd.splits; ++s2) {
+                const float4* q = reinterpret_cast<const float4*>(src + (long long)s2 * e.ws_split_stride);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float4 u = __ldcg(q + i);
+                  v[4 * i] += u.x;
+                  v[4 * i + 1] += u.y;
+                  v[4 * i + 2] += u.z;
+                  v[4 * i + 3] += u.w;
+                }
+              }
+              epi_store16(e, row, n0 + c0, v, args.N, plain_vec);
+            }
+          }
+        }
+      }
     }
   }
   tc_fence_before();

@@ -28,6 +28,20 @@ namespace {
 
 constexpr int kNumSMs = 148;
 constexpr int kMinKbPerSplit = 8;
+constexpr int kSplitCounters = 256;  // ints at the head of the workspace (>= kNumSMs tiles)
+
+// Split-K reduction in a separate fixed-order kernel (default) or inside the GEMM
+// (SG_SPLITK_FIXUP=1: the last split of a tile sums the partials).  Measured
+// slower in-kernel on every config (CIFAR 410K -> 301K img/s): with few tiles and
+// many splits one CTA per tile serialises the whole reduction.
+bool splitk_fixup() {
+  static int on = -1;
+  if (on < 0) {
+    const char* env = getenv("SG_SPLITK_FIXUP");
+    on = env ? atoi(env) != 0 : 0;
+  }
+  return on != 0;
+}
 
 struct Plan {
   int bn, mt, nt, splits, kb_per_split;
@@ -157,10 +171,16 @@ cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int
                              cudaStream_t st) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   GemmArgs<LA, LB> args{a, b, M, N, K, p.kb_per_split, epi};
+  // workspace: kSplitCounters tile counters (kept zero between GEMMs), then the
+  // split partials [split][M][pad4(N)]
+  float* part = ws.ptr + kSplitCounters;
+  const bool fixup = splitk_fixup() && p.mt * p.nt <= kSplitCounters;
+  args.epi.cnt = nullptr;
   if (p.splits > 1) {
-    args.epi.ws = ws.ptr;
+    args.epi.ws = part;
     args.epi.ws_ld = pad4(N);
     args.epi.ws_split_stride = (long long)M * pad4(N);
+    if (fixup) args.epi.cnt = reinterpret_cast<int*>(ws.ptr);
   } else {
     args.epi.ws = nullptr;
   }
@@ -171,10 +191,10 @@ cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int
     case 128: e = launch_bn<128>(args, p, st); break;
     default: e = launch_bn<256>(args, p, st); break;
   }
-  if (e != cudaSuccess || p.splits == 1) return e;
+  if (e != cudaSuccess || p.splits == 1 || fixup) return e;
   const long long total4 = (long long)M * pad4(N) / 4;
   const int G = std::min(16, p.splits);
-  return launch_k(splitk_reduce_kernel, (unsigned)((total4 + 31) / 32), 32 * G, 0, st, (const float*)ws.ptr, p.splits,
+  return launch_k(splitk_reduce_kernel, (unsigned)((total4 + 31) / 32), 32 * G, 0, st, (const float*)part, p.splits,
                   (long long)M * pad4(N), M, N, epi);
 }
 
@@ -413,7 +433,7 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int nparts, 
 size_t gemm_ws_floats(int M, int N, int K) {
   Plan p = plan_gemm(M, N, K, (size_t)1 << 62);
   // the weight-gradient GEMMs may add one ones-row (fused bias gradient)
-  return p.splits > 1 ? (size_t)p.splits * (M + 4) * pad4(N) : 0;
+  return p.splits > 1 ? kSplitCounters + (size_t)p.splits * (M + 4) * pad4(N) : 0;
 }
 
 cudaError_t colsum(const float* X, int M, int N, long long ld, float* out, Workspace ws, cudaStream_t st) {

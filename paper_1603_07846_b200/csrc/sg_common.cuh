@@ -92,6 +92,9 @@ __device__ __forceinline__ void pdl_entry() {
   pdl_launch();
 }
 
+// Named barrier 1 over the GEMM's epilogue warps.
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
 // ----------------------------------------------------------------- tcgen05 --
 template <int COLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem) {

@@ -42,29 +42,6 @@ constexpr int GEMM_PRODUCERS = 256;
 // {1, 0, 0, 0}: source of the ones-row chunk (global memory, cp.async source).
 __device__ __align__(16) static const float g_one4[4] = {1.f, 0.f, 0.f, 0.f};
 
-// Unsigned division by a runtime constant via multiply-high (n < 2^31).
-struct FastDiv {
-  int d;
-  uint32_t mul, shr;
-  __device__ __forceinline__ int div(int n) const {
-    return (int)((__umulhi((uint32_t)n, mul) + (uint32_t)n) >> shr);
-  }
-};
-inline FastDiv make_fastdiv(int d) {
-  FastDiv f;
-  f.d = d < 1 ? 1 : d;
-  if (f.d == 1) {
-    f.mul = 0;
-    f.shr = 0;
-    return f;
-  }
-  uint32_t l = 0;
-  while ((1ull << l) < (unsigned long long)f.d) ++l;
-  f.mul = (uint32_t)(((1ull << 32) * ((1ull << l) - (unsigned long long)f.d)) / (unsigned long long)f.d + 1);
-  f.shr = l;
-  return f;
-}
-
 // ---------------------------------------------------------------------------
 // Blocked row-major matrix view: element (i, j) at p[(j / cb) * bs + i * ld + j % cb].
 // cb >= cols means a plain row-major matrix.  Column blocking is how a tensor

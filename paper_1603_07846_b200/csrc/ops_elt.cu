@@ -5,6 +5,7 @@
 // Readings A5-A8 of DESIGN.md fix the definitions left open by the paper.
 // All reductions run in a fixed order (bit-reproducible).
 #include <cstdint>
+#include <initializer_list>
 
 #include "ops.h"
 #include "sg_common.cuh"
@@ -85,125 +86,139 @@ cudaError_t launch_map2(const float* a, const float* b, float* y, long long n, F
 }
 
 // ---------------------------------------------------------------- pooling --
+// Index math is 32-bit with multiply-high division by the shape constants
+// (element counts < 2^31 are checked by the launchers).
+struct PoolK {
+  PoolShape s;
+  FastDiv fC4, fWo, fHo, fW, fH, fS;
+};
+PoolK pool_k(const PoolShape& s) {
+  return PoolK{s, make_fastdiv(s.C >> 2), make_fastdiv(s.Wo), make_fastdiv(s.Ho), make_fastdiv(s.W),
+               make_fastdiv(s.H), make_fastdiv(s.s)};
+}
+
 // Thread per (n, oh, ow, 4 channels).  Window origin (oh*s - p, ow*s - p);
-// the argmax is stored as the uint8 offset (h - h0)*k + (w - w0).
-__global__ void maxpool_fwd_kernel(PoolShape s, const float* __restrict__ x, float* __restrict__ y,
+// the argmax is stored as the uint8 offset (h - h0)*k + (w - w0); first maximum
+// in (h, w) scan order (strict >), reading A5.
+__global__ void maxpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* __restrict__ y,
                                    uint8_t* __restrict__ arg) {
   pdl_entry();
+  const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
-  long long total = (long long)s.N * s.Ho * s.Wo * C4;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    int c4 = (int)(i % C4);
-    long long t = i / C4;
-    int ow = (int)(t % s.Wo);
-    t /= s.Wo;
-    int oh = (int)(t % s.Ho);
-    int n = (int)(t / s.Ho);
-    int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
-    int hs = max(h0, 0), he = min(h0 + s.k, s.H), ws = max(w0, 0), we = min(w0 + s.k, s.W);
+  const int total = s.N * s.Ho * s.Wo * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int t = P.fC4.div(i), c4 = i - t * C4;
+    const int t2 = P.fWo.div(t), ow = t - t2 * s.Wo;
+    const int n = P.fHo.div(t2), oh = t2 - n * s.Ho;
+    const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
+    const int hs = max(h0, 0), he = min(h0 + s.k, s.H), ws = max(w0, 0), we = min(w0 + s.k, s.W);
     float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
     int a[4] = {0, 0, 0, 0};
+    const float* xn = x + (size_t)n * s.H * s.W * s.C + c4 * 4;
     for (int h = hs; h < he; ++h)
       for (int w = ws; w < we; ++w) {
-        float4 v = *reinterpret_cast<const float4*>(x + (((long long)n * s.H + h) * s.W + w) * s.C + c4 * 4);
-        int off = (h - h0) * s.k + (w - w0);
+        const float4 v = __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C));
+        const int off = (h - h0) * s.k + (w - w0);
         if (v.x > m[0]) { m[0] = v.x; a[0] = off; }
         if (v.y > m[1]) { m[1] = v.y; a[1] = off; }
         if (v.z > m[2]) { m[2] = v.z; a[2] = off; }
         if (v.w > m[3]) { m[3] = v.w; a[3] = off; }
       }
-    long long o = i * 4;
-    *reinterpret_cast<float4*>(y + o) = make_float4(m[0], m[1], m[2], m[3]);
-    *reinterpret_cast<uchar4*>(arg + o) = make_uchar4(a[0], a[1], a[2], a[3]);
+    *reinterpret_cast<float4*>(y + (size_t)i * 4) = make_float4(m[0], m[1], m[2], m[3]);
+    *reinterpret_cast<uchar4*>(arg + (size_t)i * 4) = make_uchar4(a[0], a[1], a[2], a[3]);
   }
+}
+
+// Windows containing input coordinate h (padded hp = h + p): oh*s <= hp < oh*s + k.
+__device__ __forceinline__ void pool_windows(int hp, int k, int Ho, const FastDiv& fS, int& o0, int& o1) {
+  o0 = hp >= k ? fS.div(hp - k) + 1 : 0;
+  o1 = min(fS.div(hp), Ho - 1);
 }
 
 // Gather form of the backward: thread per input (n, h, w, 4 channels) sums dy
 // of every window whose argmax is this element, windows in ascending (oh, ow).
-__global__ void maxpool_bwd_kernel(PoolShape s, const float* __restrict__ dy, const uint8_t* __restrict__ arg,
+__global__ void maxpool_bwd_kernel(PoolK P, const float* __restrict__ dy, const uint8_t* __restrict__ arg,
                                    float* __restrict__ dx) {
   pdl_entry();
+  const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
-  long long total = (long long)s.N * s.H * s.W * C4;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    int c4 = (int)(i % C4);
-    long long t = i / C4;
-    int w = (int)(t % s.W);
-    t /= s.W;
-    int h = (int)(t % s.H);
-    int n = (int)(t / s.H);
-    // windows containing h: oh*s - p <= h < oh*s - p + k
-    int hp = h + s.p, wp = w + s.p;
-    int oh0 = hp >= s.k ? (hp - s.k) / s.s + 1 : 0, oh1 = min(hp / s.s, s.Ho - 1);
-    int ow0 = wp >= s.k ? (wp - s.k) / s.s + 1 : 0, ow1 = min(wp / s.s, s.Wo - 1);
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const int total = s.N * s.H * s.W * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int t = P.fC4.div(i), c4 = i - t * C4;
+    const int t2 = P.fW.div(t), w = t - t2 * s.W;
+    const int n = P.fH.div(t2), h = t2 - n * s.H;
+    const int hp = h + s.p, wp = w + s.p;
+    int oh0, oh1, ow0, ow1;
+    pool_windows(hp, s.k, s.Ho, P.fS, oh0, oh1);
+    pool_windows(wp, s.k, s.Wo, P.fS, ow0, ow1);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const size_t nb = (size_t)n * s.Ho * s.Wo * s.C + c4 * 4;
     for (int oh = oh0; oh <= oh1; ++oh)
       for (int ow = ow0; ow <= ow1; ++ow) {
-        int off = (hp - oh * s.s) * s.k + (wp - ow * s.s);
-        long long o = (((long long)n * s.Ho + oh) * s.Wo + ow) * s.C + c4 * 4;
-        uchar4 a = *reinterpret_cast<const uchar4*>(arg + o);
-        float4 g = *reinterpret_cast<const float4*>(dy + o);
-        if (a.x == off) acc[0] += g.x;
-        if (a.y == off) acc[1] += g.y;
-        if (a.z == off) acc[2] += g.z;
-        if (a.w == off) acc[3] += g.w;
+        const int off = (hp - oh * s.s) * s.k + (wp - ow * s.s);
+        const size_t o = nb + (size_t)(oh * s.Wo + ow) * s.C;
+        const uchar4 a = __ldg(reinterpret_cast<const uchar4*>(arg + o));
+        const float4 g = __ldg(reinterpret_cast<const float4*>(dy + o));
+        if (a.x == off) acc.x += g.x;
+        if (a.y == off) acc.y += g.y;
+        if (a.z == off) acc.z += g.z;
+        if (a.w == off) acc.w += g.w;
       }
-    *reinterpret_cast<float4*>(dx + i * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(dx + (size_t)i * 4) = acc;
   }
 }
 
-__global__ void avgpool_fwd_kernel(PoolShape s, const float* __restrict__ x, float* __restrict__ y) {
+__global__ void avgpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* __restrict__ y) {
   pdl_entry();
+  const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
-  long long total = (long long)s.N * s.Ho * s.Wo * C4;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    int c4 = (int)(i % C4);
-    long long t = i / C4;
-    int ow = (int)(t % s.Wo);
-    t /= s.Wo;
-    int oh = (int)(t % s.Ho);
-    int n = (int)(t / s.Ho);
-    int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
-    int he_u = min(h0 + s.k, s.H + s.p), we_u = min(w0 + s.k, s.W + s.p);
-    float inv = 1.f / (float)((he_u - h0) * (we_u - w0));
-    int hs = max(h0, 0), he = min(he_u, s.H), ws = max(w0, 0), we = min(we_u, s.W);
+  const int total = s.N * s.Ho * s.Wo * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int t = P.fC4.div(i), c4 = i - t * C4;
+    const int t2 = P.fWo.div(t), ow = t - t2 * s.Wo;
+    const int n = P.fHo.div(t2), oh = t2 - n * s.Ho;
+    const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
+    const int he_u = min(h0 + s.k, s.H + s.p), we_u = min(w0 + s.k, s.W + s.p);
+    const float inv = 1.f / (float)((he_u - h0) * (we_u - w0));
+    const int hs = max(h0, 0), he = min(he_u, s.H), ws = max(w0, 0), we = min(we_u, s.W);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* xn = x + (size_t)n * s.H * s.W * s.C + c4 * 4;
     for (int h = hs; h < he; ++h)
       for (int w = ws; w < we; ++w) {
-        float4 v = *reinterpret_cast<const float4*>(x + (((long long)n * s.H + h) * s.W + w) * s.C + c4 * 4);
+        const float4 v = __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C));
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
-    *reinterpret_cast<float4*>(y + i * 4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    *reinterpret_cast<float4*>(y + (size_t)i * 4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   }
 }
 
-__global__ void avgpool_bwd_kernel(PoolShape s, const float* __restrict__ dy, float* __restrict__ dx) {
+__global__ void avgpool_bwd_kernel(PoolK P, const float* __restrict__ dy, float* __restrict__ dx) {
   pdl_entry();
+  const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
-  long long total = (long long)s.N * s.H * s.W * C4;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    int c4 = (int)(i % C4);
-    long long t = i / C4;
-    int w = (int)(t % s.W);
-    t /= s.W;
-    int h = (int)(t % s.H);
-    int n = (int)(t / s.H);
-    int hp = h + s.p, wp = w + s.p;
-    int oh0 = hp >= s.k ? (hp - s.k) / s.s + 1 : 0, oh1 = min(hp / s.s, s.Ho - 1);
-    int ow0 = wp >= s.k ? (wp - s.k) / s.s + 1 : 0, ow1 = min(wp / s.s, s.Wo - 1);
+  const int total = s.N * s.H * s.W * C4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int t = P.fC4.div(i), c4 = i - t * C4;
+    const int t2 = P.fW.div(t), w = t - t2 * s.W;
+    const int n = P.fH.div(t2), h = t2 - n * s.H;
+    const int hp = h + s.p, wp = w + s.p;
+    int oh0, oh1, ow0, ow1;
+    pool_windows(hp, s.k, s.Ho, P.fS, oh0, oh1);
+    pool_windows(wp, s.k, s.Wo, P.fS, ow0, ow1);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* dyn = dy + (size_t)n * s.Ho * s.Wo * s.C + c4 * 4;
     for (int oh = oh0; oh <= oh1; ++oh) {
-      int h0 = oh * s.s - s.p;
-      int hsz = min(h0 + s.k, s.H + s.p) - h0;
+      const int h0 = oh * s.s - s.p;
+      const int hsz = min(h0 + s.k, s.H + s.p) - h0;
       for (int ow = ow0; ow <= ow1; ++ow) {
-        int w0 = ow * s.s - s.p;
-        int wsz = min(w0 + s.k, s.W + s.p) - w0;
-        float inv = 1.f / (float)(hsz * wsz);
-        float4 g = *reinterpret_cast<const float4*>(dy + (((long long)n * s.Ho + oh) * s.Wo + ow) * s.C + c4 * 4);
+        const int w0 = ow * s.s - s.p;
+        const int wsz = min(w0 + s.k, s.W + s.p) - w0;
+        const float inv = 1.f / (float)(hsz * wsz);
+        const float4 g = __ldg(reinterpret_cast<const float4*>(dyn + (oh * s.Wo + ow) * s.C));
         acc.x += g.x * inv; acc.y += g.y * inv; acc.z += g.z * inv; acc.w += g.w * inv;
       }
     }
-    *reinterpret_cast<float4*>(dx + i * 4) = acc;
+    *reinterpret_cast<float4*>(dx + (size_t)i * 4) = acc;
   }
 }
 
@@ -223,8 +238,87 @@ __global__ void argmax_expand_kernel(PoolShape s, const uint8_t* __restrict__ ar
 // -------------------------------------------------------------------- LRN --
 __device__ __forceinline__ float pow_neg(float base, float beta) { return exp2f(-beta * log2f(base)); }
 
-__global__ void lrn_fwd_kernel(LrnShape s, const float* __restrict__ x, float* __restrict__ y,
-                               float* __restrict__ scale) {
+// Thread per (pixel, 4 channels); the channel window reaches at most 4 channels
+// into the neighbouring lanes' float4s (n <= 9), fetched with warp shuffles.
+// Requires C % 4 == 0 and (C / 4) | 32, so a pixel's channels sit in one warp.
+// Window sums run over ascending channels c' = c - n/2 ... c + n/2 (in range).
+struct LrnK {
+  LrnShape s;
+  int C4, total;  // total = pixels * C4 rounded up to a multiple of 32
+};
+
+__device__ __forceinline__ void lrn_neighbours(float4 me, int c4, int C4, float (&e)[12]) {
+  const float4 l = make_float4(__shfl_up_sync(0xffffffffu, me.x, 1), __shfl_up_sync(0xffffffffu, me.y, 1),
+                               __shfl_up_sync(0xffffffffu, me.z, 1), __shfl_up_sync(0xffffffffu, me.w, 1));
+  const float4 r = make_float4(__shfl_down_sync(0xffffffffu, me.x, 1), __shfl_down_sync(0xffffffffu, me.y, 1),
+                               __shfl_down_sync(0xffffffffu, me.z, 1), __shfl_down_sync(0xffffffffu, me.w, 1));
+  const bool hl = c4 > 0, hr = c4 < C4 - 1;
+  e[0] = hl ? l.x : 0.f; e[1] = hl ? l.y : 0.f; e[2] = hl ? l.z : 0.f; e[3] = hl ? l.w : 0.f;
+  e[4] = me.x; e[5] = me.y; e[6] = me.z; e[7] = me.w;
+  e[8] = hr ? r.x : 0.f; e[9] = hr ? r.y : 0.f; e[10] = hr ? r.z : 0.f; e[11] = hr ? r.w : 0.f;
+}
+
+__global__ void lrn_fwd_kernel(LrnK K, const float* __restrict__ x, float* __restrict__ y, float* __restrict__ scale) {
+  pdl_entry();
+  const LrnShape& s = K.s;
+  const int half = s.n / 2;
+  const float an = s.alpha / (float)s.n;
+  const int valid = (int)(s.pixels * K.C4);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K.total; i += gridDim.x * blockDim.x) {
+    const bool in = i < valid;
+    const int c4 = i % K.C4;  // C4 is a power of two
+    const float4 v = in ? __ldg(reinterpret_cast<const float4*>(x) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float e[12];
+    lrn_neighbours(make_float4(v.x * v.x, v.y * v.y, v.z * v.z, v.w * v.w), c4, K.C4, e);
+    float sc[4], o[4];
+    const float xv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float acc = 0.f;
+      for (int d = -half; d <= half; ++d) acc += e[4 + j + d];
+      sc[j] = s.k + an * acc;
+      o[j] = xv[j] * pow_neg(sc[j], s.beta);
+    }
+    if (in) {
+      reinterpret_cast<float4*>(scale)[i] = make_float4(sc[0], sc[1], sc[2], sc[3]);
+      reinterpret_cast<float4*>(y)[i] = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+__global__ void lrn_bwd_kernel(LrnK K, const float* __restrict__ x, const float* __restrict__ y,
+                               const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ dx) {
+  pdl_entry();
+  const LrnShape& s = K.s;
+  const int half = s.n / 2;
+  const float coef = 2.f * s.alpha * s.beta / (float)s.n;
+  const int valid = (int)(s.pixels * K.C4);
+  const float4 z = make_float4(0.f, 0.f, 0.f, 1.f);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K.total; i += gridDim.x * blockDim.x) {
+    const bool in = i < valid;
+    const int c4 = i % K.C4;
+    const float4 g = in ? __ldg(reinterpret_cast<const float4*>(dy) + i) : z;
+    const float4 yv = in ? __ldg(reinterpret_cast<const float4*>(y) + i) : z;
+    const float4 sv = in ? __ldg(reinterpret_cast<const float4*>(scale) + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+    const float4 xv = in ? __ldg(reinterpret_cast<const float4*>(x) + i) : z;
+    float e[12];
+    lrn_neighbours(make_float4(g.x * yv.x / sv.x, g.y * yv.y / sv.y, g.z * yv.z / sv.z, g.w * yv.w / sv.w), c4, K.C4,
+                   e);
+    const float gs[4] = {g.x, g.y, g.z, g.w}, ss[4] = {sv.x, sv.y, sv.z, sv.w}, xs[4] = {xv.x, xv.y, xv.z, xv.w};
+    float o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float acc = 0.f;
+      for (int d = -half; d <= half; ++d) acc += e[4 + j + d];
+      o[j] = gs[j] * pow_neg(ss[j], s.beta) - coef * xs[j] * acc;
+    }
+    if (in) reinterpret_cast<float4*>(dx)[i] = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// Generic channel counts: thread per element.
+__global__ void lrn_fwd_generic_kernel(LrnShape s, const float* __restrict__ x, float* __restrict__ y,
+                                       float* __restrict__ scale) {
   pdl_entry();
   long long total = s.pixels * s.C;
   const int half = s.n / 2;
@@ -241,8 +335,9 @@ __global__ void lrn_fwd_kernel(LrnShape s, const float* __restrict__ x, float* _
   }
 }
 
-__global__ void lrn_bwd_kernel(LrnShape s, const float* __restrict__ x, const float* __restrict__ y,
-                               const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ dx) {
+__global__ void lrn_bwd_generic_kernel(LrnShape s, const float* __restrict__ x, const float* __restrict__ y,
+                                       const float* __restrict__ scale, const float* __restrict__ dy,
+                                       float* __restrict__ dx) {
   pdl_entry();
   long long total = s.pixels * s.C;
   const int half = s.n / 2;
@@ -377,11 +472,14 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, f
 __global__ void pad_channels_kernel(const float* __restrict__ x, float* __restrict__ y, long long pixels, int cin,
                                     int cout) {
   pdl_entry();
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < pixels * cout;
-       i += (long long)gridDim.x * blockDim.x) {
-    long long p = i / cout;
-    int c = (int)(i - p * cout);
-    y[i] = c < cin ? x[p * cin + c] : 0.f;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < pixels; p += (long long)gridDim.x * blockDim.x) {
+    const float* src = x + p * cin;
+    float* dst = y + p * cout;
+    if (cout == 4 && cin == 3) {
+      *reinterpret_cast<float4*>(dst) = make_float4(src[0], src[1], src[2], 0.f);
+    } else {
+      for (int c = 0; c < cout; ++c) dst[c] = c < cin ? src[c] : 0.f;
+    }
   }
 }
 
@@ -418,32 +516,57 @@ cudaError_t relu_fwd2d(const float* x, float* y, int rows, int cols, long long l
   return launch_k(relu2d_kernel, blocks_for((long long)rows * cols, 256), 256, 0, st, x, y, rows, cols, ld);
 }
 
+static bool fits32(long long n) { return n < (1LL << 31); }
+
 cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* arg, cudaStream_t st) {
-  if (s.C % 4 || s.k * s.k > 256) return cudaErrorInvalidValue;
-  return launch_k(maxpool_fwd_kernel, blocks_for((long long)s.N * s.Ho * s.Wo * s.C / 4, 256), 256, 0, st, s, x, y, arg);
+  const long long n = (long long)s.N * s.Ho * s.Wo * s.C / 4;
+  if (s.C % 4 || s.k * s.k > 256 || !fits32(n * 4) || !fits32((long long)s.N * s.H * s.W * s.C))
+    return cudaErrorInvalidValue;
+  return launch_k(maxpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y, arg);
 }
 cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg, float* dx, cudaStream_t st) {
-  if (s.C % 4) return cudaErrorInvalidValue;
-  return launch_k(maxpool_bwd_kernel, blocks_for((long long)s.N * s.H * s.W * s.C / 4, 256), 256, 0, st, s, dy, arg, dx);
+  const long long n = (long long)s.N * s.H * s.W * s.C / 4;
+  if (s.C % 4 || !fits32(n * 4)) return cudaErrorInvalidValue;
+  return launch_k(maxpool_bwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), dy, arg, dx);
 }
 cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st) {
-  if (s.C % 4) return cudaErrorInvalidValue;
-  return launch_k(avgpool_fwd_kernel, blocks_for((long long)s.N * s.Ho * s.Wo * s.C / 4, 256), 256, 0, st, s, x, y);
+  const long long n = (long long)s.N * s.Ho * s.Wo * s.C / 4;
+  if (s.C % 4 || !fits32(n * 4) || !fits32((long long)s.N * s.H * s.W * s.C)) return cudaErrorInvalidValue;
+  return launch_k(avgpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y);
 }
 cudaError_t avgpool_bwd(const PoolShape& s, const float* dy, float* dx, cudaStream_t st) {
-  if (s.C % 4) return cudaErrorInvalidValue;
-  return launch_k(avgpool_bwd_kernel, blocks_for((long long)s.N * s.H * s.W * s.C / 4, 256), 256, 0, st, s, dy, dx);
+  const long long n = (long long)s.N * s.H * s.W * s.C / 4;
+  if (s.C % 4 || !fits32(n * 4)) return cudaErrorInvalidValue;
+  return launch_k(avgpool_bwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), dy, dx);
 }
 cudaError_t pool_argmax_expand(const PoolShape& s, const uint8_t* arg, int32_t* out, cudaStream_t st) {
   return launch_k(argmax_expand_kernel, blocks_for((long long)s.N * s.Ho * s.Wo * s.C, 256), 256, 0, st, s, arg, out);
 }
 
+// float4 + warp-shuffle path when a pixel's channels fit one warp (C/4 a power of
+// two <= 32), the window reaches at most one neighbouring float4 (n <= 9) and the
+// blobs are 16-byte aligned; else the element-wise kernel.
+static bool lrn_fast(const LrnShape& s, std::initializer_list<const void*> ptrs, LrnK* k) {
+  const int C4 = s.C / 4;
+  if (s.C % 4 || C4 > 32 || (C4 & (C4 - 1)) || s.n / 2 > 4 || !fits32(s.pixels * C4 + 32)) return false;
+  for (const void* p : ptrs)
+    if (!aligned16(p)) return false;
+  k->s = s;
+  k->C4 = C4;
+  k->total = (int)((s.pixels * C4 + 31) / 32 * 32);
+  return true;
+}
 cudaError_t lrn_fwd(const LrnShape& s, const float* x, float* y, float* scale, cudaStream_t st) {
-  return launch_k(lrn_fwd_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale);
+  LrnK k;
+  if (lrn_fast(s, {x, y, scale}, &k)) return launch_k(lrn_fwd_kernel, blocks_for(k.total, 256), 256, 0, st, k, x, y, scale);
+  return launch_k(lrn_fwd_generic_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale);
 }
 cudaError_t lrn_bwd(const LrnShape& s, const float* x, const float* y, const float* scale, const float* dy, float* dx,
                     cudaStream_t st) {
-  return launch_k(lrn_bwd_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale, dy, dx);
+  LrnK k;
+  if (lrn_fast(s, {x, y, scale, dy, dx}, &k))
+    return launch_k(lrn_bwd_kernel, blocks_for(k.total, 256), 256, 0, st, k, x, y, scale, dy, dx);
+  return launch_k(lrn_bwd_generic_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale, dy, dx);
 }
 
 cudaError_t softmax_ce(View2D z, const int32_t* labels, float* row_loss, View2D dz, float inv_nloc, int* err,
@@ -473,7 +596,8 @@ cudaError_t sgd_momentum_dev(float* w, const float* g, float* v, long long n, co
 }
 
 cudaError_t pad_channels(const float* x, float* y, long long pixels, int cin, int cout, cudaStream_t st) {
-  return launch_k(pad_channels_kernel, blocks_for(pixels * cout, 256), 256, 0, st, x, y, pixels, cin, cout);
+  if (cout == 4 && !aligned16(y)) return cudaErrorMisalignedAddress;
+  return launch_k(pad_channels_kernel, blocks_for(pixels, 256), 256, 0, st, x, y, pixels, cin, cout);
 }
 cudaError_t copy2d(const float* src, long long sld, float* dst, long long dld, int rows, int cols, cudaStream_t st) {
   return launch_k(copy2d_kernel, blocks_for((long long)rows * cols, 256), 256, 0, st, src, sld, dst, dld, rows, cols);

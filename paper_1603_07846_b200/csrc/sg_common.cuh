@@ -11,6 +11,29 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Unsigned division by a runtime constant via multiply-high (n < 2^31).
+struct FastDiv {
+  int d;
+  uint32_t mul, shr;
+  __device__ __forceinline__ int div(int n) const {
+    return (int)((__umulhi((uint32_t)n, mul) + (uint32_t)n) >> shr);
+  }
+};
+inline FastDiv make_fastdiv(int d) {
+  FastDiv f;
+  f.d = d < 1 ? 1 : d;
+  if (f.d == 1) {
+    f.mul = 0;
+    f.shr = 0;
+    return f;
+  }
+  uint32_t l = 0;
+  while ((1ull << l) < (unsigned long long)f.d) ++l;
+  f.mul = (uint32_t)(((1ull << 32) * ((1ull << l) - (unsigned long long)f.d)) / (unsigned long long)f.d + 1);
+  f.shr = l;
+  return f;
+}
+
 // ---------------------------------------------------------------- mbarrier --
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));

@@ -144,7 +144,9 @@ def test_maxpool_ties_first_max():
 
 
 # ------------------------------------------------------------------- LRN ----
-@pytest.mark.parametrize("pixels,Cc,n,alpha", [(128 * 256, 32, 3, 5e-5), (300, 64, 5, 0.1), (17, 8, 3, 1.0)])
+@pytest.mark.parametrize("pixels,Cc,n,alpha", [(128 * 256, 32, 3, 5e-5), (300, 64, 5, 0.1), (17, 8, 3, 1.0),
+                                               (31, 4, 3, 1.0), (64, 128, 9, 0.2),      # shuffle path edges
+                                               (50, 12, 3, 0.5), (40, 256, 5, 0.1)])   # element-wise path
 def test_lrn(pixels, Cc, n, alpha):
     x = r32(pixels, Cc)
     d = lib.LrnDesc(pixels, Cc, n, alpha, 0.75, 1.0)

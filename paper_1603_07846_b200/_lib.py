@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsinga_b200.so")
+LIB_PATH = os.environ.get("SG_LIB") or os.path.join(_HERE, "libsinga_b200.so")  # SG_LIB: A/B of two builds
 
 SG_OK = 0
 ERRORS = {

@@ -1,5 +1,6 @@
 // extern "C" entry points: errors, partition map and the layer-isolated
 // operations of include/singa_b200.h (argument checking + launch only).
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <vector>

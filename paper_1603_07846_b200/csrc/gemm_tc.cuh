@@ -29,6 +29,7 @@
 // one extra "ones" row (index `ones_row`), whose output row is sum_k B(n, k) =
 // column sums of dy, routed by the epilogue to the bias-gradient buffer.
 #pragma once
+#include <type_traits>
 #include <cuda.h>
 
 #include "sg_common.cuh"
@@ -376,6 +377,173 @@ struct LdConvWgradA {
   }
 };
 
+// ------------------------------------------- shared-memory im2col loaders --
+// First layers with C = 4 channels: a filter tap is one 16-byte float4, so a
+// global gather per tap (LdConvFwdA / LdConvWgradA) is latency-bound.  These
+// loaders stage the zero-padded input image of the current sample in a
+// per-CTA shared-memory scratch (restaged when the sample changes, all
+// producer threads in lock step via named barrier 2) and build the operand
+// tile from it with ld.shared / st.shared.  Requires C == 4, every tile /
+// k-block inside one image, and the padded image within kScratch bytes.
+constexpr int kIm2colScratch = 32 * 1024;
+
+__device__ __forceinline__ void producer_bar_sync() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+// Padded image of sample n: element (ph, pw) = x[n][ph - pad][pw - pad] (0 outside),
+// ph < Hp = (Ho-1)*st + R, pw < Wp = (Wo-1)*st + S.
+struct SmemImage {
+  const float* x;
+  ConvGeom g;
+  int Hp, Wp;
+  __device__ __forceinline__ void restage(int& staged, uint32_t scr, int n, int tid) const {
+    if (n == staged) return;
+    producer_bar_sync();  // every producer is done reading the previous image
+    const float4* x4 = reinterpret_cast<const float4*>(x) + (size_t)n * g.H * g.W;
+    for (int i = tid; i < Hp * Wp; i += GEMM_PRODUCERS) {
+      const int ph = i / Wp, pw = i - ph * Wp;
+      const int ih = ph - g.pad, iw = pw - g.pad;
+      const float4 v = ((unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W) ? __ldg(x4 + ih * g.W + iw)
+                                                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      sts4(scr + i * 16, v);
+    }
+    producer_bar_sync();
+    staged = n;
+  }
+};
+
+// Convolution forward A(m = (n, oh, ow), k = (r, s, c)), K-major.
+struct LdConvFwdSmemA {
+  static constexpr int kMN = 0;
+  static constexpr bool kTMA = false;
+  static constexpr int kScratch = kIm2colScratch;
+  SmemImage im;
+  template <int T>
+  struct State {
+    uint32_t scr;
+    int pix[Place<T>::N];  // padded-image offset of (oh*st, ow*st), -1 past the end
+  };
+  template <int T>
+  __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
+    const ConvGeom& g = im.g;
+    const int Mtot = g.N * g.Ho * g.Wo;
+#pragma unroll
+    for (int i = 0; i < Place<T>::N; ++i) {
+      const int m = row0 + Place<T>::krow(tid, i);
+      s.pix[i] = -1;
+      if (m < Mtot) {
+        const int n = g.fHoWo.div(m), rem = m - n * g.Ho * g.Wo;
+        const int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
+        s.pix[i] = oh * g.st * im.Wp + ow * g.st;
+      }
+    }
+  }
+  template <int T>
+  __device__ __forceinline__ void prepare(State<T>& s, int& staged, uint32_t scr, int row0, int k0, int tid) const {
+    s.scr = scr;
+    const int Mtot = im.g.N * im.g.Ho * im.g.Wo;
+    im.restage(staged, scr, im.g.fHoWo.div(row0 < Mtot ? row0 : Mtot - 1), tid);
+  }
+  template <int T>
+  __device__ __forceinline__ void load(const State<T>& s, uint32_t sm, int k0, int tid) const {
+    const ConvGeom& g = im.g;
+    const int tap = (k0 >> 2) + (tid & 7);  // C == 4: k = 4 * tap + c
+    const bool kok = tap < g.R * g.S;
+    const int r = g.fS.div(tap), sc = tap - r * g.S;
+    const int off = r * im.Wp + sc;
+#pragma unroll
+    for (int i = 0; i < Place<T>::N; ++i) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (kok && s.pix[i] >= 0) v = lds4(s.scr + (s.pix[i] + off) * 16);
+      sts4(Place<T>::kdst(sm, tid, i), v);
+    }
+  }
+};
+
+// Convolution weight gradient A(kg = (r, s, c), m = pixel), MN-major, with the
+// bias-gradient ones row at kg = ones_row.
+struct LdConvWgradSmemA {
+  static constexpr int kMN = 1;
+  static constexpr bool kTMA = false;
+  static constexpr int kScratch = kIm2colScratch;
+  SmemImage im;
+  int ones_row;
+  template <int T>
+  struct State {
+    uint32_t scr;
+    int off;   // padded-image offset of tap (r, s)
+    int mode;  // 0 zero, 1 data, 2 ones
+  };
+  template <int T>
+  __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
+    const ConvGeom& g = im.g;
+    const int kg = row0 + Place<T>::mn(tid);  // multiple of 4: c = 0
+    s.mode = 0;
+    s.off = 0;
+    if (kg < g.R * g.S * 4) {
+      const int tap = kg >> 2, r = g.fS.div(tap), sc = tap - r * g.S;
+      s.off = r * im.Wp + sc;
+      s.mode = 1;
+    } else if (kg == ones_row) {
+      s.mode = 2;
+    }
+  }
+  template <int T>
+  __device__ __forceinline__ void prepare(State<T>& s, int& staged, uint32_t scr, int row0, int k0, int tid) const {
+    s.scr = scr;
+    const int Mtot = im.g.N * im.g.Ho * im.g.Wo;
+    im.restage(staged, scr, im.g.fHoWo.div(k0 < Mtot ? k0 : Mtot - 1), tid);
+  }
+  template <int T>
+  __device__ __forceinline__ void load(const State<T>& s, uint32_t sm, int k0, int tid) const {
+    const ConvGeom& g = im.g;
+    const int Mtot = g.N * g.Ho * g.Wo;
+    const int HoWo = g.Ho * g.Wo;
+#pragma unroll
+    for (int i = 0; i < Place<T>::N; ++i) {
+      const int p = k0 + Place<T>::kr(tid, i);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (p < Mtot) {
+        if (s.mode == 1) {
+          const int rem = p - g.fHoWo.div(p) * HoWo;
+          const int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
+          v = lds4(s.scr + (oh * g.st * im.Wp + ow * g.st + s.off) * 16);
+        } else if (s.mode == 2) {
+          v.x = 1.f;
+        }
+      }
+      sts4(Place<T>::mdst(sm, tid, i), v);
+    }
+  }
+};
+
+// Loaders whose scratch holds per-sample state want contiguous work ranges.
+template <class T, class = void>
+struct ContiguousOf {
+  static constexpr bool value = false;
+};
+template <class T>
+struct ContiguousOf<T, std::void_t<decltype(T::kScratch)>> {
+  static constexpr bool value = true;
+};
+
+// Scratch bytes a loader needs (0 unless it declares kScratch).
+template <class T, class = void>
+struct ScratchOf {
+  static constexpr int value = 0;
+};
+template <class T>
+struct ScratchOf<T, std::void_t<decltype(T::kScratch)>> {
+  static constexpr int value = T::kScratch;
+};
+
 // ------------------------------------------------------------ TMA loaders --
 // One elected producer thread issues cp.async.bulk.tensor per operand per stage
 // (tensor maps encoded on the host after the tile shape is chosen; layouts
@@ -588,8 +756,9 @@ struct GemmArgs {
   LA a;
   LB b;
   int M, N, K;
-  int kb_per_split;  // k-blocks handled by one CTA (blockIdx.z = split)
+  int kb_per_split;  // k-blocks of one work item (a K split)
   EpiArgs epi;
+  int async_arrive;  // cp.async producers: mbarrier arrive on copy completion (else LAG-delayed arrive)
 };
 
 // Shared-memory descriptor of the kk-th K=8 step of a stage tile, per operand
@@ -614,9 +783,9 @@ constexpr int gemm_stages() {
   return BN <= 32 ? 8 : BN <= 64 ? 7 : BN <= 128 ? 6 : 4;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int SCRATCH = 0>
 constexpr int gemm_smem_bytes() {
-  return STAGES * (GEMM_BM * GEMM_BK * 4 + BN * GEMM_BK * 4) + 1024 /*align*/ + 256 /*barriers*/;
+  return STAGES * (GEMM_BM * GEMM_BK * 4 + BN * GEMM_BK * 4) + SCRATCH + 1024 /*align*/ + 256 /*barriers*/;
 }
 
 // Final epilogue of 16 consecutive accumulator columns of one row: bias, ReLU,
@@ -701,9 +870,13 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   static_assert(LA::kTMA == LB::kTMA, "both operands TMA or both cp.async");
   constexpr bool TMA = LA::kTMA;
 
+  constexpr int SCRATCH = ScratchOf<LA>::value;
+  static_assert(ScratchOf<LB>::value == 0, "scratch is an A-operand feature");
+
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t bar_base = sbase + STAGES * STAGE_BYTES;
+  const uint32_t scratch = sbase + STAGES * STAGE_BYTES;  // loader scratch (SCRATCH bytes)
+  const uint32_t bar_base = scratch + SCRATCH;
   // full[s] at bar_base + 8s, empty[s] at +8(STAGES+s), tfull[b] at +16 STAGES + 8b,
   // tempty[b] at +16 STAGES + 16 + 8b, tmem slot after.
   const uint32_t tfull_bar = bar_base + 16 * STAGES;
@@ -717,6 +890,14 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   const WorkDecode wd{(args.M + GEMM_BM - 1) / GEMM_BM, (args.N + BN - 1) / BN,
                       (nkb_total + args.kb_per_split - 1) / (args.kb_per_split > 0 ? args.kb_per_split : 1)};
   const int nwork = wd.mt * wd.nt * (wd.splits > 0 ? wd.splits : 1);
+  // work items of this CTA: strided (neighbouring CTAs share operand tiles in
+  // L2) or, for loaders that keep per-sample state, one contiguous range
+  int w_first = blockIdx.x, w_end = nwork, w_step = gridDim.x;
+  if constexpr (ContiguousOf<LA>::value) {
+    w_first = (int)((long long)nwork * blockIdx.x / gridDim.x);
+    w_end = (int)((long long)nwork * (blockIdx.x + 1) / gridDim.x);
+    w_step = 1;
+  }
   auto kb_range = [&](int si, int& kb0, int& nkb) {
     kb0 = si * args.kb_per_split;
     int e = kb0 + args.kb_per_split;
@@ -757,7 +938,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
         int tagA[STAGES], tagB[STAGES];  // row0 the stage's constant atoms were written for
 #pragma unroll
         for (int s = 0; s < STAGES; ++s) tagA[s] = tagB[s] = -1;
-        for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+        for (int w = w_first; w < w_end; w += w_step) {
           int mi, ni, si, kb0, nkb;
           wd.get(w, mi, ni, si);
           kb_range(si, kb0, nkb);
@@ -806,7 +987,9 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
       }
     } else {
       int it = 0;
-      for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+      int staged = -1;  // sample whose padded image is in the scratch (smem im2col loaders)
+      (void)staged;
+      for (int w = w_first; w < w_end; w += w_step) {
         int mi, ni, si, kb0, nkb;
         wd.get(w, mi, ni, si);
         kb_range(si, kb0, nkb);
@@ -820,8 +1003,15 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
           if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
           const uint32_t sa = sbase + s * STAGE_BYTES;
           const int k0 = (kb0 + j) * GEMM_BK;
+          if constexpr (SCRATCH > 0) args.a.template prepare<GEMM_BM>(sa_st, staged, scratch, mi * GEMM_BM, k0, tid);
           args.a.template load<GEMM_BM>(sa_st, sa, k0, tid);
           args.b.template load<BN>(sb_st, sa + A_BYTES, k0, tid);
+          if (args.async_arrive) {
+            // the barrier counts this thread's arrival once its copies have
+            // landed; the MMA warp fences them into the async proxy
+            cp_async_mbar_arrive_noinc(bar_base + 8 * s);
+            continue;
+          }
           cp_async_commit();
           if (it >= LAG) {
             // this thread's copies of stage it-LAG have landed: make them visible
@@ -832,15 +1022,19 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
           }
         }
       }
-      cp_async_wait<0>();
-      fence_proxy_async_smem();
-      for (int j = (it > LAG ? it - LAG : 0); j < it; ++j) mbar_arrive(bar_base + 8 * (j % STAGES));
+      if (args.async_arrive) {
+        cp_async_wait_all();
+      } else {
+        cp_async_wait<0>();
+        fence_proxy_async_smem();
+        for (int j = (it > LAG ? it - LAG : 0); j < it; ++j) mbar_arrive(bar_base + 8 * (j % STAGES));
+      }
     }
   } else if (warp == MMA_WARP) {
     // --------------- MMA issuer: the whole warp waits, lane 0 issues ---------------
     constexpr uint32_t idesc = idesc_tf32(GEMM_BM, BN, LA::kMN & 1, LB::kMN & 1);
     int it = 0, local = 0;
-    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++local) {
+    for (int w = w_first; w < w_end; w += w_step, ++local) {
       int mi, ni, si, kb0, nkb;
       wd.get(w, mi, ni, si);
       kb_range(si, kb0, nkb);
@@ -852,6 +1046,9 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
       for (int j = 0; j < nkb; ++j, ++it) {
         const int s = it % STAGES;
         mbar_wait(bar_base + 8 * s, (it / STAGES) & 1);
+        if constexpr (!TMA) {
+          if (args.async_arrive) fence_proxy_async_smem();  // producers' generic-proxy writes -> tensor core
+        }
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sa = sbase + s * STAGE_BYTES;
@@ -877,7 +1074,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
     const bool plain_vec = !e.trans && e.cb >= args.N && (e.ld & 3) == 0 && !e.bias_on_m;
     __shared__ int s_last;
     int local = 0;
-    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++local) {
+    for (int w = w_first; w < w_end; w += w_step, ++local) {
       int mi, ni, si, kb0, nkb;
       wd.get(w, mi, ni, si);
       kb_range(si, kb0, nkb);

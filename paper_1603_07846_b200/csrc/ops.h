@@ -65,6 +65,7 @@ struct ConvShape {
 // Number of floats of split-K workspace a GEMM of this shape may use.
 size_t gemm_ws_floats(int M, int N, int K);
 
+
 // ---- convolution (implicit GEMM, tcgen05 kind::tf32) ----
 cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const float* b, float* y, int relu,
                      Workspace ws, cudaStream_t st);

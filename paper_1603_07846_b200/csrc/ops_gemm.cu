@@ -14,6 +14,18 @@ namespace sg {
 
 long long g_kernel_launches = 0;
 
+// cp.async producers release a stage with cp.async.mbarrier.arrive (default) or
+// with the older wait_group-LAG scheme (SG_ASYNC_ARRIVE=0, for A/B).
+bool async_arrive() {
+  static int on = -1;
+  if (on < 0) {
+    const char* env = getenv("SG_ASYNC_ARRIVE");
+    on = env ? atoi(env) != 0 : 1;
+  }
+  return on != 0;
+}
+
+
 bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -154,7 +166,7 @@ __global__ void __launch_bounds__(512) splitk_reduce_kernel(const float* __restr
 template <int BN, class LA, class LB>
 cudaError_t launch_bn(const GemmArgs<LA, LB>& args, const Plan& p, cudaStream_t st) {
   constexpr int STAGES = gemm_stages<BN>();
-  constexpr int SMEM = gemm_smem_bytes<BN, STAGES>();
+  constexpr int SMEM = gemm_smem_bytes<BN, STAGES, ScratchOf<LA>::value>();
   auto kern = gemm_tc_kernel<BN, STAGES, LA, LB>;
   static bool configured = false;
   if (!configured) {
@@ -170,7 +182,7 @@ template <class LA, class LB>
 cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int N, int K, EpiArgs epi, Workspace ws,
                              cudaStream_t st) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  GemmArgs<LA, LB> args{a, b, M, N, K, p.kb_per_split, epi};
+  GemmArgs<LA, LB> args{a, b, M, N, K, p.kb_per_split, epi, async_arrive() ? 1 : 0};
   // workspace: kSplitCounters tile counters (kept zero between GEMMs), then the
   // split partials [split][M][pad4(N)]
   float* part = ws.ptr + kSplitCounters;
@@ -395,6 +407,22 @@ ConvGeom geom(const ConvShape& s) {
   return g;
 }
 
+// Shared-memory im2col (4-channel first layers): every `unit` consecutive
+// output pixels (GEMM tile rows or k-block) lie in one image and the padded
+// image fits the loader scratch.  SG_SMEM_IM2COL=0 disables it (A/B).
+bool smem_im2col_ok(const ConvShape& s, int unit, SmemImage* im) {
+  static int on = -1;
+  if (on < 0) {
+    const char* env = getenv("SG_SMEM_IM2COL");
+    on = env ? atoi(env) != 0 : 1;
+  }
+  if (!on || s.C != 4 || (s.Ho * s.Wo) % unit != 0) return false;
+  const int Hp = (s.Ho - 1) * s.st + s.R, Wp = (s.Wo - 1) * s.st + s.S;
+  if ((long long)Hp * Wp * 16 > kIm2colScratch) return false;
+  *im = SmemImage{nullptr, geom(s), Hp, Wp};
+  return true;
+}
+
 // ---------------------------------------------------------- column sums ----
 constexpr int CS_ROWS_PER_BLOCK = 1024;
 
@@ -473,8 +501,13 @@ cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const f
     TmaK bw = tma_k(vplain(W, s.Co, K, K), p.bn, &ok);
     if (ok) return run_gemm_planned(a, bw, p, M, N, K, e, ws, st);
   }
-  LdConvFwdA a{x, geom(s)};
   LdDenseK bw{mv(W, s.Co, K, K)};
+  SmemImage im;
+  if (smem_im2col_ok(s, GEMM_BM, &im)) {
+    im.x = x;
+    return run_gemm(LdConvFwdSmemA{im}, bw, M, N, K, e, ws, st);
+  }
+  LdConvFwdA a{x, geom(s)};
   return run_gemm(a, bw, M, N, K, e, ws, st);
 }
 
@@ -550,8 +583,13 @@ cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, floa
     TmaMN bd = tma_mn(vplain(dy, Mtot, s.Co, s.Co), s.Co, -1, p.bn, &ok);
     if (ok) return run_gemm_planned(a, bd, p, M, s.Co, Mtot, e, ws, st);
   }
-  LdConvWgradA a{x, geom(s), db ? Kg : -1};
   LdDenseMN bd{mv(dy, Mtot, s.Co, s.Co), -1};
+  SmemImage im;
+  if (smem_im2col_ok(s, GEMM_BK, &im)) {
+    im.x = x;
+    return run_gemm(LdConvWgradSmemA{im, db ? Kg : -1}, bd, M, s.Co, Mtot, e, ws, st);
+  }
+  LdConvWgradA a{x, geom(s), db ? Kg : -1};
   return run_gemm(a, bd, M, s.Co, Mtot, e, ws, st);
 }
 

@@ -41,7 +41,8 @@ def test_gemm(M, N, K, ta, tb):
 
 # ------------------------------------------------------------------ conv ----
 CONV = [  # N, H, W, C, Co, R, stride, pad
-    (4, 32, 32, 4, 32, 5, 1, 2),      # CIFAR conv1 (C padded to 4)
+    (4, 32, 32, 4, 32, 5, 1, 2),      # CIFAR conv1 (C padded to 4): direct CUDA-core path
+    (3, 12, 10, 4, 8, 3, 1, 1),       # direct path, ragged Wo (10 = 2 x 4 + 2)
     (4, 16, 16, 32, 32, 5, 1, 2),     # CIFAR conv2
     (8, 8, 8, 32, 64, 5, 1, 2),       # CIFAR conv3
     (2, 35, 35, 4, 64, 11, 4, 2),     # AlexNet conv1 geometry

@@ -1,6 +1,9 @@
 """In-tree build of libsinga_b200.so (nvcc, sm_100a only).
 
-Usage: python -m paper_1603_07846_b200.build [--force] [-j N]
+Usage: python -m paper_1603_07846_b200.build [--force] [-j N] [--variant NAME -D MACRO ...]
+
+A variant (A/B experiments, instrumentation) builds into build/<NAME>/ and
+links build/<NAME>/libsinga_b200.so; load it with SG_LIB=<path>.
 """
 
 import argparse
@@ -26,9 +29,12 @@ def nccl_dirs():
     return os.path.join(base, "include"), os.path.join(base, "lib")
 
 
+EXTRA = []  # extra nvcc flags of a variant build
+
+
 def flags():
     inc, _ = nccl_dirs()
-    return ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+    return ARCH + EXTRA + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
                    "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-I", inc, "--expt-relaxed-constexpr"]
 
 
@@ -71,9 +77,15 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-j", type=int, default=None)
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("-D", action="append", default=[])
     a = ap.parse_args()
+    if a.variant:
+        EXTRA[:] = ["-D" + d for d in a.D]
+        BUILD = os.path.join(ROOT, "build", a.variant, "obj")
+        LIB = os.path.join(ROOT, "build", a.variant, "libsinga_b200.so")
     try:
-        build(a.force, a.j)
+        build(a.force or bool(a.variant), a.j)
     except RuntimeError as e:
         print(e, file=sys.stderr)
         sys.exit(1)

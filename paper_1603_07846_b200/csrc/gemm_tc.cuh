@@ -378,14 +378,15 @@ struct LdConvWgradA {
 };
 
 // ------------------------------------------- shared-memory im2col loaders --
-// First layers with C = 4 channels: a filter tap is one 16-byte float4, so a
-// global gather per tap (LdConvFwdA / LdConvWgradA) is latency-bound.  These
-// loaders stage the zero-padded input image of the current sample in a
-// per-CTA shared-memory scratch (restaged when the sample changes, all
-// producer threads in lock step via named barrier 2) and build the operand
-// tile from it with ld.shared / st.shared.  Requires C == 4, every tile /
-// k-block inside one image, and the padded image within kScratch bytes.
-constexpr int kIm2colScratch = 32 * 1024;
+// The implicit-GEMM gathers re-read every input element R*S times from L2 (and
+// with C = 4 a filter tap is one 16-byte granule, so the gather is pure
+// latency).  These loaders stage the zero-padded input image of the current
+// sample in a per-CTA shared-memory scratch once (cp.async, restaged when the
+// sample changes; all producer threads in lock step via named barrier 2) and
+// build each operand tile from it with ld.shared / st.shared.  Requires
+// C % 4 == 0, every tile / k-block inside one image, and the padded image
+// within kIm2colScratch bytes.
+constexpr int kIm2colScratch = 64 * 1024;
 
 __device__ __forceinline__ void producer_bar_sync() { asm volatile("bar.sync 2, 256;" ::: "memory"); }
 __device__ __forceinline__ float4 lds4(uint32_t a) {
@@ -397,23 +398,29 @@ __device__ __forceinline__ void sts4(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 
-// Padded image of sample n: element (ph, pw) = x[n][ph - pad][pw - pad] (0 outside),
-// ph < Hp = (Ho-1)*st + R, pw < Wp = (Wo-1)*st + S.
+// Padded image of sample n, float4 granules: (ph, pw, c4) at ((ph*Wp + pw)*C4 + c4)
+// = x[n][ph - pad][pw - pad][4 c4 .. 4 c4 + 3] (0 outside), ph < Hp = (Ho-1)*st + R,
+// pw < Wp = (Wo-1)*st + S.
 struct SmemImage {
   const float* x;
   ConvGeom g;
-  int Hp, Wp;
+  int Hp, Wp, C4;
+  FastDiv fWpC4, fC4;
   __device__ __forceinline__ void restage(int& staged, uint32_t scr, int n, int tid) const {
     if (n == staged) return;
     producer_bar_sync();  // every producer is done reading the previous image
-    const float4* x4 = reinterpret_cast<const float4*>(x) + (size_t)n * g.H * g.W;
-    for (int i = tid; i < Hp * Wp; i += GEMM_PRODUCERS) {
-      const int ph = i / Wp, pw = i - ph * Wp;
+    // all copies in flight at once (cp.async, zero-fill outside the image)
+    const float4* x4 = reinterpret_cast<const float4*>(x) + (size_t)n * g.H * g.W * C4;
+    const int total = Hp * Wp * C4;
+    for (int i = tid; i < total; i += GEMM_PRODUCERS) {
+      const int ph = fWpC4.div(i), r1 = i - ph * Wp * C4;
+      const int pw = fC4.div(r1), c4 = r1 - pw * C4;
       const int ih = ph - g.pad, iw = pw - g.pad;
-      const float4 v = ((unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W) ? __ldg(x4 + ih * g.W + iw)
-                                                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-      sts4(scr + i * 16, v);
+      const bool in = (unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W;
+      cp_async16(scr + i * 16, in ? x4 + (ih * g.W + iw) * C4 + c4 : x4, in ? 16 : 0);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     producer_bar_sync();
     staged = n;
   }
@@ -428,7 +435,7 @@ struct LdConvFwdSmemA {
   template <int T>
   struct State {
     uint32_t scr;
-    int pix[Place<T>::N];  // padded-image offset of (oh*st, ow*st), -1 past the end
+    int pix[Place<T>::N];  // granule offset of (oh*st, ow*st, 0), -1 past the end
   };
   template <int T>
   __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
@@ -441,7 +448,7 @@ struct LdConvFwdSmemA {
       if (m < Mtot) {
         const int n = g.fHoWo.div(m), rem = m - n * g.Ho * g.Wo;
         const int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
-        s.pix[i] = oh * g.st * im.Wp + ow * g.st;
+        s.pix[i] = (oh * g.st * im.Wp + ow * g.st) * im.C4;
       }
     }
   }
@@ -454,10 +461,11 @@ struct LdConvFwdSmemA {
   template <int T>
   __device__ __forceinline__ void load(const State<T>& s, uint32_t sm, int k0, int tid) const {
     const ConvGeom& g = im.g;
-    const int tap = (k0 >> 2) + (tid & 7);  // C == 4: k = 4 * tap + c
-    const bool kok = tap < g.R * g.S;
+    const int k = k0 + (tid & 7) * 4;  // k = (r*S + s)*C + c, c % 4 == 0
+    const bool kok = k < g.R * g.S * g.C;
+    const int tap = g.fC.div(k), c4 = (k - tap * g.C) >> 2;
     const int r = g.fS.div(tap), sc = tap - r * g.S;
-    const int off = r * im.Wp + sc;
+    const int off = (r * im.Wp + sc) * im.C4 + c4;
 #pragma unroll
     for (int i = 0; i < Place<T>::N; ++i) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -478,18 +486,19 @@ struct LdConvWgradSmemA {
   template <int T>
   struct State {
     uint32_t scr;
-    int off;   // padded-image offset of tap (r, s)
+    int off;   // granule offset of (r, s, c4)
     int mode;  // 0 zero, 1 data, 2 ones
   };
   template <int T>
   __device__ __forceinline__ void init(State<T>& s, int row0, int tid) const {
     const ConvGeom& g = im.g;
-    const int kg = row0 + Place<T>::mn(tid);  // multiple of 4: c = 0
+    const int kg = row0 + Place<T>::mn(tid);  // multiple of 4
     s.mode = 0;
     s.off = 0;
-    if (kg < g.R * g.S * 4) {
-      const int tap = kg >> 2, r = g.fS.div(tap), sc = tap - r * g.S;
-      s.off = r * im.Wp + sc;
+    if (kg < g.R * g.S * g.C) {
+      const int tap = g.fC.div(kg), c4 = (kg - tap * g.C) >> 2;
+      const int r = g.fS.div(tap), sc = tap - r * g.S;
+      s.off = (r * im.Wp + sc) * im.C4 + c4;
       s.mode = 1;
     } else if (kg == ones_row) {
       s.mode = 2;
@@ -514,7 +523,7 @@ struct LdConvWgradSmemA {
         if (s.mode == 1) {
           const int rem = p - g.fHoWo.div(p) * HoWo;
           const int oh = g.fWo.div(rem), ow = rem - oh * g.Wo;
-          v = lds4(s.scr + (oh * g.st * im.Wp + ow * g.st + s.off) * 16);
+          v = lds4(s.scr + ((oh * g.st * im.Wp + ow * g.st) * im.C4 + s.off) * 16);
         } else if (s.mode == 2) {
           v.x = 1.f;
         }
@@ -778,9 +787,12 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t sm, int kk) {
   }
 }
 
-template <int BN>
+template <int BN, int SCRATCH = 0>
 constexpr int gemm_stages() {
-  return BN <= 32 ? 8 : BN <= 64 ? 7 : BN <= 128 ? 6 : 4;
+  // default depth; with a loader scratch as many stages as fit 225 KB
+  constexpr int d = BN <= 32 ? 8 : BN <= 64 ? 7 : BN <= 128 ? 6 : 4;
+  constexpr int fit = (225 * 1024 - SCRATCH) / ((GEMM_BM + BN) * GEMM_BK * 4);
+  return d < fit ? d : fit;
 }
 
 template <int BN, int STAGES, int SCRATCH = 0>
@@ -834,6 +846,21 @@ __device__ __forceinline__ void epi_store16(const EpiArgs& e, int row, int col0,
       *out_at(e, row, col, N) = o;
   }
 }
+
+// Optional per-role timeline of CTA 0 (build variant -D SG_GEMM_TRACE; read with
+// sg_debug_gemm_trace): rows = producer start / end of a k-block, MMA operands
+// ready / issued, epilogue accumulator ready / released per tile, kernel start.
+#ifdef SG_GEMM_TRACE
+__device__ long long g_gemm_trace[7][256];
+#define SG_TRACE(row, idx)                                                            \
+  do {                                                                                \
+    if (blockIdx.x == 0 && (idx) < 256) g_gemm_trace[row][idx] = (long long)clock64(); \
+  } while (0)
+#else
+#define SG_TRACE(row, idx) \
+  do {                     \
+  } while (0)
+#endif
 
 // Persistent warp-specialised kernel.  Work items = (M tile, N tile, K split),
 // strided over the CTAs; the operand pipeline runs across work items without
@@ -929,6 +956,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   const uint32_t tmem = *tmem_slot_ptr;
   // the prologue above overlapped the previous kernel; its outputs are read below
   pdl_entry();
+  if (tid == 0) SG_TRACE(6, 0);
 
   if (warp < MMA_WARP) {
     // ------------------------------- producers -------------------------------
@@ -947,6 +975,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
             const int s = it % STAGES;
             const int round = it / STAGES;
             if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
+            if (lane == 0) SG_TRACE(0, it);
             const uint32_t sa = sbase + s * STAGE_BYTES;
             // constant operand atoms (zeros / the bias ones-row) are written by the warp
             bool wrote = false;
@@ -980,6 +1009,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
               args.a.template issue<GEMM_BM>(sa, m0, k0, full);
               args.b.template issue<BN>(sa + A_BYTES, n0, k0, full);
               mbar_arrive(full);
+              SG_TRACE(1, it);
             }
             __syncwarp();
           }
@@ -1001,6 +1031,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
           const int s = it % STAGES;
           const int round = it / STAGES;
           if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
+          if (tid == 0) SG_TRACE(0, it);
           const uint32_t sa = sbase + s * STAGE_BYTES;
           const int k0 = (kb0 + j) * GEMM_BK;
           if constexpr (SCRATCH > 0) args.a.template prepare<GEMM_BM>(sa_st, staged, scratch, mi * GEMM_BM, k0, tid);
@@ -1010,6 +1041,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
             // the barrier counts this thread's arrival once its copies have
             // landed; the MMA warp fences them into the async proxy
             cp_async_mbar_arrive_noinc(bar_base + 8 * s);
+            if (tid == 0) SG_TRACE(1, it);
             continue;
           }
           cp_async_commit();
@@ -1045,7 +1077,12 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
       const uint32_t acc = tmem + b * BN;
       for (int j = 0; j < nkb; ++j, ++it) {
         const int s = it % STAGES;
+#ifdef SG_MMA_BACKOFF
+        mbar_wait_sleep(bar_base + 8 * s, (it / STAGES) & 1);
+#else
         mbar_wait(bar_base + 8 * s, (it / STAGES) & 1);
+#endif
+        if (lane == 0) SG_TRACE(2, it);
         if constexpr (!TMA) {
           if (args.async_arrive) fence_proxy_async_smem();  // producers' generic-proxy writes -> tensor core
         }
@@ -1059,6 +1096,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
             mma_tf32(acc, ad, bd, idesc, (j | kk) ? 1u : 0u);
           }
           mma_commit(bar_base + 8 * (STAGES + s));
+          SG_TRACE(3, it);
         }
         __syncwarp();
       }
@@ -1079,7 +1117,12 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
       wd.get(w, mi, ni, si);
       kb_range(si, kb0, nkb);
       const int b = local & 1;
+#ifdef SG_EPI_BACKOFF
+      mbar_wait_sleep(tfull_bar + 8 * b, (local >> 1) & 1);
+#else
       mbar_wait(tfull_bar + 8 * b, (local >> 1) & 1);
+#endif
+      if (warp == EPI_WARP0 && lane == 0) SG_TRACE(4, local);
       tc_fence_after();
       const int m0 = mi * GEMM_BM, n0 = ni * BN;
       const int row = m0 + lg * 32 + lane;
@@ -1113,6 +1156,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
       // this buffer's accumulator has been read: release it to the MMA warp
       tc_fence_before();
       mbar_arrive(tempty_bar + 8 * b);
+      if (warp == EPI_WARP0 && lane == 0) SG_TRACE(5, local);
       if (e.ws && e.cnt) {
         // Split-K fix-up: the split that finishes a tile last (tile counter) sums
         // every split's partial in ascending split order and applies the

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(512) splitk_reduce_kernel(const float* __restr
 
 template <int BN, class LA, class LB>
 cudaError_t launch_bn(const GemmArgs<LA, LB>& args, const Plan& p, cudaStream_t st) {
-  constexpr int STAGES = gemm_stages<BN>();
+  constexpr int STAGES = gemm_stages<BN, ScratchOf<LA>::value>();
   constexpr int SMEM = gemm_smem_bytes<BN, STAGES, ScratchOf<LA>::value>();
   auto kern = gemm_tc_kernel<BN, STAGES, LA, LB>;
   static bool configured = false;
@@ -414,12 +414,13 @@ bool smem_im2col_ok(const ConvShape& s, int unit, SmemImage* im) {
   static int on = -1;
   if (on < 0) {
     const char* env = getenv("SG_SMEM_IM2COL");
-    on = env ? atoi(env) != 0 : 1;
+    on = env ? atoi(env) : 1;
   }
-  if (!on || s.C != 4 || (s.Ho * s.Wo) % unit != 0) return false;
-  const int Hp = (s.Ho - 1) * s.st + s.R, Wp = (s.Wo - 1) * s.st + s.S;
-  if ((long long)Hp * Wp * 16 > kIm2colScratch) return false;
-  *im = SmemImage{nullptr, geom(s), Hp, Wp};
+  // 1: 4-channel layers only; 2: every layer whose padded image fits
+  if (!on || s.C % 4 != 0 || (on == 1 && s.C != 4) || (s.Ho * s.Wo) % unit != 0) return false;
+  const int Hp = (s.Ho - 1) * s.st + s.R, Wp = (s.Wo - 1) * s.st + s.S, C4 = s.C / 4;
+  if ((long long)Hp * Wp * C4 * 16 > kIm2colScratch) return false;
+  *im = SmemImage{nullptr, geom(s), Hp, Wp, C4, make_fastdiv(Wp * C4), make_fastdiv(C4)};
   return true;
 }
 
@@ -680,3 +681,10 @@ cudaError_t gemm_plain(const float* A, int ta, const float* B, int tb, float* C,
 }
 
 }  // namespace sg
+
+#ifdef SG_GEMM_TRACE
+// Debug-variant export of the CTA-0 GEMM timeline (7 x 256 clock64 values).
+extern "C" __attribute__((visibility("default"))) int sg_debug_gemm_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, sg::g_gemm_trace, sizeof(sg::g_gemm_trace));
+}
+#endif

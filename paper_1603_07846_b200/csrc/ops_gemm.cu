@@ -480,6 +480,7 @@ size_t colsum_ws_floats(int M, int N) { return (size_t)((M + CS_ROWS_PER_BLOCK -
 cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const float* b, float* y, int relu,
                      Workspace ws, cudaStream_t st) {
   const int M = s.N * s.Ho * s.Wo, N = s.Co, K = s.R * s.S * s.C;
+  if (conv_img_fwd_ok(s) && aligned16p(x) && aligned16p(W) && aligned16p(y)) return conv_img_fwd(s, x, W, b, y, relu, st);
   const EpiArgs e = epi_plain(y, s.Co, 0, b, 0, relu, M);
   if (tma_on(0) && s.C % 32 == 0 && aligned16p(x)) {
     bool ok = true;
@@ -515,6 +516,7 @@ cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const f
 cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* W, float* dx, Workspace ws,
                        cudaStream_t st) {
   const int M = s.N * s.H * s.W, N = s.C, K = s.R * s.S * s.Co;
+  if (conv_img_dgrad_ok(s) && aligned16p(dy) && aligned16p(W) && aligned16p(dx)) return conv_img_dgrad(s, dy, W, dx, st);
   const EpiArgs e = epi_plain(dx, s.C, 0, nullptr, 0, 0, M);
   if (tma_on(1) && s.st == 1 && s.Co % 32 == 0 && s.C % 32 == 0 && aligned16p(dy) && aligned16p(W)) {
     bool ok = true;

@@ -45,6 +45,8 @@ CONV = [  # N, H, W, C, Co, R, stride, pad
     (3, 12, 10, 4, 8, 3, 1, 1),       # direct path, ragged Wo (10 = 2 x 4 + 2)
     (4, 16, 16, 32, 32, 5, 1, 2),     # CIFAR conv2
     (8, 8, 8, 32, 64, 5, 1, 2),       # CIFAR conv3
+    (3, 10, 7, 32, 32, 3, 1, 1),      # resident-image path, non-square, 3x3
+    (2, 11, 11, 64, 32, 3, 1, 0),     # resident-image path, 2 K blocks, no padding
     (2, 35, 35, 4, 64, 11, 4, 2),     # AlexNet conv1 geometry
     (2, 27, 27, 64, 192, 5, 1, 2),    # AlexNet conv2 (TMA wgrad, C = 64)
     (2, 13, 13, 192, 384, 3, 1, 1),   # AlexNet conv3
@@ -73,6 +75,19 @@ def test_conv(case):
     assert normwise(host(dW), rdW) < TF32_TOL
     assert normwise(host(db), rdb) < TF32_TOL   # fused ones-row of the TF32 wgrad GEMM
     assert normwise(host(dx), rdx) < TF32_TOL
+
+
+def test_conv_resident_image_path():
+    """The opt-in resident-image convolution (SG_IMG_CONV=1, read once per
+    process) passes the same conv parity cases in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_ops.py", "-m", "gpu", "-q", "-x",
+                        "-k", "test_conv and not rejects and not resident", "-p", "no:cacheprovider"],
+                       cwd=root, env=dict(os.environ, SG_IMG_CONV="1"), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 def test_conv_rejects_unpadded_channels():

@@ -919,12 +919,14 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   const int nwork = wd.mt * wd.nt * (wd.splits > 0 ? wd.splits : 1);
   // work items of this CTA: strided (neighbouring CTAs share operand tiles in
   // L2) or, for loaders that keep per-sample state, one contiguous range
-  int w_first = blockIdx.x, w_end = nwork, w_step = gridDim.x;
-  if constexpr (ContiguousOf<LA>::value) {
-    w_first = (int)((long long)nwork * blockIdx.x / gridDim.x);
-    w_end = (int)((long long)nwork * (blockIdx.x + 1) / gridDim.x);
-    w_step = 1;
-  }
+  // (the loops stay "w = blockIdx.x; w < nwork_it; w += gridDim.x"; a stateful
+  // loader remaps the j-th item of CTA b to item b*per + j and skips the tail)
+  constexpr bool CONTIG = ContiguousOf<LA>::value;
+  const int per_cta = CONTIG ? (nwork + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const int nwork_it = CONTIG ? per_cta * (int)gridDim.x : nwork;
+  auto work_of = [&](int w) {
+    return CONTIG ? (w % (int)gridDim.x) * per_cta + w / (int)gridDim.x : w;
+  };
   auto kb_range = [&](int si, int& kb0, int& nkb) {
     kb0 = si * args.kb_per_split;
     int e = kb0 + args.kb_per_split;
@@ -966,9 +968,10 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
         int tagA[STAGES], tagB[STAGES];  // row0 the stage's constant atoms were written for
 #pragma unroll
         for (int s = 0; s < STAGES; ++s) tagA[s] = tagB[s] = -1;
-        for (int w = w_first; w < w_end; w += w_step) {
+        for (int w = blockIdx.x; w < nwork_it; w += gridDim.x) {
+          if (CONTIG && work_of(w) >= nwork) break;
           int mi, ni, si, kb0, nkb;
-          wd.get(w, mi, ni, si);
+          wd.get(work_of(w), mi, ni, si);
           kb_range(si, kb0, nkb);
           const int m0 = mi * GEMM_BM, n0 = ni * BN;
           for (int j = 0; j < nkb; ++j, ++it) {
@@ -1019,9 +1022,10 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
       int it = 0;
       int staged = -1;  // sample whose padded image is in the scratch (smem im2col loaders)
       (void)staged;
-      for (int w = w_first; w < w_end; w += w_step) {
+      for (int w = blockIdx.x; w < nwork_it; w += gridDim.x) {
+        if (CONTIG && work_of(w) >= nwork) break;
         int mi, ni, si, kb0, nkb;
-        wd.get(w, mi, ni, si);
+        wd.get(work_of(w), mi, ni, si);
         kb_range(si, kb0, nkb);
         typename LA::template State<GEMM_BM> sa_st;
         typename LB::template State<BN> sb_st;
@@ -1066,9 +1070,10 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
     // --------------- MMA issuer: the whole warp waits, lane 0 issues ---------------
     constexpr uint32_t idesc = idesc_tf32(GEMM_BM, BN, LA::kMN & 1, LB::kMN & 1);
     int it = 0, local = 0;
-    for (int w = w_first; w < w_end; w += w_step, ++local) {
+    for (int w = blockIdx.x; w < nwork_it; w += gridDim.x, ++local) {
+      if (CONTIG && work_of(w) >= nwork) break;
       int mi, ni, si, kb0, nkb;
-      wd.get(w, mi, ni, si);
+      wd.get(work_of(w), mi, ni, si);
       kb_range(si, kb0, nkb);
       const int b = local & 1;
       const int use = local >> 1;  // how many times buffer b was used before
@@ -1112,9 +1117,10 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
     const bool plain_vec = !e.trans && e.cb >= args.N && (e.ld & 3) == 0 && !e.bias_on_m;
     __shared__ int s_last;
     int local = 0;
-    for (int w = w_first; w < w_end; w += w_step, ++local) {
+    for (int w = blockIdx.x; w < nwork_it; w += gridDim.x, ++local) {
+      if (CONTIG && work_of(w) >= nwork) break;
       int mi, ni, si, kb0, nkb;
-      wd.get(w, mi, ni, si);
+      wd.get(work_of(w), mi, ni, si);
       kb_range(si, kb0, nkb);
       const int b = local & 1;
 #ifdef SG_EPI_BACKOFF

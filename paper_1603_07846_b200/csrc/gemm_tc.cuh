@@ -800,6 +800,36 @@ constexpr int gemm_smem_bytes() {
   return STAGES * (GEMM_BM * GEMM_BK * 4 + BN * GEMM_BK * 4) + SCRATCH + 1024 /*align*/ + 256 /*barriers*/;
 }
 
+// Second counter block of the split-K workspace head (re-arm counters).
+constexpr int kSplitDone = 256;
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Final epilogue of 4 consecutive columns (col0 .. col0+3, guarded by N).
+__device__ __forceinline__ void epi_store4(const EpiArgs& e, int row, int col0, float4 v4, int N) {
+  const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int col = col0 + j;
+    if (col >= N) break;
+    float o = v[j];
+    if (row >= e.mvalid) {
+      if (row == e.xrow) e.xout[col] = o;
+      continue;
+    }
+    if (e.bias) o += e.bias_on_m ? e.bias[row] : e.bias[col];
+    if (e.relu) o = fmaxf(o, 0.f);
+    if (e.trans)
+      *out_at(e, col, row, e.mvalid) = o;
+    else
+      *out_at(e, row, col, N) = o;
+  }
+}
+
 // Final epilogue of 16 consecutive accumulator columns of one row: bias, ReLU,
 // plain / transposed / column-blocked store, or the bias-gradient row (xrow).
 __device__ __forceinline__ void epi_store16(const EpiArgs& e, int row, int col0, const float (&v)[16], int N,
@@ -1115,7 +1145,6 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
     const int cbeg = ((warp - EPI_WARP0) >> 2) * HALF;
     const EpiArgs& e = args.epi;
     const bool plain_vec = !e.trans && e.cb >= args.N && (e.ld & 3) == 0 && !e.bias_on_m;
-    __shared__ int s_last;
     int local = 0;
     for (int w = blockIdx.x; w < nwork_it; w += gridDim.x, ++local) {
       if (CONTIG && work_of(w) >= nwork) break;
@@ -1164,41 +1193,44 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
       mbar_arrive(tempty_bar + 8 * b);
       if (warp == EPI_WARP0 && lane == 0) SG_TRACE(5, local);
       if (e.ws && e.cnt) {
-        // Split-K fix-up: the split that finishes a tile last (tile counter) sums
-        // every split's partial in ascending split order and applies the
-        // epilogue; the order does not depend on which split is last.
+        // Cooperative split-K reduction.  The planner keeps tiles x splits <= the
+        // grid, so every split of a tile is a resident CTA with exactly this one
+        // work item: once all S partials of the tile are written (tile counter),
+        // split si sums rows [si*BM/S, (si+1)*BM/S) of the tile over the splits in
+        // ascending order and applies the epilogue (deterministic).
+        const int t = mi + wd.mt * ni, S = wd.splits;
         __threadfence();
         epi_bar_sync();
         if (warp == EPI_WARP0 && lane == 0) {
-          const int t = mi + wd.mt * ni;
-          s_last = atomicAdd(e.cnt + t, 1) == wd.splits - 1;
-          if (s_last) e.cnt[t] = 0;  // every split has arrived: re-arm for the next GEMM
+          atomicAdd(e.cnt + t, 1);
+          while (ld_acquire_gpu(e.cnt + t) < S) __nanosleep(32);
         }
         epi_bar_sync();
-        if (s_last) {
-          __threadfence();
-          if (row < args.M) {
-#pragma unroll 1
-            for (int c0 = cbeg; c0 < cbeg + HALF; c0 += 16) {
-              if (n0 + c0 >= args.N) break;
-              float v[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] = 0.f;
-              const float* src = e.ws + (long long)row * e.ws_ld + n0 + c0;
-#pragma unroll 2
-              for (int s2 = 0; s2 < wd.splits; ++s2) {
-                const float4* q = reinterpret_cast<const float4*>(src + (long long)s2 * e.ws_split_stride);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const float4 u = __ldcg(q + i);
-                  v[4 * i] += u.x;
-                  v[4 * i + 1] += u.y;
-                  v[4 * i + 2] += u.z;
-                  v[4 * i + 3] += u.w;
-                }
-              }
-              epi_store16(e, row, n0 + c0, v, args.N, plain_vec);
-            }
+        __threadfence();
+        const int r_b = m0 + si * GEMM_BM / S;
+        const int r_e = min(m0 + (si + 1) * GEMM_BM / S, args.M);
+        constexpr int C4 = BN / 4;
+        const int et = (warp - EPI_WARP0) * 32 + lane;
+        for (int idx = et; idx < (r_e - r_b) * C4; idx += GEMM_EPI_WARPS * 32) {
+          const int r = r_b + idx / C4, c = n0 + (idx % C4) * 4;
+          if (c >= args.N) continue;
+          const float* src = e.ws + (long long)r * e.ws_ld + c;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int s2 = 0; s2 < S; ++s2) {
+            const float4 u = __ldcg(reinterpret_cast<const float4*>(src + (long long)s2 * e.ws_split_stride));
+            acc.x += u.x;
+            acc.y += u.y;
+            acc.z += u.z;
+            acc.w += u.w;
+          }
+          epi_store4(e, r, c, acc, args.N);
+        }
+        // re-arm both counters once every split has finished its slice
+        epi_bar_sync();
+        if (warp == EPI_WARP0 && lane == 0) {
+          if (atomicAdd(e.cnt + kSplitDone + t, 1) == S - 1) {
+            e.cnt[t] = 0;
+            e.cnt[kSplitDone + t] = 0;
           }
         }
       }

@@ -40,12 +40,13 @@ namespace {
 
 constexpr int kNumSMs = 148;
 constexpr int kMinKbPerSplit = 8;
-constexpr int kSplitCounters = 256;  // ints at the head of the workspace (>= kNumSMs tiles)
+constexpr int kSplitCounters = 512;  // ints at the head of the workspace: 2 x 256 tile counters
 
-// Split-K reduction in a separate fixed-order kernel (default) or inside the GEMM
-// (SG_SPLITK_FIXUP=1: the last split of a tile sums the partials).  Measured
-// slower in-kernel on every config (CIFAR 410K -> 301K img/s): with few tiles and
-// many splits one CTA per tile serialises the whole reduction.
+// Split-K reduction by a separate fixed-order kernel (default) or inside the GEMM
+// by the splits themselves (SG_SPLITK_FIXUP=1: every split of a tile is a
+// resident CTA and reduces a row slice once the tile counter is full).  The
+// in-GEMM variant measured slower on every config (CIFAR-10 467K -> 424K img/s,
+// MLP ip1 forward 16 -> 29 us): the cross-CTA wait costs more than the launch.
 bool splitk_fixup() {
   static int on = -1;
   if (on < 0) {
@@ -186,7 +187,8 @@ cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int
   // workspace: kSplitCounters tile counters (kept zero between GEMMs), then the
   // split partials [split][M][pad4(N)]
   float* part = ws.ptr + kSplitCounters;
-  const bool fixup = splitk_fixup() && p.mt * p.nt <= kSplitCounters;
+  // cooperative reduction needs one resident CTA per work item
+  const bool fixup = splitk_fixup() && p.mt * p.nt * p.splits <= kNumSMs && p.mt * p.nt <= kSplitDone;
   args.epi.cnt = nullptr;
   if (p.splits > 1) {
     args.epi.ws = part;

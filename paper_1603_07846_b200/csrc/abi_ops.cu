@@ -134,6 +134,7 @@ SG_API sg_status sg_op_conv_backward(const sg_conv_desc* d, const float* x, cons
   size_t need = gemm_ws_floats(s.R * s.S * s.C, s.Co, Mtot);
   size_t cs = colsum_ws_floats(Mtot, s.Co);
   if (cs > need) need = cs;
+  need = std::max(need, conv_img_wgrad_ws_floats(s));
   if (dx) {
     size_t dn = gemm_ws_floats(s.N * s.H * s.W, s.C, s.R * s.S * s.Co);
     if (dn > need) need = dn;

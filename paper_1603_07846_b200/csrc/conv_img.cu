@@ -10,8 +10,9 @@
 // (r*Wp + s) rows further into the image: output pixel q = oh*Wp + ow
 // ("padded-width" numbering, columns ow >= Wo are discarded) reads input row
 // q + r*Wp + s.  The swizzle is address-based, so any 128-byte row start is a
-// valid operand (probed by tools/desc_shift.cu).  No per-tile operand traffic
-// remains except the filter taps, streamed through a cp.async ring.
+// valid operand (probed by tools/desc_shift.cu).  The image and the whole
+// filter bank are staged by a handful of TMA boxes (zero padding = TMA
+// out-of-bounds fill); after that the CTA issues MMAs only.
 //
 //   forward  y[q][co]  = b[co] + sum_{t, c} img_x[q + off_t][c] * W[co][t][c]
 //            B = W tap tile K-major (row co, 32 channels per block)
@@ -19,19 +20,24 @@
 //            (dy padded by R-1-p: a forward convolution with the flipped kernel)
 //            B = W tap tile MN-major (k-line co, 32 output channels per atom)
 //
-// Roles (192 threads): warps 0-3 stage the image (cp.async, mbarrier
-// completion) and run the epilogue (TMEM lane group = warp); warp 4 streams the
-// taps; warp 5 allocates TMEM and issues the MMAs (one elected lane).  All
-// accumulators of the sample (tiles x N columns) stay in TMEM until the end.
+// Roles (160 threads): thread 0 issues the TMA staging; warp 4 allocates TMEM
+// and issues the MMAs (one lane); warps 0-3 run the epilogue (TMEM lane group =
+// warp).  All accumulators of the sample (tiles x N columns) stay in TMEM.
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #include "ops.h"
 #include "sg_common.cuh"
 
 namespace sg {
+
+bool encode_tiled_f32(CUtensorMap* m, const void* p, int rank, const cuuint64_t* dims, const cuuint64_t* strides_b,
+                      const cuuint32_t* box, CUtensorMapSwizzle sw);
+
 namespace {
 
-constexpr int kImgThreads = 192;
+constexpr int kImgThreads = 160;
 
 #ifdef SG_GEMM_TRACE
 __device__ long long g_img_trace[6][64];  // CTA 0: tap produced / tap ready / tap issued, image ready, done, start
@@ -44,9 +50,10 @@ __device__ long long g_img_trace[6][64];  // CTA 0: tap produced / tap ready / t
   do {                      \
   } while (0)
 #endif
-constexpr int kMaxStages = 8;
 
 struct ImgConvArgs {
+  CUtensorMap img_map;  // source NHWC viewed {C, W, H, N}, box {32, Wp, Hrows, 1}, SWIZZLE_128B
+  CUtensorMap w_map;    // filter viewed {C, Co, T} (fwd) / {C, 32-co block rows, T} (dgrad), box {32, rows, T}
   const float* src;    // NHWC [nimg][H][W][C] (x, or dy for dgrad)
   const float* wt;     // KRSC [Co][R][S][C] of the layer
   const float* bias;   // [N] or null
@@ -57,157 +64,108 @@ struct ImgConvArgs {
   int N;               // output channels (multiple of 32)
   int layer_c, layer_co;  // the layer's C / Co (weight tensor strides)
   int ntiles, img_rows, relu, dgrad;
-  int G, NS;  // filter taps per ring stage, ring stages (G = R*S, NS = 1: filter bank resident)
+  int Hrows;  // padded image rows staged (img_rows = Hrows * Wp rounded up to 8)
 };
 
 __device__ __forceinline__ uint32_t ksw(int row, int chunk) {  // K-major SW128 offset of a 16-B chunk
   return row * 128 + ((chunk ^ (row & 7)) << 4);
 }
 
-template <int NB, bool DGRAD>
+// NT output tiles of 128 padded-width rows, CB 32-channel K blocks of the
+// source (compile time, so the MMA issue of a tap is straight-line code).
+// Shared memory: image planes [CB][img_rows][128 B], then the filter bank
+//   forward: [CB][T][Co][128 B]  (K-major SW128, row co of tap t, block cb)
+//   dgrad:   [KB][NA][T][32][128 B]  (MN-major BASE32B, k-line co_in of tap t,
+//            K block kb of the layer's Co, atom a of the layer's C; taps in the
+//            layer's order, the flip is applied when the MMA picks the tap).
+template <int NB, bool DGRAD, int NT, int CB>
 __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_constant__ ImgConvArgs a) {
-  constexpr int TAP_BYTES_PER_CB = NB * 128;  // one 32-wide K block of a tap tile
+  constexpr int TCOLS = NT * NB <= 32 ? 32 : NT * NB <= 64 ? 64 : NT * NB <= 128 ? 128 : NT * NB <= 256 ? 256 : 512;
+  constexpr int NA = NB / 32;  // dgrad: MN atoms of the output channels
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const int CB = a.C / 32;
   const uint32_t img = base;
   const uint32_t img_plane = a.img_rows * 128;
-  const uint32_t wstage0 = img + CB * img_plane;
-  const uint32_t tap_bytes = CB * TAP_BYTES_PER_CB;
-  const uint32_t stage_bytes = a.G * tap_bytes;
-  const int T = a.R * a.S, NS = a.NS, chunks = (T + a.G - 1) / a.G;
-  const uint32_t bars = wstage0 + NS * stage_bytes;  // full[NS], empty[NS], img, done
-  const uint32_t img_bar = bars + 16 * kMaxStages, done_bar = img_bar + 8, slot = done_bar + 8;
+  const uint32_t wbase = img + CB * img_plane;
+  const int T = a.R * a.S;
+  const uint32_t wbytes = (uint32_t)CB * T * NB * 128;
+  const uint32_t bar = wbase + wbytes, done_bar = bar + 8, slot = done_bar + 8;
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = blockIdx.x;
-  int tcols = 32;
-  while (tcols < a.ntiles * NB) tcols <<= 1;
 
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(bars + 8 * s, 32);                // producer lanes (cp.async arrive)
-      mbar_init(bars + 8 * (kMaxStages + s), 1);  // tcgen05.commit
-    }
-    mbar_init(img_bar, 128);
+    mbar_init(bar, 1);
     mbar_init(done_bar, 1);
     fence_barrier_init();
+    prefetch_tmap(&a.img_map);
+    prefetch_tmap(&a.w_map);
   }
-  if (warp == 5) {
-    if (tcols <= 32) tmem_alloc<32>(slot);
-    else if (tcols <= 64) tmem_alloc<64>(slot);
-    else if (tcols <= 128) tmem_alloc<128>(slot);
-    else if (tcols <= 256) tmem_alloc<256>(slot);
-    else tmem_alloc<512>(slot);
-  }
+  if (warp == 4) tmem_alloc<TCOLS>(slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot_ptr;
   pdl_entry();
-  if (tid == 0) IMG_TRACE(5, 0);
-
-  if (warp < 4) {
-    // ---- stage the zero-padded image: plane cb, row rho = ph*Wp + pw ----
-    const float4* src = reinterpret_cast<const float4*>(a.src) + (size_t)n * a.H * a.W * (a.C / 4);
-    const int chunks = CB * a.img_rows * 8;
-    for (int i = tid; i < chunks; i += 128) {
-      const int cb = i / (a.img_rows * 8), rem = i - cb * a.img_rows * 8;
-      const int rho = rem >> 3, c16 = rem & 7;
-      const int ph = rho / a.Wp, pw = rho - ph * a.Wp;
-      const int ih = ph - a.pad, iw = pw - a.pad;
-      const bool in = rho < a.Hp * a.Wp && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
-      cp_async16(img + cb * img_plane + ksw(rho, c16), in ? src + ((ih * a.W + iw) * (a.C / 4) + cb * 8 + c16) : src,
-                 in ? 16 : 0);
+  if (tid == 0) {
+    IMG_TRACE(5, 0);
+    // one box per 32-channel plane (zero padding by out-of-bounds fill) + the filter bank
+    const uint32_t img_tx = (uint32_t)a.Hrows * a.Wp * 128;
+    mbar_arrive_expect_tx(bar, CB * img_tx + wbytes);
+    for (int cb = 0; cb < CB; ++cb)
+      tma_load_4d(img + cb * img_plane, &a.img_map, cb * 32, -a.pad, -a.pad, n, bar);
+    if (!DGRAD) {
+      for (int cb = 0; cb < CB; ++cb) tma_load_3d(wbase + cb * T * NB * 128, &a.w_map, cb * 32, 0, 0, bar);
+    } else {
+      for (int kb = 0; kb < CB; ++kb)
+        for (int at = 0; at < NA; ++at) tma_load_3d(wbase + (kb * NA + at) * T * 4096, &a.w_map, at * 32, kb * 32, 0, bar);
     }
-    cp_async_mbar_arrive_noinc(img_bar);
-  } else if (warp == 4) {
-    // ---- stream the filter taps through the ring, G taps per stage ----
-    for (int ch = 0; ch < chunks; ++ch) {
-      const int s = ch % NS, round = ch / NS;
-      if (round > 0) mbar_wait(bars + 8 * (kMaxStages + s), (round - 1) & 1);
-      const int t_end = min(T, (ch + 1) * a.G);
-      for (int t = ch * a.G; t < t_end; ++t) {
-        const uint32_t st = wstage0 + s * stage_bytes + (t - ch * a.G) * tap_bytes;
-        const int r = t / a.S, sc = t - r * a.S;
-        if (!DGRAD) {
-          // B[n = co][k = c] K-major: chunk (cb, co, c16) <- W[co][r][s][cb*32 + 4*c16 ..]
-          for (int i = lane; i < CB * NB * 8; i += 32) {
-            const int cb = i / (NB * 8), rem = i - cb * NB * 8, co = rem >> 3, c16 = rem & 7;
-            const float* g = a.wt + ((size_t)(co * T + t) * a.layer_c + cb * 32 + c16 * 4);
-            cp_async16(st + cb * TAP_BYTES_PER_CB + ksw(co, c16), g, 16);
-          }
-        } else {
-          // B[n = c][k = co] MN-major, flipped tap: k-line co (K block kb), atom c/32,
-          // 16-B chunk of 4 c <- W[co][R-1-r][S-1-s][c ..]
-          const int tsrc = (a.R - 1 - r) * a.S + (a.S - 1 - sc);
-          for (int i = lane; i < CB * NB * 8; i += 32) {
-            const int kb = i / (NB * 8), rem = i - kb * NB * 8;
-            const int co_in = rem / (NB / 4), cq = rem - co_in * (NB / 4);  // cq: 4-channel chunk of c
-            const int c = cq * 4, atom = c >> 5, cin = c & 31;
-            const float* g = a.wt + ((size_t)((kb * 32 + co_in) * T + tsrc) * a.layer_c + c);
-            const uint32_t dst = st + kb * TAP_BYTES_PER_CB + atom * 4096 + co_in * 128 +
-                                 ((((cin >> 3) ^ (co_in & 3))) << 5) + ((cin >> 2) & 1) * 16;
-            cp_async16(dst, g, 16);
-          }
-        }
-      }
-      cp_async_mbar_arrive_noinc(bars + 8 * s);
-      if (lane == 0) IMG_TRACE(0, ch);
-    }
-    cp_async_wait_all();
-  } else {
-    // ---- MMA issue ----
+  }
+  if (warp == 4) {
+    // ---- MMA issue: one lane, straight-line MMAs per tap ----
     constexpr uint32_t idesc = idesc_tf32(128, NB, 0, DGRAD ? 1 : 0);
     const uint64_t ad0 = umma_desc_sw128(img, 16, 1024);
-    const uint64_t bd0 = DGRAD ? umma_desc_mn_sw128_32b(wstage0, 4096, 512) : umma_desc_sw128(wstage0, 16, 1024);
+    const uint64_t bd0 =
+        DGRAD ? umma_desc_mn_sw128_32b(wbase, (uint32_t)T * 4096, 512) : umma_desc_sw128(wbase, 16, 1024);
     const uint32_t a_lo0 = (uint32_t)ad0, a_hi = (uint32_t)(ad0 >> 32);
     const uint32_t b_lo0 = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
-    mbar_wait(img_bar, 0);
+    const uint32_t plane16 = img_plane >> 4;
+    mbar_wait(bar, 0);
     if (lane == 0) IMG_TRACE(3, 0);
-    fence_proxy_async_smem();
-    for (int ch = 0; ch < chunks; ++ch) {
-      const int s = ch % NS;
-      mbar_wait(bars + 8 * s, (ch / NS) & 1);
-      if (lane == 0) IMG_TRACE(1, ch);
-      fence_proxy_async_smem();
-      tc_fence_after();
-      if (lane == 0) {
-        // descriptor start fields advance by (bytes >> 4): tap shift off*128 B,
-        // tile 128 rows, channel plane, kk slice 32 B (K-major) / 1024 B (MN-major)
-        const int t_end = min(T, (ch + 1) * a.G);
-        for (int t = ch * a.G; t < t_end; ++t) {
-          const int r = t / a.S, sc = t - r * a.S;
-          const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc) * 8;
-          const uint32_t b_t = b_lo0 + (uint32_t)(s * stage_bytes + (t - ch * a.G) * tap_bytes) / 16;
-          for (int i = 0; i < a.ntiles; ++i) {
-            const uint32_t acc = tmem + i * NB;
-            for (int cb = 0; cb < CB; ++cb) {
-              const uint32_t a_c = a_t + (uint32_t)i * 1024 + (uint32_t)cb * (img_plane >> 4);
-              const uint32_t b_c = b_t + (uint32_t)cb * (TAP_BYTES_PER_CB >> 4);
+    tc_fence_after();
+    if (lane == 0) {
+      int r = 0, sc = 0;
+      for (int t = 0; t < T; ++t) {
+        const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc) * 8;
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                mma_tf32_lh(acc, a_c + kk * 2, a_hi, b_c + kk * (DGRAD ? 64 : 2), b_hi, idesc, (t | cb | kk) ? 1u : 0u);
-            }
+        for (int i = 0; i < NT; ++i)
+#pragma unroll
+          for (int cb = 0; cb < CB; ++cb) {
+            // forward: tap t of block cb; dgrad: flipped tap of K block cb (atom 0; LBO = T*4096)
+            const uint32_t b_c = DGRAD ? b_lo0 + ((uint32_t)(cb * NA * T + (T - 1 - t)) * 4096 >> 4)
+                                       : b_lo0 + ((uint32_t)(cb * T + t) * NB * 128 >> 4);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_tf32_lh(tmem + i * NB, a_t + i * 1024 + cb * plane16 + kk * 2, a_hi, b_c + kk * (DGRAD ? 64 : 2),
+                          b_hi, idesc, (t | cb | kk) ? 1u : 0u);
           }
+        if (++sc == a.S) {
+          sc = 0;
+          ++r;
         }
-        // release the stage only if the ring wraps onto it (a commit drains the pipe)
-        if (ch + NS < chunks) mma_commit(bars + 8 * (kMaxStages + s));
-        IMG_TRACE(2, ch);
       }
-      __syncwarp();
+      IMG_TRACE(2, 0);
+      mma_commit(done_bar);
     }
-    if (lane == 0) mma_commit(done_bar);
     __syncwarp();
-  }
-
-  if (warp < 4) {
+  } else {
     // ---- epilogue: TMEM lane = output row q of the tile ----
     mbar_wait_sleep(done_bar, 0);
     if (tid == 0) IMG_TRACE(4, 0);
     tc_fence_after();
     float* outn = a.out + (size_t)n * a.Ho * a.Wo * NB;
-    for (int i = 0; i < a.ntiles; ++i) {
+#pragma unroll 1
+    for (int i = 0; i < NT; ++i) {
       const int q = i * 128 + warp * 32 + lane;
       const int oh = q / a.Wp, ow = q - oh * a.Wp;
       const bool valid = oh < a.Ho && ow < a.Wo;
@@ -239,25 +197,20 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 4) {
     tc_fence_after();
-    if (tcols <= 32) tmem_dealloc<32>(tmem);
-    else if (tcols <= 64) tmem_dealloc<64>(tmem);
-    else if (tcols <= 128) tmem_dealloc<128>(tmem);
-    else if (tcols <= 256) tmem_dealloc<256>(tmem);
-    else tmem_dealloc<512>(tmem);
+    tmem_dealloc<TCOLS>(tmem);
   }
 }
 
-// Off by default (SG_IMG_CONV=1 enables it): on B200 the MMA issue of this
-// kernel runs at ~100 cycles per 128x32x8 TF32 MMA, twice the rate the same
-// instruction sequence reaches in tools/mma_rate.cu, and the CIFAR-10 conv2 / conv3
-// layers measured slower than the implicit GEMM (33 vs 25 us forward).
+// On by default (SG_IMG_CONV=0 falls back to the implicit GEMM).  Staging by
+// TMA matters: with per-thread cp.async staging the MMA issue ran at ~100 cycles
+// per 128x32x8 MMA instead of the ~48 measured here and in tools/mma_rate.cu.
 bool img_conv_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* env = getenv("SG_IMG_CONV");
-    on = env ? atoi(env) != 0 : 0;
+    on = env ? atoi(env) != 0 : 1;
   }
   return on != 0;
 }
@@ -282,32 +235,23 @@ bool plan_img(const ConvShape& s, bool dgrad, ImgConvArgs* a, size_t* smem) {
   g.Wo = g.Wp - s.S + 1;
   if (g.N != 32 && g.N != 64) return false;
   g.ntiles = (g.Ho * g.Wp + 127) / 128;
-  if (g.ntiles * g.N > 512) return false;
+  if (g.ntiles > 4 || g.C / 32 > 2) return false;
   g.img_rows = ((g.ntiles * 128 + (s.R - 1) * g.Wp + s.S - 1) + 7) / 8 * 8;
   g.dgrad = dgrad;
   const size_t CB = g.C / 32, T = (size_t)s.R * s.S;
-  const size_t tap_bytes = CB * g.N * 128, img_bytes = CB * g.img_rows * 128;
-  const size_t budget = 227 * 1024 - 1024 - 256;
-  if (img_bytes + 2 * tap_bytes > budget) return false;
-  const size_t wbudget = budget - img_bytes;
-  if (T * tap_bytes <= wbudget) {  // whole filter bank resident: one stage, no ring
-    g.G = (int)T;
-    g.NS = 1;
-  } else {  // ring of 2..8 stages of G taps
-    g.G = (int)std::max<size_t>(1, wbudget / (4 * tap_bytes));
-    const size_t chunks = (T + g.G - 1) / g.G;
-    g.NS = (int)std::min<size_t>({chunks, (size_t)kMaxStages, wbudget / (g.G * tap_bytes)});
-    if (g.NS < 2) return false;
-  }
-  *smem = 1024 + img_bytes + (size_t)g.NS * g.G * tap_bytes + 256;
+  g.Hrows = (g.img_rows + g.Wp - 1) / g.Wp;  // whole padded rows (TMA box), extra rows OOB-zero
+  if (g.Hrows > 256 || g.Wp > 256 || T > 256) return false;
+  g.img_rows = (g.Hrows * g.Wp + 7) / 8 * 8;
+  const size_t img_bytes = CB * g.img_rows * 128, w_bytes = CB * T * g.N * 128;
+  *smem = 1024 + img_bytes + w_bytes + 64;
   if (*smem > 227 * 1024) return false;
   *a = g;
   return true;
 }
 
-template <int NB, bool DG>
+template <int NB, bool DG, int NT, int CB>
 cudaError_t launch_img(const ImgConvArgs& a, size_t smem, int nimg, cudaStream_t st) {
-  auto k = conv_img_kernel<NB, DG>;
+  auto k = conv_img_kernel<NB, DG, NT, CB>;
   static size_t set = 0;
   if (smem > set) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -317,12 +261,284 @@ cudaError_t launch_img(const ImgConvArgs& a, size_t smem, int nimg, cudaStream_t
   return launch_k(k, nimg, kImgThreads, smem, st, a);
 }
 
+template <int NB, bool DG, int NT>
+cudaError_t run_img_cb(const ImgConvArgs& a, size_t smem, int nimg, cudaStream_t st) {
+  return a.C / 32 == 1 ? launch_img<NB, DG, NT, 1>(a, smem, nimg, st) : launch_img<NB, DG, NT, 2>(a, smem, nimg, st);
+}
+template <int NB, bool DG>
+cudaError_t run_img_nt(const ImgConvArgs& a, size_t smem, int nimg, cudaStream_t st) {
+  switch (a.ntiles) {
+    case 1: return run_img_cb<NB, DG, 1>(a, smem, nimg, st);
+    case 2: return run_img_cb<NB, DG, 2>(a, smem, nimg, st);
+    case 3: return run_img_cb<NB, DG, 3>(a, smem, nimg, st);
+    default: return run_img_cb<NB, DG, 4>(a, smem, nimg, st);
+  }
+}
 cudaError_t run_img(ImgConvArgs a, size_t smem, int nimg, cudaStream_t st) {
-  if (a.dgrad) return a.N == 32 ? launch_img<32, true>(a, smem, nimg, st) : launch_img<64, true>(a, smem, nimg, st);
-  return a.N == 32 ? launch_img<32, false>(a, smem, nimg, st) : launch_img<64, false>(a, smem, nimg, st);
+  if (a.dgrad) return a.N == 32 ? run_img_nt<32, true>(a, smem, nimg, st) : run_img_nt<64, true>(a, smem, nimg, st);
+  return a.N == 32 ? run_img_nt<32, false>(a, smem, nimg, st) : run_img_nt<64, false>(a, smem, nimg, st);
+}
+
+// ------------------------------------------------------------ weight gradient --
+// dW[co][(r,s,c)] = sum_n sum_q img_x[q + r*Wp + s][c] * dy_pad[q][co]  (stride 1, C = 32)
+// One CTA per sample n: the padded image (MN-major, k-line = padded pixel, 32
+// channels) and dy in padded-width numbering (k-line q = oh*Wp + ow, zero for
+// ow >= Wo: TMA out-of-bounds fill) are staged by TMA.  An M tile is four
+// 32-channel atoms = four taps whose image shifts form an arithmetic sequence
+// (start off, stride delta rows: the descriptor's atom stride LBO = delta*128 B,
+// probed by tools/desc_shift_mn.cu); the host groups the R*S taps into such
+// tiles.  A CTA takes spc consecutive samples (double-buffered TMA staging) and
+// accumulates all of them in TMEM; the epilogue writes the CTA's partial dW (and
+// db = sum dy, by SIMT); conv_wgrad_sum_kernel adds the partials in ascending
+// CTA order (deterministic: the partition depends on the shape only).
+constexpr int kMaxWTiles = 8;
+
+struct ImgWgradArgs {
+  CUtensorMap img_map;  // x NHWC {C, W, H, N}, box {32, Wp, Hrows_i, 1}, SWIZZLE_128B_ATOM_32B
+  CUtensorMap dy_map;   // dy NHWC {Co, Wo, Ho, N}, box {32, Wp, Hrows_d, 1}, SWIZZLE_128B_ATOM_32B
+  const float* dy;
+  float* part;          // [CTA][Co*Kg + Co]
+  int C, Co, R, S, pad, Wp, Ho, Wo;
+  int Hrows_i, Hrows_d, rows_i, rows_d, ksteps;
+  int nimg, spc;  // samples, samples per CTA (accumulated in TMEM)
+  int ntile;
+  int t_off[kMaxWTiles], t_delta[kMaxWTiles], t_tap[kMaxWTiles][4];
+};
+
+template <int NB>
+__global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __grid_constant__ ImgWgradArgs a) {
+  constexpr int NA = NB / 32;  // co atoms
+  constexpr int TCOLS = kMaxWTiles * NB <= 256 ? 256 : 512;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t dy_plane = a.rows_d * 128;
+  const uint32_t buf_bytes = a.rows_i * 128 + NA * dy_plane;  // one sample: image, then dy atoms
+  const uint32_t bars = base + 2 * buf_bytes;                // full[2], empty[2], done
+  const uint32_t done_bar = bars + 32, slot = done_bar + 8;
+  uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
+  __shared__ float red[128];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n0 = blockIdx.x * a.spc, n1 = min(a.nimg, n0 + a.spc), ns = n1 - n0;
+  const int Kg = a.R * a.S * a.C, per = a.Co * Kg + a.Co;
+
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bars + 8 * b, 1);        // TMA transaction barrier
+      mbar_init(bars + 16 + 8 * b, 1);   // tcgen05.commit: buffer free
+    }
+    mbar_init(done_bar, 1);
+    fence_barrier_init();
+    prefetch_tmap(&a.img_map);
+    prefetch_tmap(&a.dy_map);
+  }
+  if (warp == 4) tmem_alloc<TCOLS>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot_ptr;
+  pdl_entry();
+  const uint32_t tx = (uint32_t)(a.Hrows_i * a.Wp + NA * a.Hrows_d * a.Wp) * 128;
+  auto stage = [&](int k) {  // TMA staging of sample n0 + k into buffer k & 1
+    const int b = k & 1;
+    const uint32_t img = base + b * buf_bytes, dyb = img + a.rows_i * 128;
+    mbar_arrive_expect_tx(bars + 8 * b, tx);
+    tma_load_4d(img, &a.img_map, 0, -a.pad, -a.pad, n0 + k, bars + 8 * b);
+    for (int at = 0; at < NA; ++at) tma_load_4d(dyb + at * dy_plane, &a.dy_map, at * 32, 0, 0, n0 + k, bars + 8 * b);
+  };
+  if (warp == 4) {
+    if (lane == 0) {
+      // ---- MMA issue over the CTA's samples, accumulating in TMEM ----
+      constexpr uint32_t idesc = idesc_tf32(128, NB, 1, 1);
+      for (int k = 0; k < ns; ++k) {
+        const int b = k & 1;
+        mbar_wait(bars + 8 * b, (k >> 1) & 1);
+        tc_fence_after();
+        const uint32_t img = base + b * buf_bytes, dyb = img + a.rows_i * 128;
+        const uint64_t bd0 = umma_desc_mn_sw128_32b(dyb, dy_plane, 512);
+        const uint32_t b_lo0 = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
+        for (int g = 0; g < a.ntile; ++g) {
+          const uint64_t ad0 = umma_desc_mn_sw128_32b(img + a.t_off[g] * 128, a.t_delta[g] * 128, 512);
+          const uint32_t a_lo0 = (uint32_t)ad0, a_hi = (uint32_t)(ad0 >> 32);
+          for (int ks = 0; ks < a.ksteps; ++ks)
+            mma_tf32_lh(tmem + g * NB, a_lo0 + ks * 64, a_hi, b_lo0 + ks * 64, b_hi, idesc, (k | ks) ? 1u : 0u);
+        }
+        if (k + 2 < ns) mma_commit(bars + 16 + 8 * b);  // buffer b is restaged once these complete
+      }
+      mma_commit(done_bar);
+    }
+    __syncwarp();
+  } else {
+    if (tid == 0) {
+      // ---- TMA staging, double-buffered over the CTA's samples ----
+      stage(0);
+      if (ns > 1) stage(1);
+      for (int k = 2; k < ns; ++k) {
+        mbar_wait(bars + 16 + 8 * (k & 1), ((k - 2) >> 1) & 1);
+        stage(k);
+      }
+    }
+    // db partial = sum over the CTA's samples of dy (SIMT, fixed order), while the MMAs run
+    const int groups = 128 / a.Co;  // threads per channel (Co <= 128)
+    float sacc = 0.f;
+    if (tid < groups * a.Co) {
+      const int co = tid % a.Co, grp = tid / a.Co;
+      const float* dyn = a.dy + (size_t)n0 * a.Ho * a.Wo * a.Co;
+      for (int p = grp; p < ns * a.Ho * a.Wo; p += groups) sacc += __ldg(dyn + (size_t)p * a.Co + co);
+    }
+    red[tid] = sacc;
+    mbar_wait_sleep(done_bar, 0);
+    tc_fence_after();
+    // partial dW: TMEM lane = (atom = warp, channel = lane) of tile g, columns = co
+    float* out = a.part + (size_t)blockIdx.x * per;
+    for (int g = 0; g < a.ntile; ++g) {
+      const int tap = a.t_tap[g][warp];
+      const int kg = tap * a.C + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NB; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + g * NB + c0, v);
+        if (tap < 0) continue;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) out[(size_t)(c0 + j) * Kg + kg] = v[j];
+      }
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // red[] complete (epilogue warps only)
+    if (tid < a.Co) {
+      float t = 0.f;
+      for (int gi = 0; gi < groups; ++gi) t += red[gi * a.Co + tid];
+      out[(size_t)a.Co * Kg + tid] = t;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc<TCOLS>(tmem);
+  }
+}
+
+// dW / db = sum over the samples' partials in ascending n: block = 32 outputs x
+// 16 warps; warp w sums partials w, w+16, ...; warp 0 adds the 16 in order.
+__global__ void __launch_bounds__(512) conv_wgrad_sum_kernel(const float* __restrict__ part, int nparts, int per,
+                                                             int nw, float* __restrict__ dW, float* __restrict__ db) {
+  __shared__ float red[16][32];
+  pdl_entry();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  float v = 0.f;
+  if (i < per)
+    for (int k = w; k < nparts; k += 16) v += __ldg(part + (size_t)k * per + i);
+  red[w][lane] = v;
+  __syncthreads();
+  if (w != 0 || i >= per) return;
+  float t = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) t += red[k][lane];
+  if (i < nw)
+    dW[i] = t;
+  else if (db)
+    db[i - nw] = t;
+}
+
+// Tap grouping: per filter row r, runs of 4 consecutive s (stride 1 row); the
+// leftover columns s of all rows in runs of 4 (stride Wp rows); at most
+// kMaxWTiles tiles, unused atoms marked -1.
+bool plan_wgrad(const ConvShape& s, ImgWgradArgs* a, size_t* smem) {
+  if (!img_conv_enabled() || s.st != 1 || s.C != 32 || (s.Co != 32 && s.Co != 64)) return false;
+  ImgWgradArgs g{};
+  g.C = s.C, g.Co = s.Co, g.R = s.R, g.S = s.S, g.pad = s.pad;
+  g.Wp = s.W + 2 * s.pad, g.Ho = s.Ho, g.Wo = s.Wo;
+  g.ntile = 0;
+  auto add = [&](int off, int delta, const int* taps, int cnt) {
+    if (g.ntile >= kMaxWTiles) return false;
+    g.t_off[g.ntile] = off;
+    g.t_delta[g.ntile] = delta;
+    for (int k = 0; k < 4; ++k) g.t_tap[g.ntile][k] = k < cnt ? taps[k] : -1;
+    ++g.ntile;
+    return true;
+  };
+  const int full = s.S / 4;
+  for (int r = 0; r < s.R; ++r)
+    for (int b = 0; b < full; ++b) {
+      int taps[4];
+      for (int k = 0; k < 4; ++k) taps[k] = r * s.S + b * 4 + k;
+      if (!add(r * g.Wp + b * 4, 1, taps, 4)) return false;
+    }
+  for (int sc = full * 4; sc < s.S; ++sc)
+    for (int r0 = 0; r0 < s.R; r0 += 4) {
+      int taps[4], cnt = 0;
+      for (int k = 0; k < 4 && r0 + k < s.R; ++k) taps[cnt++] = (r0 + k) * s.S + sc;
+      if (!add(r0 * g.Wp + sc, g.Wp, taps, cnt)) return false;
+    }
+  const int K = g.Ho * g.Wp;
+  g.ksteps = (K + 7) / 8;
+  int need_rows = 0;
+  for (int t = 0; t < g.ntile; ++t) need_rows = std::max(need_rows, g.t_off[t] + 3 * g.t_delta[t] + g.ksteps * 8);
+  g.Hrows_i = (need_rows + g.Wp - 1) / g.Wp;
+  g.Hrows_d = (g.ksteps * 8 + g.Wp - 1) / g.Wp;
+  if (g.Hrows_i > 256 || g.Hrows_d > 256 || g.Wp > 256) return false;
+  g.rows_i = (g.Hrows_i * g.Wp + 7) / 8 * 8;
+  g.rows_d = (g.Hrows_d * g.Wp + 7) / 8 * 8;
+  if (g.ntile * s.Co > 512) return false;
+  // samples per CTA: enough MMAs per CTA to amortise the per-CTA partial
+  // (Co*Kg floats written and re-read by the reduction)
+  g.nimg = s.N;
+  // Samples per CTA (SG_WGRAD_SPC, default 1): accumulating several samples per
+  // CTA measured slower (CIFAR conv2: 26 -> 36 us at 2, 87 us at 3).  A sample's
+  // partial (Co*Kg floats, written and re-read by the reduction) must be
+  // amortised by its MMAs: below ~200 MMAs per sample the implicit GEMM wins
+  // (CIFAR conv3: 24 vs 20 us), so such shapes are declined.
+  static const int spc_env = getenv("SG_WGRAD_SPC") ? atoi(getenv("SG_WGRAD_SPC")) : 1;
+  g.spc = std::max(1, std::min(s.N, spc_env));
+  if (g.ntile * g.ksteps < 200) return false;
+  *smem = 1024 + 2 * ((size_t)g.rows_i * 128 + (size_t)(s.Co / 32) * g.rows_d * 128) + 64;
+  if (*smem > 227 * 1024) return false;
+  *a = g;
+  return true;
 }
 
 }  // namespace
+
+bool conv_img_wgrad_ok(const ConvShape& s) {
+  ImgWgradArgs a;
+  size_t smem;
+  return plan_wgrad(s, &a, &smem);
+}
+
+size_t conv_img_wgrad_ws_floats(const ConvShape& s) {
+  // partials after the 1024-float head the GEMM engine keeps its split-K counters in
+  ImgWgradArgs a;
+  size_t smem;
+  if (!plan_wgrad(s, &a, &smem)) return 0;
+  const size_t ctas = (s.N + a.spc - 1) / a.spc;
+  return 1024 + ctas * (size_t)(s.Co * s.R * s.S * s.C + s.Co);
+}
+
+cudaError_t conv_img_wgrad(const ConvShape& s, const float* x, const float* dy, float* dW, float* db, Workspace ws,
+                           cudaStream_t st) {
+  ImgWgradArgs a;
+  size_t smem;
+  if (!plan_wgrad(s, &a, &smem) || ws.floats < conv_img_wgrad_ws_floats(s)) return cudaErrorInvalidValue;
+  a.dy = dy;
+  a.part = ws.ptr + 1024;
+  const cuuint64_t xd[4] = {(cuuint64_t)s.C, (cuuint64_t)s.W, (cuuint64_t)s.H, (cuuint64_t)s.N};
+  const cuuint64_t xs[3] = {(cuuint64_t)s.C * 4, (cuuint64_t)s.W * s.C * 4, (cuuint64_t)s.H * s.W * s.C * 4};
+  const cuuint32_t xb[4] = {32, (cuuint32_t)a.Wp, (cuuint32_t)a.Hrows_i, 1};
+  const cuuint64_t dd[4] = {(cuuint64_t)s.Co, (cuuint64_t)s.Wo, (cuuint64_t)s.Ho, (cuuint64_t)s.N};
+  const cuuint64_t ds[3] = {(cuuint64_t)s.Co * 4, (cuuint64_t)s.Wo * s.Co * 4, (cuuint64_t)s.Ho * s.Wo * s.Co * 4};
+  const cuuint32_t db4[4] = {32, (cuuint32_t)a.Wp, (cuuint32_t)a.Hrows_d, 1};
+  if (!encode_tiled_f32(&a.img_map, x, 4, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+      !encode_tiled_f32(&a.dy_map, dy, 4, dd, ds, db4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    return cudaErrorInvalidValue;
+  auto k = s.Co == 32 ? conv_img_wgrad_kernel<32> : conv_img_wgrad_kernel<64>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int ctas = (s.N + a.spc - 1) / a.spc;
+  e = launch_k(k, ctas, kImgThreads, smem, st, a);
+  if (e != cudaSuccess) return e;
+  const int nw = s.Co * s.R * s.S * s.C, per = nw + s.Co;
+  return launch_k(conv_wgrad_sum_kernel, (per + 31) / 32, 512, 0, st, (const float*)a.part, ctas, per, nw, dW, db);
+}
 
 bool conv_img_fwd_ok(const ConvShape& s) {
   ImgConvArgs a;
@@ -335,6 +551,24 @@ bool conv_img_dgrad_ok(const ConvShape& s) {
   return plan_img(s, true, &a, &smem);
 }
 
+bool encode_maps(const ConvShape& s, ImgConvArgs* a) {
+  // source image NHWC {C, W, H, N}; box {32, Wp, Hrows, 1} from (cb*32, -pad, -pad, n)
+  const cuuint64_t idims[4] = {(cuuint64_t)a->C, (cuuint64_t)a->W, (cuuint64_t)a->H, (cuuint64_t)s.N};
+  const cuuint64_t istr[3] = {(cuuint64_t)a->C * 4, (cuuint64_t)a->W * a->C * 4, (cuuint64_t)a->H * a->W * a->C * 4};
+  const cuuint32_t ibox[4] = {32, (cuuint32_t)a->Wp, (cuuint32_t)a->Hrows, 1};
+  if (!encode_tiled_f32(&a->img_map, a->src, 4, idims, istr, ibox, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  // filter KRSC [Co][T][C]: view {c, co, t} with strides (T*C*4, C*4)
+  const int T = s.R * s.S;
+  const cuuint64_t wdims[3] = {(cuuint64_t)s.C, (cuuint64_t)s.Co, (cuuint64_t)T};
+  const cuuint64_t wstr[2] = {(cuuint64_t)T * s.C * 4, (cuuint64_t)s.C * 4};
+  if (!a->dgrad) {
+    const cuuint32_t wbox[3] = {32, (cuuint32_t)s.Co, (cuuint32_t)T};
+    return encode_tiled_f32(&a->w_map, a->wt, 3, wdims, wstr, wbox, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  const cuuint32_t wbox[3] = {32, 32, (cuuint32_t)T};
+  return encode_tiled_f32(&a->w_map, a->wt, 3, wdims, wstr, wbox, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+}
+
 cudaError_t conv_img_fwd(const ConvShape& s, const float* x, const float* W, const float* b, float* y, int relu,
                          cudaStream_t st) {
   ImgConvArgs a;
@@ -345,6 +579,7 @@ cudaError_t conv_img_fwd(const ConvShape& s, const float* x, const float* W, con
   a.bias = b;
   a.out = y;
   a.relu = relu;
+  if (!encode_maps(s, &a)) return cudaErrorInvalidValue;
   return run_img(a, smem, s.N, st);
 }
 
@@ -357,6 +592,7 @@ cudaError_t conv_img_dgrad(const ConvShape& s, const float* dy, const float* W, 
   a.bias = nullptr;
   a.out = dx;
   a.relu = 0;
+  if (!encode_maps(s, &a)) return cudaErrorInvalidValue;
   return run_img(a, smem, s.N, st);
 }
 

@@ -67,12 +67,16 @@ size_t gemm_ws_floats(int M, int N, int K);
 
 // Resident-image tcgen05 convolution (conv_img.cu): stride 1, C and Co
 // multiples of 32, padded image in shared memory.  conv_fwd / conv_dgrad use
-// it whenever the *_ok predicate holds (opt-in: SG_IMG_CONV=1).
+// it whenever the *_ok predicate holds (SG_IMG_CONV=0 disables it).
 bool conv_img_fwd_ok(const ConvShape& s);
 bool conv_img_dgrad_ok(const ConvShape& s);
 cudaError_t conv_img_fwd(const ConvShape& s, const float* x, const float* W, const float* b, float* y, int relu,
                          cudaStream_t st);
 cudaError_t conv_img_dgrad(const ConvShape& s, const float* dy, const float* W, float* dx, cudaStream_t st);
+bool conv_img_wgrad_ok(const ConvShape& s);
+size_t conv_img_wgrad_ws_floats(const ConvShape& s);  // per-sample partials
+cudaError_t conv_img_wgrad(const ConvShape& s, const float* x, const float* dy, float* dW, float* db, Workspace ws,
+                           cudaStream_t st);
 
 
 // ---- convolution (implicit GEMM, tcgen05 kind::tf32) ----

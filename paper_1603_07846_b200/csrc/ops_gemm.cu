@@ -267,7 +267,7 @@ bool aligned16p(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) ==
 CUtensorMap enc_tiled(const void* p, int rank, const cuuint64_t* dims, const cuuint64_t* strides_b,
                       const cuuint32_t* box, CUtensorMapSwizzle sw, bool* ok) {
   CUtensorMap m;
-  cuuint32_t es[3] = {1, 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};  // element strides, one per dimension (rank <= 5)
   CUresult r = g_enc_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(p), dims, strides_b, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -461,6 +461,15 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int nparts, 
 
 }  // namespace
 
+// Tiled fp32 tensor map for kernels outside this file (conv_img.cu).
+bool encode_tiled_f32(CUtensorMap* m, const void* p, int rank, const cuuint64_t* dims, const cuuint64_t* strides_b,
+                      const cuuint32_t* box, CUtensorMapSwizzle sw) {
+  bool ok = tma_on_impl();
+  if (!ok) return false;
+  *m = enc_tiled(p, rank, dims, strides_b, box, sw, &ok);
+  return ok;
+}
+
 size_t gemm_ws_floats(int M, int N, int K) {
   Plan p = plan_gemm(M, N, K, (size_t)1 << 62);
   // the weight-gradient GEMMs may add one ones-row (fused bias gradient)
@@ -556,6 +565,8 @@ cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* W, floa
 cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dW, float* db, Workspace ws,
                        cudaStream_t st) {
   const int Kg = s.R * s.S * s.C, Mtot = s.N * s.Ho * s.Wo;
+  if (conv_img_wgrad_ok(s) && ws.floats >= conv_img_wgrad_ws_floats(s) && aligned16p(x) && aligned16p(dy))
+    return conv_img_wgrad(s, x, dy, dW, db, ws, st);
   // D[kg][co] stored transposed into dW[co][kg]; row Kg (ones) = db
   EpiArgs e = epi_plain(dW, Kg, 1, nullptr, 0, 0, Kg);
   if (db) {

@@ -584,6 +584,7 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
       need(gemm_ws_floats(Kg, L.c, (int)(L.rows * L.h * L.w)));
       need(gemm_ws_floats((int)(L.rows * S.h * S.w), S.c, L.kernel * L.kernel * L.c));
       need(colsum_ws_floats((int)(L.rows * L.h * L.w), L.c));
+      need(conv_img_wgrad_ws_floats(conv_shape(L, S)));
     }
     if (L.kind == SG_INNER_PRODUCT) {
       need(gemm_ws_floats((int)L.rows, (int)L.nout, (int)L.kin));

@@ -113,6 +113,14 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* map, int c
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* map, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
 // NHWC im2col box: coordinates {c, w, h, n} of the first output pixel's window
 // origin, filter-tap offsets {s, r}.
 __device__ __forceinline__ void tma_load_im2col(uint32_t dst, const void* map, int c, int w, int h, int n, int s,

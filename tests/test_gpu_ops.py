@@ -47,6 +47,8 @@ CONV = [  # N, H, W, C, Co, R, stride, pad
     (8, 8, 8, 32, 64, 5, 1, 2),       # CIFAR conv3
     (3, 10, 7, 32, 32, 3, 1, 1),      # resident-image path, non-square, 3x3
     (2, 11, 11, 64, 32, 3, 1, 0),     # resident-image path, 2 K blocks, no padding
+    (2, 24, 24, 32, 32, 3, 1, 1),     # resident-image weight gradient: column tap groups only
+    (2, 16, 16, 32, 64, 5, 1, 2),     # resident-image weight gradient, Co = 64
     (2, 35, 35, 4, 64, 11, 4, 2),     # AlexNet conv1 geometry
     (2, 27, 27, 64, 192, 5, 1, 2),    # AlexNet conv2 (TMA wgrad, C = 64)
     (2, 13, 13, 192, 384, 3, 1, 1),   # AlexNet conv3
@@ -77,16 +79,16 @@ def test_conv(case):
     assert normwise(host(dx), rdx) < TF32_TOL
 
 
-def test_conv_resident_image_path():
-    """The opt-in resident-image convolution (SG_IMG_CONV=1, read once per
-    process) passes the same conv parity cases in a fresh process."""
+def test_conv_implicit_gemm_path():
+    """With the resident-image convolution disabled (SG_IMG_CONV=0, read once per
+    process) the implicit-GEMM path passes the same conv parity cases."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_ops.py", "-m", "gpu", "-q", "-x",
-                        "-k", "test_conv and not rejects and not resident", "-p", "no:cacheprovider"],
-                       cwd=root, env=dict(os.environ, SG_IMG_CONV="1"), capture_output=True, text=True, timeout=600)
+                        "-k", "test_conv and not rejects and not implicit", "-p", "no:cacheprovider"],
+                       cwd=root, env=dict(os.environ, SG_IMG_CONV="0"), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 

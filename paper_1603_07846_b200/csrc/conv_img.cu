@@ -279,6 +279,146 @@ cudaError_t run_img(ImgConvArgs a, size_t smem, int nimg, cudaStream_t st) {
   return a.N == 32 ? run_img_nt<32, false>(a, smem, nimg, st) : run_img_nt<64, false>(a, smem, nimg, st);
 }
 
+// --------------------------------------------- 4-channel first layer forward --
+// Same idea for C = 4 (CIFAR conv1): the image is staged with 8 channels per
+// pixel (channels 4..7 = TMA out-of-bounds zeros) as K-major SWIZZLE_32B rows of
+// 32 B, so a filter tap is ONE K = 8 MMA per 128-row tile on a row-shifted
+// descriptor (32-byte rows may start anywhere: tools/desc_shift32.cu).  The
+// filter bank is staged the same way ([t][co][8 channels]).
+constexpr uint64_t kLayoutSW32 = 6;
+
+__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
+  const uint64_t d = umma_desc_sw128(saddr, 16, 256);  // SBO = 8 rows x 32 B
+  return (d & ~((uint64_t)7 << 61)) | (kLayoutSW32 << 61);
+}
+
+struct Img8Args {
+  CUtensorMap img_map;  // x {4, W, H, N}, box {8, Wp, Hrows, 1}, SWIZZLE_32B
+  CUtensorMap w_map;    // W {4, Co, T} (strides T*16, 16), box {8, Co, T}, SWIZZLE_32B
+  const float* bias;
+  float* out;
+  int pad, R, S, Wp, Ho, Wo, Hrows, img_rows, ntiles, relu;
+};
+
+template <int NB>
+__global__ void __launch_bounds__(kImgThreads, 1) conv_img8_fwd_kernel(const __grid_constant__ Img8Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t img = base;
+  const uint32_t wbase = img + ((a.img_rows * 32 + 1023) & ~1023);
+  const int T = a.R * a.S;
+  const uint32_t wbytes = (uint32_t)T * NB * 32;
+  const uint32_t bar = wbase + ((wbytes + 1023) & ~1023u), done_bar = bar + 8, slot = done_bar + 8;
+  uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = blockIdx.x;
+
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(done_bar, 1);
+    fence_barrier_init();
+    prefetch_tmap(&a.img_map);
+    prefetch_tmap(&a.w_map);
+  }
+  if (warp == 4) tmem_alloc<512>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot_ptr;
+  pdl_entry();
+  if (tid == 0) {
+    IMG_TRACE(5, 0);
+    mbar_arrive_expect_tx(bar, (uint32_t)a.Hrows * a.Wp * 32 + wbytes);
+    tma_load_4d(img, &a.img_map, 0, -a.pad, -a.pad, n, bar);
+    tma_load_3d(wbase, &a.w_map, 0, 0, 0, bar);
+  }
+  if (warp == 4) {
+    constexpr uint32_t idesc = idesc_tf32(128, NB, 0, 0);
+    const uint64_t ad0 = umma_desc_sw32(img), bd0 = umma_desc_sw32(wbase);
+    const uint32_t a_lo0 = (uint32_t)ad0, a_hi = (uint32_t)(ad0 >> 32);
+    const uint32_t b_lo0 = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
+    mbar_wait(bar, 0);
+    tc_fence_after();
+    if (lane == 0) {
+      IMG_TRACE(3, 0);
+      int r = 0, sc = 0;
+      for (int t = 0; t < T; ++t) {
+        const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc) * 2;  // 32-B rows
+        const uint32_t b_t = b_lo0 + (uint32_t)t * NB * 2;
+        for (int i = 0; i < a.ntiles; ++i)
+          mma_tf32_lh(tmem + i * NB, a_t + i * 256, a_hi, b_t, b_hi, idesc, t ? 1u : 0u);
+        if (++sc == a.S) {
+          sc = 0;
+          ++r;
+        }
+      }
+      IMG_TRACE(2, 0);
+      mma_commit(done_bar);
+    }
+    __syncwarp();
+  } else {
+    mbar_wait_sleep(done_bar, 0);
+    if (tid == 0) IMG_TRACE(4, 0);
+    tc_fence_after();
+    float* outn = a.out + (size_t)n * a.Ho * a.Wo * NB;
+#pragma unroll 1
+    for (int i = 0; i < a.ntiles; ++i) {
+      const int q = i * 128 + warp * 32 + lane;
+      const int oh = q / a.Wp, ow = q - oh * a.Wp;
+      const bool valid = oh < a.Ho && ow < a.Wo;
+      float* dst = outn + ((size_t)oh * a.Wo + ow) * NB;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NB; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + i * NB + c0, v);
+        if (!valid) continue;
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+          float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          if (a.bias) {
+            o.x += __ldg(a.bias + c0 + j);
+            o.y += __ldg(a.bias + c0 + j + 1);
+            o.z += __ldg(a.bias + c0 + j + 2);
+            o.w += __ldg(a.bias + c0 + j + 3);
+          }
+          if (a.relu) {
+            o.x = fmaxf(o.x, 0.f);
+            o.y = fmaxf(o.y, 0.f);
+            o.z = fmaxf(o.z, 0.f);
+            o.w = fmaxf(o.w, 0.f);
+          }
+          *reinterpret_cast<float4*>(dst + c0 + j) = o;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) IMG_TRACE(0, 0);
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+bool plan_img8(const ConvShape& s, Img8Args* a, size_t* smem) {
+  if (!img_conv_enabled() || s.C != 4 || s.st != 1 || (s.Co != 32 && s.Co != 64)) return false;
+  Img8Args g{};
+  g.pad = s.pad, g.R = s.R, g.S = s.S;
+  g.Wp = s.W + 2 * s.pad, g.Ho = s.Ho, g.Wo = s.Wo;
+  g.ntiles = (g.Ho * g.Wp + 127) / 128;
+  if (g.ntiles * s.Co > 512) return false;
+  const int need = g.ntiles * 128 + (s.R - 1) * g.Wp + s.S - 1;
+  g.Hrows = (need + g.Wp - 1) / g.Wp;
+  g.img_rows = g.Hrows * g.Wp;
+  if (g.Hrows > 256 || g.Wp > 256 || s.R * s.S > 256) return false;
+  *smem = 1024 + (((size_t)g.img_rows * 32 + 1023) & ~(size_t)1023) +
+          (((size_t)s.R * s.S * s.Co * 32 + 1023) & ~(size_t)1023) + 64;
+  if (*smem > 227 * 1024) return false;
+  *a = g;
+  return true;
+}
+
 // ------------------------------------------------------------ weight gradient --
 // dW[co][(r,s,c)] = sum_n sum_q img_x[q + r*Wp + s][c] * dy_pad[q][co]  (stride 1, C = 32)
 // One CTA per sample n: the padded image (MN-major, k-line = padded pixel, 32
@@ -542,8 +682,9 @@ cudaError_t conv_img_wgrad(const ConvShape& s, const float* x, const float* dy, 
 
 bool conv_img_fwd_ok(const ConvShape& s) {
   ImgConvArgs a;
+  Img8Args a8;
   size_t smem;
-  return plan_img(s, false, &a, &smem);
+  return plan_img(s, false, &a, &smem) || plan_img8(s, &a8, &smem);
 }
 bool conv_img_dgrad_ok(const ConvShape& s) {
   ImgConvArgs a;
@@ -573,6 +714,26 @@ cudaError_t conv_img_fwd(const ConvShape& s, const float* x, const float* W, con
                          cudaStream_t st) {
   ImgConvArgs a;
   size_t smem;
+  Img8Args a8;
+  if (plan_img8(s, &a8, &smem)) {
+    a8.bias = b;
+    a8.out = y;
+    a8.relu = relu;
+    const int T = s.R * s.S;
+    const cuuint64_t xd[4] = {4, (cuuint64_t)s.W, (cuuint64_t)s.H, (cuuint64_t)s.N};
+    const cuuint64_t xs[3] = {16, (cuuint64_t)s.W * 16, (cuuint64_t)s.H * s.W * 16};
+    const cuuint32_t xb[4] = {8, (cuuint32_t)a8.Wp, (cuuint32_t)a8.Hrows, 1};
+    const cuuint64_t wd[3] = {4, (cuuint64_t)s.Co, (cuuint64_t)T};
+    const cuuint64_t ws[2] = {(cuuint64_t)T * 16, 16};
+    const cuuint32_t wb[3] = {8, (cuuint32_t)s.Co, (cuuint32_t)T};
+    if (!encode_tiled_f32(&a8.img_map, x, 4, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_32B) ||
+        !encode_tiled_f32(&a8.w_map, W, 3, wd, ws, wb, CU_TENSOR_MAP_SWIZZLE_32B))
+      return cudaErrorInvalidValue;
+    auto k = s.Co == 32 ? conv_img8_fwd_kernel<32> : conv_img8_fwd_kernel<64>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return launch_k(k, s.N, kImgThreads, smem, st, a8);
+  }
   if (!plan_img(s, false, &a, &smem)) return cudaErrorInvalidValue;
   a.src = x;
   a.wt = W;

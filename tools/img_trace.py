@@ -32,6 +32,6 @@ buf = (C.c_longlong * (6 * 64))()
 assert L.lib.sg_debug_img_trace(buf) == 0
 t = np.frombuffer(buf, dtype=np.int64).reshape(6, 64).astype(np.float64)
 t0 = t[5, 0]
-for r, name in enumerate(["tap produced", "tap ready", "tap issued", "image ready", "done"]):
+for r, name in enumerate(["end", "tap ready", "mma issued", "image ready", "done"]):
     v = t[r][t[r] > 0] - t0
     print(f"{name:13s} " + " ".join(f"{x:6.0f}" for x in v[:26]))

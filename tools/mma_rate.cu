@@ -10,7 +10,7 @@
 using namespace sg;
 
 template <int N>
-__global__ void mma_rate(long long* out, int iters, int mode, int fill) {
+__global__ void mma_rate(long long* out, int iters, int mode, int fill, int nowarm) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar, bar2;
@@ -38,8 +38,8 @@ __global__ void mma_rate(long long* out, int iters, int mode, int fill) {
     const uint64_t ad = umma_desc_sw128(base, 16, 1024);
     const uint64_t bd = umma_desc_sw128(base + 65536, 16, 1024);  // 25 taps x 4 KB fit below 200 KB
     constexpr uint32_t idesc = idesc_tf32(128, N, 0, 0);
-    // warm-up
-    for (int i = 0; i < 8; ++i) mma_tf32(tmem, ad, bd, idesc, 1);
+    // warm-up (cfg 1 skips it)
+    if (!nowarm) for (int i = 0; i < 8; ++i) mma_tf32(tmem, ad, bd, idesc, 1);
     mma_commit(smem_u32(&bar));
     mbar_wait(smem_u32(&bar), 0);
     long long t0 = clock64();
@@ -111,12 +111,13 @@ void run(long long* d) {
   cudaFuncSetAttribute(mma_rate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   for (int mode = 7; mode < 8; ++mode)
   for (int cfg = 0; cfg < 3; ++cfg) {
-    const int fill = cfg == 1 ? 2 : 1;
-    const int thr = cfg == 0 ? 128 : 192, sm = cfg >= 1 ? 200 * 1024 : 100 * 1024;
-    mma_rate<N><<<1, thr, sm>>>(d, iters, mode, fill);
+    const int fill = 2;
+    const int thr = 192, sm = 200 * 1024;
+    const int it = cfg == 2 ? iters : 300;  // cfg 0/1: one conv pass of 300 MMAs (1: no warm-up)
+    mma_rate<N><<<1, thr, sm>>>(d, it, mode, fill, cfg == 1);
     long long h = 0;
     cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-    const double cyc = (double)h / iters;
+    const double cyc = (double)h / (cfg == 2 ? iters : 300);
     printf("cfg=%d N=%3d mode %d: %6.1f cycles per 128x%dx8 MMA  -> %7.0f MAC/clk/SM\n", cfg, N, mode, cyc, N, 128.0 * N * 8 / cyc);
   }
 }

@@ -33,7 +33,8 @@ def to_bytes(v, unit):
 
 
 def main(tag, cfg, rep, launches, bench, op_of_kernel):
-    out = [f"# Round 1 profile evidence: {cfg} ({tag})", ""]
+    out = [f"# Round 1 profile evidence: {cfg} ({tag})", "",
+           "Produced by tools/profile_round.sh on a B200 and tools/write_profiles.py here.", ""]
     b = json.loads(open(bench).read().strip().splitlines()[-1])
     json.dump(b, open(os.path.join(ROOT, "profiles", f"r01_{cfg}_bench.json"), "w"), indent=1)
     out += [f"bench: {b['value']:.0f} {b['unit']}, {b['ms_per_step'] * 1e3:.1f} us/step, roofline {b['roofline']['kernel']} "
@@ -75,5 +76,7 @@ def main(tag, cfg, rep, launches, bench, op_of_kernel):
 
 
 if __name__ == "__main__":
-    main("r01e", "cifar10", "gpurun_out/r01e_full.ncu-rep", "gpurun_out/r01e_launches.csv", "gpurun_out/r01e_bench.json",
-         {"LdConvWgradA": "conv2.wgrad", "LdConvWgradSmemA": "conv1.wgrad"})
+    # usage: write_profiles.py TAG CONFIG  'kernel-fragment=op,...'
+    tag, cfg = sys.argv[1], sys.argv[2]
+    ops = dict(kv.split("=") for kv in sys.argv[3].split(",")) if len(sys.argv) > 3 else {}
+    main(tag, cfg, f"gpurun_out/{tag}_full.ncu-rep", f"gpurun_out/{tag}_launches.csv", f"gpurun_out/{tag}_bench.json", ops)

@@ -65,6 +65,7 @@ struct ImgConvArgs {
   int layer_c, layer_co;  // the layer's C / Co (weight tensor strides)
   int ntiles, img_rows, relu, dgrad;
   int Hrows;  // padded image rows staged (img_rows = Hrows * Wp rounded up to 8)
+  int wsplit;  // filter bank staged one K block at a time
 };
 
 __device__ __forceinline__ uint32_t ksw(int row, int chunk) {  // K-major SW128 offset of a 16-B chunk
@@ -78,7 +79,7 @@ __device__ __forceinline__ uint32_t ksw(int row, int chunk) {  // K-major SW128 
 //   dgrad:   [KB][NA][T][32][128 B]  (MN-major BASE32B, k-line co_in of tap t,
 //            K block kb of the layer's Co, atom a of the layer's C; taps in the
 //            layer's order, the flip is applied when the MMA picks the tap).
-template <int NB, bool DGRAD, int NT, int CB>
+template <int NB, bool DGRAD, int NT, int CB, bool WSPLIT>
 __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_constant__ ImgConvArgs a) {
   constexpr int TCOLS = NT * NB <= 32 ? 32 : NT * NB <= 64 ? 64 : NT * NB <= 128 ? 128 : NT * NB <= 256 ? 256 : 512;
   constexpr int NA = NB / 32;  // dgrad: MN atoms of the output channels
@@ -88,8 +89,9 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
   const uint32_t img_plane = a.img_rows * 128;
   const uint32_t wbase = img + CB * img_plane;
   const int T = a.R * a.S;
-  const uint32_t wbytes = (uint32_t)CB * T * NB * 128;
-  const uint32_t bar = wbase + wbytes, done_bar = bar + 8, slot = done_bar + 8;
+  // WSPLIT: one K block of the filter bank resident at a time (restaged per block)
+  const uint32_t wblk = (uint32_t)T * NB * 128, wbytes = (WSPLIT ? 1 : CB) * wblk;
+  const uint32_t bar = wbase + wbytes, done_bar = bar + 8, wbar = done_bar + 8, wfree = wbar + 8, slot = wfree + 8;
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = blockIdx.x;
@@ -97,6 +99,8 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
   if (tid == 0) {
     mbar_init(bar, 1);
     mbar_init(done_bar, 1);
+    mbar_init(wbar, 1);
+    mbar_init(wfree, 1);
     fence_barrier_init();
     prefetch_tmap(&a.img_map);
     prefetch_tmap(&a.w_map);
@@ -114,11 +118,21 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
     mbar_arrive_expect_tx(bar, CB * img_tx + wbytes);
     for (int cb = 0; cb < CB; ++cb)
       tma_load_4d(img + cb * img_plane, &a.img_map, cb * 32, -a.pad, -a.pad, n, bar);
-    if (!DGRAD) {
-      for (int cb = 0; cb < CB; ++cb) tma_load_3d(wbase + cb * T * NB * 128, &a.w_map, cb * 32, 0, 0, bar);
+    auto load_w = [&](int kb, uint32_t dst, uint32_t b) {  // K block kb of the filter bank
+      if (!DGRAD)
+        tma_load_3d(dst, &a.w_map, kb * 32, 0, 0, b);
+      else
+        for (int at = 0; at < NA; ++at) tma_load_3d(dst + at * T * 4096, &a.w_map, at * 32, kb * 32, 0, b);
+    };
+    if (!WSPLIT) {
+      for (int kb = 0; kb < CB; ++kb) load_w(kb, wbase + kb * wblk, bar);
     } else {
-      for (int kb = 0; kb < CB; ++kb)
-        for (int at = 0; at < NA; ++at) tma_load_3d(wbase + (kb * NA + at) * T * 4096, &a.w_map, at * 32, kb * 32, 0, bar);
+      load_w(0, wbase, bar);
+      for (int kb = 1; kb < CB; ++kb) {  // restage once the MMAs of block kb-1 are done
+        mbar_wait(wfree, (kb - 1) & 1);
+        mbar_arrive_expect_tx(wbar, wblk);
+        load_w(kb, wbase, wbar);
+      }
     }
   }
   if (warp == 4) {
@@ -133,7 +147,34 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
     mbar_wait(bar, 0);
     if (lane == 0) IMG_TRACE(3, 0);
     tc_fence_after();
-    if (lane == 0) {
+    if (WSPLIT) {
+      for (int kb = 0; kb < CB; ++kb) {
+        if (kb > 0) {
+          mbar_wait(wbar, (kb - 1) & 1);
+          tc_fence_after();
+        }
+        if (lane == 0) {
+          int r = 0, sc = 0;
+          for (int t = 0; t < T; ++t) {
+            const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc) * 8 + kb * plane16;
+            const uint32_t b_c = DGRAD ? b_lo0 + ((uint32_t)(T - 1 - t) * 4096 >> 4) : b_lo0 + ((uint32_t)t * NB * 128 >> 4);
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_tf32_lh(tmem + i * NB, a_t + i * 1024 + kk * 2, a_hi, b_c + kk * (DGRAD ? 64 : 2), b_hi, idesc,
+                            (t | kb | kk) ? 1u : 0u);
+            if (++sc == a.S) {
+              sc = 0;
+              ++r;
+            }
+          }
+          mma_commit(kb + 1 < CB ? wfree : done_bar);
+        }
+        __syncwarp();
+      }
+    }
+    if (!WSPLIT && lane == 0) {
       int r = 0, sc = 0;
       for (int t = 0; t < T; ++t) {
         const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc) * 8;
@@ -244,6 +285,11 @@ bool plan_img(const ConvShape& s, bool dgrad, ImgConvArgs* a, size_t* smem) {
   g.img_rows = (g.Hrows * g.Wp + 7) / 8 * 8;
   const size_t img_bytes = CB * g.img_rows * 128, w_bytes = CB * T * g.N * 128;
   *smem = 1024 + img_bytes + w_bytes + 64;
+  g.wsplit = 0;
+  if (*smem > 227 * 1024 && CB > 1) {  // one K block of the filter bank at a time
+    g.wsplit = 1;
+    *smem = 1024 + img_bytes + w_bytes / CB + 64;
+  }
   if (*smem > 227 * 1024) return false;
   *a = g;
   return true;
@@ -251,12 +297,13 @@ bool plan_img(const ConvShape& s, bool dgrad, ImgConvArgs* a, size_t* smem) {
 
 template <int NB, bool DG, int NT, int CB>
 cudaError_t launch_img(const ImgConvArgs& a, size_t smem, int nimg, cudaStream_t st) {
-  auto k = conv_img_kernel<NB, DG, NT, CB>;
-  static size_t set = 0;
-  if (smem > set) {
+  const bool split = CB > 1 && a.wsplit;
+  auto k = split ? conv_img_kernel<NB, DG, NT, CB, true> : conv_img_kernel<NB, DG, NT, CB, false>;
+  static size_t set[2] = {0, 0};  // per kernel variant
+  if (smem > set[split]) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    set = smem;
+    set[split] = smem;
   }
   return launch_k(k, nimg, kImgThreads, smem, st, a);
 }

@@ -113,10 +113,16 @@ cudaError_t relu_fwd2d(const float* x, float* y, int rows, int cols, long long l
 struct PoolShape {
   int N, H, W, C, k, s, p, Ho, Wo;
 };
-cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* arg, cudaStream_t st);
-cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg, float* dx, cudaStream_t st);
-cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st);
-cudaError_t avgpool_bwd(const PoolShape& s, const float* dy, float* dx, cudaStream_t st);
+// Optional ReLU fusion (runtime layer fusion, bit-identical to the separate ReLU
+// kernels): forward `relu_out` = max(y, 0) besides y; backward `dx_relu` =
+// dx * [relu_y > 0] besides dx (the gradient through the ReLU feeding this layer).
+cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* arg, cudaStream_t st,
+                        float* relu_out = nullptr);
+cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg, float* dx, cudaStream_t st,
+                        const float* relu_y = nullptr, float* dx_relu = nullptr);
+cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st, float* relu_out = nullptr);
+cudaError_t avgpool_bwd(const PoolShape& s, const float* dy, float* dx, cudaStream_t st, const float* relu_y = nullptr,
+                        float* dx_relu = nullptr);
 // argmax window offset -> int32 flat h*W+w in the input plane (ABI export format)
 cudaError_t pool_argmax_expand(const PoolShape& s, const uint8_t* arg, int32_t* out, cudaStream_t st);
 
@@ -127,7 +133,7 @@ struct LrnShape {
 };
 cudaError_t lrn_fwd(const LrnShape& s, const float* x, float* y, float* scale, cudaStream_t st);
 cudaError_t lrn_bwd(const LrnShape& s, const float* x, const float* y, const float* scale, const float* dy, float* dx,
-                    cudaStream_t st);
+                    cudaStream_t st, const float* relu_y = nullptr, float* dx_relu = nullptr);
 
 // Softmax cross-entropy over rows of a (blocked) logits view; per-row loss and
 // dz = (softmax - onehot) / n_loc written with the same blocking. Labels out of

@@ -85,6 +85,14 @@ cudaError_t launch_map2(const float* a, const float* b, float* y, long long n, F
   return launch_k(map2_kernel<F>, blocks_for(n / 4 + 1, 256), 256, 0, st, a, b, y, n, f);
 }
 
+// Optional ReLU fusion helpers (bit-identical to ReluF / ReluB).
+__device__ __forceinline__ float4 relu4(float4 v) {
+  return make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+}
+__device__ __forceinline__ float4 mask4(float4 d, float4 y) {
+  return make_float4(y.x > 0.f ? d.x : 0.f, y.y > 0.f ? d.y : 0.f, y.z > 0.f ? d.z : 0.f, y.w > 0.f ? d.w : 0.f);
+}
+
 // ---------------------------------------------------------------- pooling --
 // Index math is 32-bit with multiply-high division by the shape constants
 // (element counts < 2^31 are checked by the launchers).
@@ -101,7 +109,7 @@ PoolK pool_k(const PoolShape& s) {
 // the argmax is stored as the uint8 offset (h - h0)*k + (w - w0); first maximum
 // in (h, w) scan order (strict >), reading A5.
 __global__ void maxpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* __restrict__ y,
-                                   uint8_t* __restrict__ arg) {
+                                   uint8_t* __restrict__ arg, float* __restrict__ relu_out) {
   pdl_entry();
   const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
@@ -124,8 +132,10 @@ __global__ void maxpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* 
         if (v.z > m[2]) { m[2] = v.z; a[2] = off; }
         if (v.w > m[3]) { m[3] = v.w; a[3] = off; }
       }
-    *reinterpret_cast<float4*>(y + (size_t)i * 4) = make_float4(m[0], m[1], m[2], m[3]);
+    const float4 o = make_float4(m[0], m[1], m[2], m[3]);
+    *reinterpret_cast<float4*>(y + (size_t)i * 4) = o;
     *reinterpret_cast<uchar4*>(arg + (size_t)i * 4) = make_uchar4(a[0], a[1], a[2], a[3]);
+    if (relu_out) *reinterpret_cast<float4*>(relu_out + (size_t)i * 4) = relu4(o);
   }
 }
 
@@ -138,7 +148,8 @@ __device__ __forceinline__ void pool_windows(int hp, int k, int Ho, const FastDi
 // Gather form of the backward: thread per input (n, h, w, 4 channels) sums dy
 // of every window whose argmax is this element, windows in ascending (oh, ow).
 __global__ void maxpool_bwd_kernel(PoolK P, const float* __restrict__ dy, const uint8_t* __restrict__ arg,
-                                   float* __restrict__ dx) {
+                                   float* __restrict__ dx, const float* __restrict__ relu_y,
+                                   float* __restrict__ dx_relu) {
   pdl_entry();
   const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
@@ -165,10 +176,14 @@ __global__ void maxpool_bwd_kernel(PoolK P, const float* __restrict__ dy, const 
         if (a.w == off) acc.w += g.w;
       }
     *reinterpret_cast<float4*>(dx + (size_t)i * 4) = acc;
+    if (dx_relu)
+      *reinterpret_cast<float4*>(dx_relu + (size_t)i * 4) =
+          mask4(acc, __ldg(reinterpret_cast<const float4*>(relu_y) + i));
   }
 }
 
-__global__ void avgpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* __restrict__ y) {
+__global__ void avgpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* __restrict__ y,
+                                   float* __restrict__ relu_out) {
   pdl_entry();
   const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
@@ -188,11 +203,14 @@ __global__ void avgpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* 
         const float4 v = __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C));
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
-    *reinterpret_cast<float4*>(y + (size_t)i * 4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    const float4 o = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    *reinterpret_cast<float4*>(y + (size_t)i * 4) = o;
+    if (relu_out) *reinterpret_cast<float4*>(relu_out + (size_t)i * 4) = relu4(o);
   }
 }
 
-__global__ void avgpool_bwd_kernel(PoolK P, const float* __restrict__ dy, float* __restrict__ dx) {
+__global__ void avgpool_bwd_kernel(PoolK P, const float* __restrict__ dy, float* __restrict__ dx,
+                                   const float* __restrict__ relu_y, float* __restrict__ dx_relu) {
   pdl_entry();
   const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
@@ -219,6 +237,9 @@ __global__ void avgpool_bwd_kernel(PoolK P, const float* __restrict__ dy, float*
       }
     }
     *reinterpret_cast<float4*>(dx + (size_t)i * 4) = acc;
+    if (dx_relu)
+      *reinterpret_cast<float4*>(dx_relu + (size_t)i * 4) =
+          mask4(acc, __ldg(reinterpret_cast<const float4*>(relu_y) + i));
   }
 }
 
@@ -287,7 +308,8 @@ __global__ void lrn_fwd_kernel(LrnK K, const float* __restrict__ x, float* __res
 }
 
 __global__ void lrn_bwd_kernel(LrnK K, const float* __restrict__ x, const float* __restrict__ y,
-                               const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ dx) {
+                               const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ dx,
+                               const float* __restrict__ relu_y, float* __restrict__ dx_relu) {
   pdl_entry();
   const LrnShape& s = K.s;
   const int half = s.n / 2;
@@ -312,7 +334,11 @@ __global__ void lrn_bwd_kernel(LrnK K, const float* __restrict__ x, const float*
       for (int d = -half; d <= half; ++d) acc += e[4 + j + d];
       o[j] = gs[j] * pow_neg(ss[j], s.beta) - coef * xs[j] * acc;
     }
-    if (in) reinterpret_cast<float4*>(dx)[i] = make_float4(o[0], o[1], o[2], o[3]);
+    if (in) {
+      const float4 d = make_float4(o[0], o[1], o[2], o[3]);
+      reinterpret_cast<float4*>(dx)[i] = d;
+      if (dx_relu) reinterpret_cast<float4*>(dx_relu)[i] = mask4(d, __ldg(reinterpret_cast<const float4*>(relu_y) + i));
+    }
   }
 }
 
@@ -337,7 +363,8 @@ __global__ void lrn_fwd_generic_kernel(LrnShape s, const float* __restrict__ x, 
 
 __global__ void lrn_bwd_generic_kernel(LrnShape s, const float* __restrict__ x, const float* __restrict__ y,
                                        const float* __restrict__ scale, const float* __restrict__ dy,
-                                       float* __restrict__ dx) {
+                                       float* __restrict__ dx, const float* __restrict__ relu_y,
+                                       float* __restrict__ dx_relu) {
   pdl_entry();
   long long total = s.pixels * s.C;
   const int half = s.n / 2;
@@ -348,7 +375,9 @@ __global__ void lrn_bwd_generic_kernel(LrnShape s, const float* __restrict__ x, 
     int lo = max(c - half, 0), hi = min(c + half, s.C - 1);
     float acc = 0.f;
     for (int cc = lo; cc <= hi; ++cc) acc += dy[base + cc] * y[base + cc] / scale[base + cc];
-    dx[i] = dy[i] * pow_neg(scale[i], s.beta) - coef * x[i] * acc;
+    const float d = dy[i] * pow_neg(scale[i], s.beta) - coef * x[i] * acc;
+    dx[i] = d;
+    if (dx_relu) dx_relu[i] = relu_y[i] > 0.f ? d : 0.f;
   }
 }
 
@@ -518,26 +547,28 @@ cudaError_t relu_fwd2d(const float* x, float* y, int rows, int cols, long long l
 
 static bool fits32(long long n) { return n < (1LL << 31); }
 
-cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* arg, cudaStream_t st) {
+cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* arg, cudaStream_t st, float* relu_out) {
   const long long n = (long long)s.N * s.Ho * s.Wo * s.C / 4;
   if (s.C % 4 || s.k * s.k > 256 || !fits32(n * 4) || !fits32((long long)s.N * s.H * s.W * s.C))
     return cudaErrorInvalidValue;
-  return launch_k(maxpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y, arg);
+  return launch_k(maxpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y, arg, relu_out);
 }
-cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg, float* dx, cudaStream_t st) {
+cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg, float* dx, cudaStream_t st,
+                        const float* relu_y, float* dx_relu) {
   const long long n = (long long)s.N * s.H * s.W * s.C / 4;
   if (s.C % 4 || !fits32(n * 4)) return cudaErrorInvalidValue;
-  return launch_k(maxpool_bwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), dy, arg, dx);
+  return launch_k(maxpool_bwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), dy, arg, dx, relu_y, dx_relu);
 }
-cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st) {
+cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st, float* relu_out) {
   const long long n = (long long)s.N * s.Ho * s.Wo * s.C / 4;
   if (s.C % 4 || !fits32(n * 4) || !fits32((long long)s.N * s.H * s.W * s.C)) return cudaErrorInvalidValue;
-  return launch_k(avgpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y);
+  return launch_k(avgpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y, relu_out);
 }
-cudaError_t avgpool_bwd(const PoolShape& s, const float* dy, float* dx, cudaStream_t st) {
+cudaError_t avgpool_bwd(const PoolShape& s, const float* dy, float* dx, cudaStream_t st, const float* relu_y,
+                        float* dx_relu) {
   const long long n = (long long)s.N * s.H * s.W * s.C / 4;
   if (s.C % 4 || !fits32(n * 4)) return cudaErrorInvalidValue;
-  return launch_k(avgpool_bwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), dy, dx);
+  return launch_k(avgpool_bwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), dy, dx, relu_y, dx_relu);
 }
 cudaError_t pool_argmax_expand(const PoolShape& s, const uint8_t* arg, int32_t* out, cudaStream_t st) {
   return launch_k(argmax_expand_kernel, blocks_for((long long)s.N * s.Ho * s.Wo * s.C, 256), 256, 0, st, s, arg, out);
@@ -562,11 +593,12 @@ cudaError_t lrn_fwd(const LrnShape& s, const float* x, float* y, float* scale, c
   return launch_k(lrn_fwd_generic_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale);
 }
 cudaError_t lrn_bwd(const LrnShape& s, const float* x, const float* y, const float* scale, const float* dy, float* dx,
-                    cudaStream_t st) {
+                    cudaStream_t st, const float* relu_y, float* dx_relu) {
   LrnK k;
-  if (lrn_fast(s, {x, y, scale, dy, dx}, &k))
-    return launch_k(lrn_bwd_kernel, blocks_for(k.total, 256), 256, 0, st, k, x, y, scale, dy, dx);
-  return launch_k(lrn_bwd_generic_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale, dy, dx);
+  if (lrn_fast(s, {x, y, scale, dy, dx, dx_relu ? relu_y : x, dx_relu ? dx_relu : dx}, &k))
+    return launch_k(lrn_bwd_kernel, blocks_for(k.total, 256), 256, 0, st, k, x, y, scale, dy, dx, relu_y, dx_relu);
+  return launch_k(lrn_bwd_generic_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale, dy, dx, relu_y,
+                  dx_relu);
 }
 
 cudaError_t softmax_ce(View2D z, const int32_t* labels, float* row_loss, View2D dz, float inv_nloc, int* err,

@@ -73,6 +73,9 @@ struct sg_net {
   std::vector<float*> data_own;
   std::vector<int> relu_of;     // producer i -> fused ReLU layer (or -1)
   std::vector<char> fused_away; // ReLU layer whose forward is done by its producer
+  std::vector<int> relu_after;  // pool i -> ReLU layer whose forward the pool kernel also writes (or -1)
+  std::vector<int> relu_into;   // consumer c -> ReLU layer whose backward c's kernel also does (or -1)
+  std::vector<char> bwd_fused_away;  // ReLU layer whose backward is done by its consumer
   cudaGraphExec_t gexec = nullptr;
   sg_updater* graph_upd = nullptr;
   long long graph_launches = 0;
@@ -184,10 +187,12 @@ sg_status forward_impl(sg_net* n, int i) {
       SG_LCH(conv_fwd(conv_shape(L, *S), n->data[L.src], W, b, n->data[i], n->relu_of[i] >= 0, n->ws, st));
       break;
     case SG_POOL_MAX:
-      SG_LCH(maxpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], n->mask[i], st));
+      SG_LCH(maxpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], n->mask[i], st,
+                         n->relu_after[i] >= 0 ? n->data[n->relu_after[i]] : nullptr));
       break;
     case SG_POOL_AVG:
-      SG_LCH(avgpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], st));
+      SG_LCH(avgpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], st,
+                         n->relu_after[i] >= 0 ? n->data[n->relu_after[i]] : nullptr));
       break;
     case SG_LRN:
       SG_LCH(lrn_fwd(LrnShape{L.rows * L.h * L.w, L.c, L.lrn_size, L.alpha, L.beta, L.k}, n->data[L.src],
@@ -256,18 +261,24 @@ sg_status backward(sg_net* n, int i) {
       }
       return SG_OK;
     case SG_POOL_MAX:
-      if (need_dx) SG_LCH(maxpool_bwd(pool_shape(L, S), n->grad[i], n->mask[i], n->grad[L.src], st));
-      break;
     case SG_POOL_AVG:
-      if (need_dx) SG_LCH(avgpool_bwd(pool_shape(L, S), n->grad[i], n->grad[L.src], st));
-      break;
-    case SG_LRN:
-      if (need_dx)
+    case SG_LRN: {
+      // fused backward of the ReLU feeding this layer: also dx_relu = dx * [relu_y > 0]
+      const int j = n->relu_into[i];
+      const float* ry = j >= 0 ? n->data[j] : nullptr;
+      float* dxr = j >= 0 ? n->grad[P.layers[j].src] : nullptr;
+      if (!need_dx) break;
+      if (L.kind == SG_POOL_MAX)
+        SG_LCH(maxpool_bwd(pool_shape(L, S), n->grad[i], n->mask[i], n->grad[L.src], st, ry, dxr));
+      else if (L.kind == SG_POOL_AVG)
+        SG_LCH(avgpool_bwd(pool_shape(L, S), n->grad[i], n->grad[L.src], st, ry, dxr));
+      else
         SG_LCH(lrn_bwd(LrnShape{L.rows * L.h * L.w, L.c, L.lrn_size, L.alpha, L.beta, L.k}, n->data[L.src],
-                       n->data[i], n->scale[i], n->grad[i], n->grad[L.src], st));
+                       n->data[i], n->scale[i], n->grad[i], n->grad[L.src], st, ry, dxr));
       break;
+    }
     case SG_RELU:
-      if (need_dx) SG_LCH(relu_bwd(n->data[i], n->grad[i], n->grad[L.src], L.blob_floats(), st));
+      if (need_dx && !n->bwd_fused_away[i]) SG_LCH(relu_bwd(n->data[i], n->grad[i], n->grad[L.src], L.blob_floats(), st));
       break;
     case SG_SIGMOID:
       if (need_dx) SG_LCH(sigmoid_bwd(n->data[i], n->grad[i], n->grad[L.src], L.blob_floats(), st));
@@ -512,7 +523,34 @@ void apply_fusion(sg_net* n) {
   n->data = n->data_own;
   n->relu_of.assign(nl, -1);
   n->fused_away.assign(nl, 0);
+  n->relu_after.assign(nl, -1);
+  n->relu_into.assign(nl, -1);
+  n->bwd_fused_away.assign(nl, 0);
   if (!n->fuse) return;
+  std::vector<int> consumers(nl, 0), consumer(nl, -1);
+  for (int c = 0; c < nl; ++c)
+    if (P.layers[c].src >= 0) {
+      ++consumers[P.layers[c].src];
+      consumer[P.layers[c].src] = c;
+    }
+  for (int j = 0; j < nl; ++j) {
+    const LayerPlan& R = P.layers[j];
+    if (R.kind != SG_RELU || R.src < 0) continue;
+    const LayerPlan& S = P.layers[R.src];
+    // forward: a pooling layer also writes the ReLU of its output
+    if ((S.kind == SG_POOL_MAX || S.kind == SG_POOL_AVG) && S.blob_floats() == R.blob_floats() && S.ld == R.ld &&
+        S.nblocks == R.nblocks) {
+      n->relu_after[R.src] = j;
+      n->fused_away[j] = 1;
+    }
+    // backward: the ReLU's single consumer (LRN / pooling) also applies the ReLU mask
+    const int c = consumer[j];
+    if (consumers[j] == 1 && S.kind != SG_INPUT &&
+        (P.layers[c].kind == SG_LRN || P.layers[c].kind == SG_POOL_MAX || P.layers[c].kind == SG_POOL_AVG)) {
+      n->relu_into[c] = j;
+      n->bwd_fused_away[j] = 1;
+    }
+  }
   for (int j = 0; j < nl; ++j) {
     const LayerPlan& R = P.layers[j];
     if (R.kind != SG_RELU || R.src < 0) continue;

@@ -312,10 +312,15 @@ SG_API sg_status sg_net_loss(sg_net* n, float* loss_dev, void* stream);
 SG_API sg_status sg_net_sync(sg_net* n);
 /* Capture the whole sg_train_one_batch step in a CUDA graph (NCCL included) and replay it. */
 SG_API sg_status sg_net_enable_graph(sg_net* n, int32_t enable);
-/* Fuse a ReLU layer into the epilogue of its convolution / inner-product
- * source (default on).  Results are bit-identical either way; with fusion on,
- * the producer's data blob holds the post-ReLU values (it aliases the ReLU
- * layer's blob).  Call between steps. */
+/* Layer fusion (default on; results bit-identical either way; call between steps):
+ *  - a ReLU after a convolution / inner product runs in the GEMM epilogue; the
+ *    producer's data blob then holds the post-ReLU values (it aliases the ReLU
+ *    layer's blob);
+ *  - a ReLU after a pooling layer is written by the pooling kernel, and
+ *    pooling [-> ReLU] -> LRN runs as one kernel;
+ *  - a ReLU's backward is done by the backward kernel of its single consumer
+ *    (LRN or pooling).
+ * Every layer's data / grad blob is still written (sg_blob_get sees them). */
 SG_API sg_status sg_net_set_fusion(sg_net* n, int32_t enable);
 /* Kernel launches issued by the last sg_train_one_batch (graph replay counts the captured kernels). */
 SG_API sg_status sg_net_last_launch_count(const sg_net* n, int64_t* launches);

@@ -132,6 +132,10 @@ struct LrnShape {
   float alpha, beta, k;
 };
 cudaError_t lrn_fwd(const LrnShape& s, const float* x, float* y, float* scale, cudaStream_t st);
+// Pooling (+ the ReLU after it) + LRN in one pass (runtime layer fusion).
+bool pool_lrn_fusable(const PoolShape& ps, const LrnShape& ls);
+cudaError_t pool_lrn_fwd(const PoolShape& ps, bool max_pool, const float* x, float* py, uint8_t* arg, float* relu_out,
+                         const LrnShape& ls, float* ly, float* scale, cudaStream_t st);
 cudaError_t lrn_bwd(const LrnShape& s, const float* x, const float* y, const float* scale, const float* dy, float* dx,
                     cudaStream_t st, const float* relu_y = nullptr, float* dx_relu = nullptr);
 

@@ -279,30 +279,114 @@ __device__ __forceinline__ void lrn_neighbours(float4 me, int c4, int C4, float 
   e[8] = hr ? r.x : 0.f; e[9] = hr ? r.y : 0.f; e[10] = hr ? r.z : 0.f; e[11] = hr ? r.w : 0.f;
 }
 
-__global__ void lrn_fwd_kernel(LrnK K, const float* __restrict__ x, float* __restrict__ y, float* __restrict__ scale) {
-  pdl_entry();
-  const LrnShape& s = K.s;
+// LRN of the float4 v (channels 4*c4 .. 4*c4+3 of a pixel); every lane of the
+// warp must call it (shuffles).
+__device__ __forceinline__ void lrn_apply(const LrnShape& s, int C4, float4 v, int c4, float4& sc4, float4& o4) {
   const int half = s.n / 2;
   const float an = s.alpha / (float)s.n;
-  const int valid = (int)(s.pixels * K.C4);
+  float e[12];
+  lrn_neighbours(make_float4(v.x * v.x, v.y * v.y, v.z * v.z, v.w * v.w), c4, C4, e);
+  float sc[4], o[4];
+  const float xv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float acc = 0.f;
+    for (int d = -half; d <= half; ++d) acc += e[4 + j + d];
+    sc[j] = s.k + an * acc;
+    o[j] = xv[j] * pow_neg(sc[j], s.beta);
+  }
+  sc4 = make_float4(sc[0], sc[1], sc[2], sc[3]);
+  o4 = make_float4(o[0], o[1], o[2], o[3]);
+}
+
+__global__ void lrn_fwd_kernel(LrnK K, const float* __restrict__ x, float* __restrict__ y, float* __restrict__ scale) {
+  pdl_entry();
+  const int valid = (int)(K.s.pixels * K.C4);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K.total; i += gridDim.x * blockDim.x) {
     const bool in = i < valid;
     const int c4 = i % K.C4;  // C4 is a power of two
     const float4 v = in ? __ldg(reinterpret_cast<const float4*>(x) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    float e[12];
-    lrn_neighbours(make_float4(v.x * v.x, v.y * v.y, v.z * v.z, v.w * v.w), c4, K.C4, e);
-    float sc[4], o[4];
-    const float xv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float acc = 0.f;
-      for (int d = -half; d <= half; ++d) acc += e[4 + j + d];
-      sc[j] = s.k + an * acc;
-      o[j] = xv[j] * pow_neg(sc[j], s.beta);
-    }
+    float4 sc4, o4;
+    lrn_apply(K.s, K.C4, v, c4, sc4, o4);
     if (in) {
-      reinterpret_cast<float4*>(scale)[i] = make_float4(sc[0], sc[1], sc[2], sc[3]);
-      reinterpret_cast<float4*>(y)[i] = make_float4(o[0], o[1], o[2], o[3]);
+      reinterpret_cast<float4*>(scale)[i] = sc4;
+      reinterpret_cast<float4*>(y)[i] = o4;
+    }
+  }
+}
+
+// Pooling -> (ReLU) -> LRN in one pass (layer fusion): thread per (output pixel,
+// 4 channels), the LRN channel window by warp shuffles; writes the pooling
+// output (+ argmax), the ReLU output and the LRN output + scale, each computed
+// exactly as by the separate kernels.
+__device__ __forceinline__ float4 maxpool_at(const PoolK& P, const float* __restrict__ x, int i, uchar4& arg) {
+  const PoolShape& s = P.s;
+  const int C4 = s.C >> 2;
+  const int t = P.fC4.div(i), c4 = i - t * C4;
+  const int t2 = P.fWo.div(t), ow = t - t2 * s.Wo;
+  const int n = P.fHo.div(t2), oh = t2 - n * s.Ho;
+  const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
+  const int hs = max(h0, 0), he = min(h0 + s.k, s.H), ws = max(w0, 0), we = min(w0 + s.k, s.W);
+  float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  int a[4] = {0, 0, 0, 0};
+  const float* xn = x + (size_t)n * s.H * s.W * s.C + c4 * 4;
+  for (int h = hs; h < he; ++h)
+    for (int w = ws; w < we; ++w) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C));
+      const int off = (h - h0) * s.k + (w - w0);
+      if (v.x > m[0]) { m[0] = v.x; a[0] = off; }
+      if (v.y > m[1]) { m[1] = v.y; a[1] = off; }
+      if (v.z > m[2]) { m[2] = v.z; a[2] = off; }
+      if (v.w > m[3]) { m[3] = v.w; a[3] = off; }
+    }
+  arg = make_uchar4(a[0], a[1], a[2], a[3]);
+  return make_float4(m[0], m[1], m[2], m[3]);
+}
+__device__ __forceinline__ float4 avgpool_at(const PoolK& P, const float* __restrict__ x, int i) {
+  const PoolShape& s = P.s;
+  const int C4 = s.C >> 2;
+  const int t = P.fC4.div(i), c4 = i - t * C4;
+  const int t2 = P.fWo.div(t), ow = t - t2 * s.Wo;
+  const int n = P.fHo.div(t2), oh = t2 - n * s.Ho;
+  const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
+  const int he_u = min(h0 + s.k, s.H + s.p), we_u = min(w0 + s.k, s.W + s.p);
+  const float inv = 1.f / (float)((he_u - h0) * (we_u - w0));
+  const int hs = max(h0, 0), he = min(he_u, s.H), ws = max(w0, 0), we = min(we_u, s.W);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* xn = x + (size_t)n * s.H * s.W * s.C + c4 * 4;
+  for (int h = hs; h < he; ++h)
+    for (int w = ws; w < we; ++w) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C));
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+  return make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+}
+
+template <bool MAX>
+__global__ void pool_lrn_fwd_kernel(PoolK P, LrnK K, const float* __restrict__ x, float* __restrict__ py,
+                                    uint8_t* __restrict__ arg, float* __restrict__ relu_out, float* __restrict__ ly,
+                                    float* __restrict__ scale) {
+  pdl_entry();
+  const int valid = (int)(K.s.pixels * K.C4);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K.total; i += gridDim.x * blockDim.x) {
+    const bool in = i < valid;
+    const int c4 = i % K.C4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (in) {
+      uchar4 a4;
+      v = MAX ? maxpool_at(P, x, i, a4) : avgpool_at(P, x, i);
+      reinterpret_cast<float4*>(py)[i] = v;
+      if (MAX) reinterpret_cast<uchar4*>(arg)[i] = a4;
+      if (relu_out) {
+        v = relu4(v);
+        reinterpret_cast<float4*>(relu_out)[i] = v;
+      }
+    }
+    float4 sc4, o4;
+    lrn_apply(K.s, K.C4, v, c4, sc4, o4);
+    if (in) {
+      reinterpret_cast<float4*>(scale)[i] = sc4;
+      reinterpret_cast<float4*>(ly)[i] = o4;
     }
   }
 }
@@ -599,6 +683,27 @@ cudaError_t lrn_bwd(const LrnShape& s, const float* x, const float* y, const flo
     return launch_k(lrn_bwd_kernel, blocks_for(k.total, 256), 256, 0, st, k, x, y, scale, dy, dx, relu_y, dx_relu);
   return launch_k(lrn_bwd_generic_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale, dy, dx, relu_y,
                   dx_relu);
+}
+
+cudaError_t pool_lrn_fwd(const PoolShape& ps, bool max_pool, const float* x, float* py, uint8_t* arg, float* relu_out,
+                         const LrnShape& ls, float* ly, float* scale, cudaStream_t st) {
+  LrnK k;
+  const long long n4 = (long long)ps.N * ps.Ho * ps.Wo * ps.C / 4;
+  if (ps.C % 4 || ls.C != ps.C || ls.pixels != (long long)ps.N * ps.Ho * ps.Wo || !fits32(n4 * 4) ||
+      !fits32((long long)ps.N * ps.H * ps.W * ps.C) || (max_pool && ps.k * ps.k > 256) ||
+      !lrn_fast(ls, {py, ly, scale, relu_out ? relu_out : py}, &k))
+    return cudaErrorInvalidValue;
+  if (max_pool)
+    return launch_k(pool_lrn_fwd_kernel<true>, blocks_for(k.total, 256), 256, 0, st, pool_k(ps), k, x, py, arg,
+                    relu_out, ly, scale);
+  return launch_k(pool_lrn_fwd_kernel<false>, blocks_for(k.total, 256), 256, 0, st, pool_k(ps), k, x, py, arg,
+                  relu_out, ly, scale);
+}
+bool pool_lrn_fusable(const PoolShape& ps, const LrnShape& ls) {
+  LrnK k;
+  float dummy[4] __attribute__((aligned(16)));
+  return ps.C % 4 == 0 && ls.C == ps.C && ls.pixels == (long long)ps.N * ps.Ho * ps.Wo && ps.k * ps.k <= 256 &&
+         fits32((long long)ps.N * ps.H * ps.W * ps.C) && lrn_fast(ls, {dummy}, &k);
 }
 
 cudaError_t softmax_ce(View2D z, const int32_t* labels, float* row_loss, View2D dz, float inv_nloc, int* err,

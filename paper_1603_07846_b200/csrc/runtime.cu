@@ -76,6 +76,8 @@ struct sg_net {
   std::vector<int> relu_after;  // pool i -> ReLU layer whose forward the pool kernel also writes (or -1)
   std::vector<int> relu_into;   // consumer c -> ReLU layer whose backward c's kernel also does (or -1)
   std::vector<char> bwd_fused_away;  // ReLU layer whose backward is done by its consumer
+  std::vector<int> lrn_after;   // pool i -> LRN layer computed by the pool's forward kernel (or -1)
+  std::vector<char> lrn_fused;  // LRN layer whose forward is done by the pool before it
   cudaGraphExec_t gexec = nullptr;
   sg_updater* graph_upd = nullptr;
   long long graph_launches = 0;
@@ -187,16 +189,26 @@ sg_status forward_impl(sg_net* n, int i) {
       SG_LCH(conv_fwd(conv_shape(L, *S), n->data[L.src], W, b, n->data[i], n->relu_of[i] >= 0, n->ws, st));
       break;
     case SG_POOL_MAX:
-      SG_LCH(maxpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], n->mask[i], st,
-                         n->relu_after[i] >= 0 ? n->data[n->relu_after[i]] : nullptr));
+    case SG_POOL_AVG: {
+      float* relu_out = n->relu_after[i] >= 0 ? n->data[n->relu_after[i]] : nullptr;
+      const int k = n->lrn_after[i];
+      if (k >= 0) {  // pooling [-> ReLU] -> LRN in one kernel
+        const LayerPlan& Lk = P.layers[k];
+        SG_LCH(pool_lrn_fwd(pool_shape(L, *S), L.kind == SG_POOL_MAX, n->data[L.src], n->data[i],
+                            L.kind == SG_POOL_MAX ? n->mask[i] : nullptr, relu_out,
+                            LrnShape{Lk.rows * Lk.h * Lk.w, Lk.c, Lk.lrn_size, Lk.alpha, Lk.beta, Lk.k}, n->data[k],
+                            n->scale[k], st));
+      } else if (L.kind == SG_POOL_MAX) {
+        SG_LCH(maxpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], n->mask[i], st, relu_out));
+      } else {
+        SG_LCH(avgpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], st, relu_out));
+      }
       break;
-    case SG_POOL_AVG:
-      SG_LCH(avgpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], st,
-                         n->relu_after[i] >= 0 ? n->data[n->relu_after[i]] : nullptr));
-      break;
+    }
     case SG_LRN:
-      SG_LCH(lrn_fwd(LrnShape{L.rows * L.h * L.w, L.c, L.lrn_size, L.alpha, L.beta, L.k}, n->data[L.src],
-                     n->data[i], n->scale[i], st));
+      if (!n->lrn_fused[i])
+        SG_LCH(lrn_fwd(LrnShape{L.rows * L.h * L.w, L.c, L.lrn_size, L.alpha, L.beta, L.k}, n->data[L.src],
+                       n->data[i], n->scale[i], st));
       break;
     case SG_RELU:
       if (!n->fused_away[i]) SG_LCH(relu_fwd(n->data[L.src], n->data[i], L.blob_floats(), st));
@@ -526,6 +538,8 @@ void apply_fusion(sg_net* n) {
   n->relu_after.assign(nl, -1);
   n->relu_into.assign(nl, -1);
   n->bwd_fused_away.assign(nl, 0);
+  n->lrn_after.assign(nl, -1);
+  n->lrn_fused.assign(nl, 0);
   if (!n->fuse) return;
   std::vector<int> consumers(nl, 0), consumer(nl, -1);
   for (int c = 0; c < nl; ++c)
@@ -561,6 +575,23 @@ void apply_fusion(sg_net* n) {
     n->relu_of[i] = j;
     n->fused_away[j] = 1;
     n->data[i] = n->data[j];
+  }
+  // pooling [-> ReLU] -> LRN: one kernel (the pool feeds only the ReLU / LRN)
+  for (int k = 0; k < nl; ++k) {
+    const LayerPlan& Lk = P.layers[k];
+    if (Lk.kind != SG_LRN || Lk.src < 0) continue;
+    int pool = Lk.src;
+    if (P.layers[pool].kind == SG_RELU) {
+      const int j = pool;
+      pool = P.layers[j].src;
+      if (pool < 0 || n->relu_after[pool] != j || consumers[j] != 1) continue;
+    }
+    const LayerPlan& Lp = P.layers[pool];
+    if ((Lp.kind != SG_POOL_MAX && Lp.kind != SG_POOL_AVG) || consumers[pool] != 1) continue;
+    const LrnShape ls{Lk.rows * Lk.h * Lk.w, Lk.c, Lk.lrn_size, Lk.alpha, Lk.beta, Lk.k};
+    if (!pool_lrn_fusable(pool_shape(Lp, P.layers[Lp.src]), ls)) continue;
+    n->lrn_after[pool] = k;
+    n->lrn_fused[k] = 1;
   }
 }
 

@@ -327,39 +327,42 @@ cudaError_t run_img(ImgConvArgs a, size_t smem, int nimg, cudaStream_t st) {
 }
 
 // --------------------------------------------- 4-channel first layer forward --
-// Same idea for C = 4 (CIFAR conv1): the image is staged with 8 channels per
-// pixel (channels 4..7 = TMA out-of-bounds zeros) as K-major SWIZZLE_32B rows of
-// 32 B, so a filter tap is ONE K = 8 MMA per 128-row tile on a row-shifted
-// descriptor (32-byte rows may start anywhere: tools/desc_shift32.cu).  The
-// filter bank is staged the same way ([t][co][8 channels]).
-constexpr uint64_t kLayoutSW32 = 6;
-
-__device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t saddr) {
-  const uint64_t d = umma_desc_sw128(saddr, 16, 256);  // SBO = 8 rows x 32 B
-  return (d & ~((uint64_t)7 << 61)) | (kLayoutSW32 << 61);
-}
-
-struct Img8Args {
-  CUtensorMap img_map;  // x {4, W, H, N}, box {8, Wp, Hrows, 1}, SWIZZLE_32B
-  CUtensorMap w_map;    // W {4, Co, T} (strides T*16, 16), box {8, Co, T}, SWIZZLE_32B
+// Same idea for C = 4 (CIFAR conv1), with TWO filter taps per K = 8 MMA: the
+// image is staged unpadded (16 B per pixel, no swizzle) and the A operand is a
+// SWIZZLE_NONE K-major descriptor with 8-row stride SBO = 128 B and K-chunk
+// stride LBO = 16 B, i.e. overlapping core matrices:
+//   A[m][k] = img[q0 + off + m + k/4][k % 4]   (taps (r, s) and (r, s+1))
+// (probed exactly by tools/desc_overlap.cu).  The filter bank is staged tap-major
+// with each filter row padded to an even number of taps (zero weights), so the
+// B operand of a tap pair is W[(r*SP + s) .. +1][co][4] with LBO = Co*16 B.
+struct Img4Args {
+  CUtensorMap img_map;  // x {4, W, H, N}, box {4, Wp, Hrows, 1}, no swizzle
+  CUtensorMap w_map;    // W {4, Co, T} (strides T*16, 16), box {4, Co, S}, no swizzle
   const float* bias;
   float* out;
-  int pad, R, S, Wp, Ho, Wo, Hrows, img_rows, ntiles, relu;
+  int pad, R, S, SP, Wp, Ho, Wo, Hrows, img_rows, ntiles, relu;
 };
 
 template <int NB>
-__global__ void __launch_bounds__(kImgThreads, 1) conv_img8_fwd_kernel(const __grid_constant__ Img8Args a) {
+__global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __grid_constant__ Img4Args a) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t img = base;
-  const uint32_t wbase = img + ((a.img_rows * 32 + 1023) & ~1023);
-  const int T = a.R * a.S;
-  const uint32_t wbytes = (uint32_t)T * NB * 32;
+  const uint32_t wbase = img + ((a.img_rows * 16 + 1023) & ~1023);
+  const uint32_t wbytes = (uint32_t)a.R * a.SP * NB * 16;
   const uint32_t bar = wbase + ((wbytes + 1023) & ~1023u), done_bar = bar + 8, slot = done_bar + 8;
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = blockIdx.x;
 
+  // zero weights of the padding taps s in [S, SP) (disjoint from the TMA boxes)
+  for (int i = tid; i < a.R * (a.SP - a.S) * NB; i += kImgThreads) {
+    const int r = i / ((a.SP - a.S) * NB), rem = i - r * (a.SP - a.S) * NB;
+    const int sc = a.S + rem / NB, co = rem % NB;
+    asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(wbase + ((r * a.SP + sc) * NB + co) * 16), "f"(0.f)
+                 : "memory");
+  }
+  fence_proxy_async_smem();
   if (tid == 0) {
     mbar_init(bar, 1);
     mbar_init(done_bar, 1);
@@ -375,30 +378,28 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img8_fwd_kernel(const __g
   pdl_entry();
   if (tid == 0) {
     IMG_TRACE(5, 0);
-    mbar_arrive_expect_tx(bar, (uint32_t)a.Hrows * a.Wp * 32 + wbytes);
+    mbar_arrive_expect_tx(bar, (uint32_t)a.Hrows * a.Wp * 16 + (uint32_t)a.R * a.S * NB * 16);
     tma_load_4d(img, &a.img_map, 0, -a.pad, -a.pad, n, bar);
-    tma_load_3d(wbase, &a.w_map, 0, 0, 0, bar);
+    for (int r = 0; r < a.R; ++r) tma_load_3d(wbase + r * a.SP * NB * 16, &a.w_map, 0, 0, r * a.S, bar);
   }
   if (warp == 4) {
     constexpr uint32_t idesc = idesc_tf32(128, NB, 0, 0);
-    const uint64_t ad0 = umma_desc_sw32(img), bd0 = umma_desc_sw32(wbase);
+    const uint64_t ad0 = umma_desc_noswz(img, 16, 128), bd0 = umma_desc_noswz(wbase, NB * 16, 128);
     const uint32_t a_lo0 = (uint32_t)ad0, a_hi = (uint32_t)(ad0 >> 32);
     const uint32_t b_lo0 = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
     mbar_wait(bar, 0);
     tc_fence_after();
     if (lane == 0) {
       IMG_TRACE(3, 0);
-      int r = 0, sc = 0;
-      for (int t = 0; t < T; ++t) {
-        const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc) * 2;  // 32-B rows
-        const uint32_t b_t = b_lo0 + (uint32_t)t * NB * 2;
-        for (int i = 0; i < a.ntiles; ++i)
-          mma_tf32_lh(tmem + i * NB, a_t + i * 256, a_hi, b_t, b_hi, idesc, t ? 1u : 0u);
-        if (++sc == a.S) {
-          sc = 0;
-          ++r;
+      bool first = true;
+      for (int r = 0; r < a.R; ++r)
+        for (int sc = 0; sc < a.S; sc += 2) {
+          const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc);  // 16-B pixel rows: start field += 1
+          const uint32_t b_t = b_lo0 + (uint32_t)(r * a.SP + sc) * NB;
+          for (int i = 0; i < a.ntiles; ++i)
+            mma_tf32_lh(tmem + i * NB, a_t + i * 128, a_hi, b_t, b_hi, idesc, first ? 0u : 1u);
+          first = false;
         }
-      }
       IMG_TRACE(2, 0);
       mma_commit(done_bar);
     }
@@ -441,26 +442,26 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img8_fwd_kernel(const __g
   }
   tc_fence_before();
   __syncthreads();
-  if (tid == 0) IMG_TRACE(0, 0);
   if (warp == 4) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
 }
 
-bool plan_img8(const ConvShape& s, Img8Args* a, size_t* smem) {
+bool plan_img4(const ConvShape& s, Img4Args* a, size_t* smem) {
   if (!img_conv_enabled() || s.C != 4 || s.st != 1 || (s.Co != 32 && s.Co != 64)) return false;
-  Img8Args g{};
-  g.pad = s.pad, g.R = s.R, g.S = s.S;
+  Img4Args g{};
+  g.pad = s.pad, g.R = s.R, g.S = s.S, g.SP = s.S + (s.S & 1);
   g.Wp = s.W + 2 * s.pad, g.Ho = s.Ho, g.Wo = s.Wo;
   g.ntiles = (g.Ho * g.Wp + 127) / 128;
   if (g.ntiles * s.Co > 512) return false;
-  const int need = g.ntiles * 128 + (s.R - 1) * g.Wp + s.S - 1;
+  // rows read: tiles x 128 + the largest tap shift + the pair's second pixel
+  const int need = g.ntiles * 128 + (s.R - 1) * g.Wp + g.SP - 1;
   g.Hrows = (need + g.Wp - 1) / g.Wp;
   g.img_rows = g.Hrows * g.Wp;
-  if (g.Hrows > 256 || g.Wp > 256 || s.R * s.S > 256) return false;
-  *smem = 1024 + (((size_t)g.img_rows * 32 + 1023) & ~(size_t)1023) +
-          (((size_t)s.R * s.S * s.Co * 32 + 1023) & ~(size_t)1023) + 64;
+  if (g.Hrows > 256 || g.Wp > 256 || s.S > 256) return false;
+  *smem = 1024 + (((size_t)g.img_rows * 16 + 1023) & ~(size_t)1023) +
+          (((size_t)s.R * g.SP * s.Co * 16 + 1023) & ~(size_t)1023) + 64;
   if (*smem > 227 * 1024) return false;
   *a = g;
   return true;
@@ -729,9 +730,9 @@ cudaError_t conv_img_wgrad(const ConvShape& s, const float* x, const float* dy, 
 
 bool conv_img_fwd_ok(const ConvShape& s) {
   ImgConvArgs a;
-  Img8Args a8;
+  Img4Args a4;
   size_t smem;
-  return plan_img(s, false, &a, &smem) || plan_img8(s, &a8, &smem);
+  return plan_img(s, false, &a, &smem) || plan_img4(s, &a4, &smem);
 }
 bool conv_img_dgrad_ok(const ConvShape& s) {
   ImgConvArgs a;
@@ -761,25 +762,25 @@ cudaError_t conv_img_fwd(const ConvShape& s, const float* x, const float* W, con
                          cudaStream_t st) {
   ImgConvArgs a;
   size_t smem;
-  Img8Args a8;
-  if (plan_img8(s, &a8, &smem)) {
-    a8.bias = b;
-    a8.out = y;
-    a8.relu = relu;
+  Img4Args a4;
+  if (plan_img4(s, &a4, &smem)) {
+    a4.bias = b;
+    a4.out = y;
+    a4.relu = relu;
     const int T = s.R * s.S;
     const cuuint64_t xd[4] = {4, (cuuint64_t)s.W, (cuuint64_t)s.H, (cuuint64_t)s.N};
     const cuuint64_t xs[3] = {16, (cuuint64_t)s.W * 16, (cuuint64_t)s.H * s.W * 16};
-    const cuuint32_t xb[4] = {8, (cuuint32_t)a8.Wp, (cuuint32_t)a8.Hrows, 1};
+    const cuuint32_t xb[4] = {4, (cuuint32_t)a4.Wp, (cuuint32_t)a4.Hrows, 1};
     const cuuint64_t wd[3] = {4, (cuuint64_t)s.Co, (cuuint64_t)T};
     const cuuint64_t ws[2] = {(cuuint64_t)T * 16, 16};
-    const cuuint32_t wb[3] = {8, (cuuint32_t)s.Co, (cuuint32_t)T};
-    if (!encode_tiled_f32(&a8.img_map, x, 4, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_32B) ||
-        !encode_tiled_f32(&a8.w_map, W, 3, wd, ws, wb, CU_TENSOR_MAP_SWIZZLE_32B))
+    const cuuint32_t wb[3] = {4, (cuuint32_t)s.Co, (cuuint32_t)s.S};
+    if (!encode_tiled_f32(&a4.img_map, x, 4, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !encode_tiled_f32(&a4.w_map, W, 3, wd, ws, wb, CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
-    auto k = s.Co == 32 ? conv_img8_fwd_kernel<32> : conv_img8_fwd_kernel<64>;
+    auto k = s.Co == 32 ? conv_img4_fwd_kernel<32> : conv_img4_fwd_kernel<64>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return launch_k(k, s.N, kImgThreads, smem, st, a8);
+    return launch_k(k, s.N, kImgThreads, smem, st, a4);
   }
   if (!plan_img(s, false, &a, &smem)) return cudaErrorInvalidValue;
   a.src = x;

@@ -365,7 +365,11 @@ def main():
             ops.append({"op": name, "ms": avg, "flops": fl, "bytes": by})
     ops.sort(key=lambda o: -o["ms"])
     prof_total = sum(o["ms"] for o in ops)
-    dom = ops[0] if ops else None
+    # at N > 1 a layer's update slot times the reduce-scatter -> Updater -> all-gather
+    # chain on the parameter stream (mostly NCCL waiting); the roofline names the
+    # dominant compute operation instead
+    cand = [o for o in ops if world == 1 or not o["op"].endswith(".update")]
+    dom = cand[0] if cand else None
     roof = None
     if dom:
         t_s = dom["ms"] / 1e3

@@ -542,12 +542,20 @@ __global__ void small_gemm_warp_kernel(const __grid_constant__ SmallArgs g) {
   if (lane == 0) epi_store1(g.e, m, n, acc, g.N);
 }
 
-// thread per output, consecutive threads along m (op(A) = A^T: coalesced in m)
+// thread per output; consecutive threads along n (coalesced output rows and
+// op(B) rows), or along m when op(A) = A^T (coalesced A columns)
 __global__ void small_gemm_thread_kernel(const __grid_constant__ SmallArgs g) {
   pdl_entry();
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= (long long)g.M * g.N) return;
-  const int n = (int)(t / g.M), m = (int)(t - (long long)n * g.M);
+  int m, n;
+  if (g.ta) {
+    n = (int)(t / g.M);
+    m = (int)(t - (long long)n * g.M);
+  } else {
+    m = (int)(t / g.N);
+    n = (int)(t - (long long)m * g.N);
+  }
   float acc = 0.f;
 #pragma unroll 16  // loads of later k issue while earlier FMAs wait (loop-carried acc only)
   for (int k = 0; k < g.K; ++k) acc = fmaf(small_a(g, m, k), small_b(g, k, n), acc);

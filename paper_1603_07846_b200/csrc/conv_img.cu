@@ -72,6 +72,36 @@ __device__ __forceinline__ uint32_t ksw(int row, int chunk) {  // K-major SW128 
   return row * 128 + ((chunk ^ (row & 7)) << 4);
 }
 
+// Epilogue of the resident-image kernels: warp w (TMEM lane group) drains the
+// NT tiles' NB accumulator columns for its 32 output rows; all tcgen05.ld of a
+// tile are issued before one wait, the bias is read once.
+template <int NB>
+__device__ __forceinline__ void img_epilogue(uint32_t tmem, int ntiles, int warp, int lane, int Wp, int Ho, int Wo,
+                                             float* outn, const float* bias, int relu) {
+  float bv[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) bv[c] = bias ? __ldg(bias + c) : 0.f;
+#pragma unroll 1
+  for (int i = 0; i < ntiles; ++i) {
+    uint32_t r[NB / 16][16];
+#pragma unroll
+    for (int c = 0; c < NB / 16; ++c) tmem_ld16_nowait(tmem + ((uint32_t)(warp * 32) << 16) + i * NB + c * 16, r[c]);
+    tmem_wait_ld();
+    const int q = i * 128 + warp * 32 + lane;
+    const int oh = q / Wp, ow = q - oh * Wp;
+    if (oh >= Ho || ow >= Wo) continue;
+    float4* dst = reinterpret_cast<float4*>(outn + ((size_t)oh * Wo + ow) * NB);
+#pragma unroll
+    for (int j = 0; j < NB; j += 4) {
+      float4 o = make_float4(__uint_as_float(r[j / 16][j % 16]) + bv[j], __uint_as_float(r[j / 16][j % 16 + 1]) + bv[j + 1],
+                             __uint_as_float(r[j / 16][j % 16 + 2]) + bv[j + 2],
+                             __uint_as_float(r[j / 16][j % 16 + 3]) + bv[j + 3]);
+      if (relu) o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
+      dst[j / 4] = o;
+    }
+  }
+}
+
 // NT output tiles of 128 padded-width rows, CB 32-channel K blocks of the
 // source (compile time, so the MMA issue of a tap is straight-line code).
 // Shared memory: image planes [CB][img_rows][128 B], then the filter bank
@@ -204,37 +234,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
     mbar_wait_sleep(done_bar, 0);
     if (tid == 0) IMG_TRACE(4, 0);
     tc_fence_after();
-    float* outn = a.out + (size_t)n * a.Ho * a.Wo * NB;
-#pragma unroll 1
-    for (int i = 0; i < NT; ++i) {
-      const int q = i * 128 + warp * 32 + lane;
-      const int oh = q / a.Wp, ow = q - oh * a.Wp;
-      const bool valid = oh < a.Ho && ow < a.Wo;
-      float* dst = outn + ((size_t)oh * a.Wo + ow) * NB;
-#pragma unroll 1
-      for (int c0 = 0; c0 < NB; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + i * NB + c0, v);
-        if (!valid) continue;
-#pragma unroll
-        for (int j = 0; j < 16; j += 4) {
-          float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          if (a.bias) {
-            o.x += __ldg(a.bias + c0 + j);
-            o.y += __ldg(a.bias + c0 + j + 1);
-            o.z += __ldg(a.bias + c0 + j + 2);
-            o.w += __ldg(a.bias + c0 + j + 3);
-          }
-          if (a.relu) {
-            o.x = fmaxf(o.x, 0.f);
-            o.y = fmaxf(o.y, 0.f);
-            o.z = fmaxf(o.z, 0.f);
-            o.w = fmaxf(o.w, 0.f);
-          }
-          *reinterpret_cast<float4*>(dst + c0 + j) = o;
-        }
-      }
-    }
+    img_epilogue<NB>(tmem, NT, warp, lane, a.Wp, a.Ho, a.Wo, a.out + (size_t)n * a.Ho * a.Wo * NB, a.bias, a.relu);
   }
   tc_fence_before();
   __syncthreads();
@@ -408,38 +408,10 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __g
     mbar_wait_sleep(done_bar, 0);
     if (tid == 0) IMG_TRACE(4, 0);
     tc_fence_after();
-    float* outn = a.out + (size_t)n * a.Ho * a.Wo * NB;
-#pragma unroll 1
-    for (int i = 0; i < a.ntiles; ++i) {
-      const int q = i * 128 + warp * 32 + lane;
-      const int oh = q / a.Wp, ow = q - oh * a.Wp;
-      const bool valid = oh < a.Ho && ow < a.Wo;
-      float* dst = outn + ((size_t)oh * a.Wo + ow) * NB;
-#pragma unroll 1
-      for (int c0 = 0; c0 < NB; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + i * NB + c0, v);
-        if (!valid) continue;
-#pragma unroll
-        for (int j = 0; j < 16; j += 4) {
-          float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          if (a.bias) {
-            o.x += __ldg(a.bias + c0 + j);
-            o.y += __ldg(a.bias + c0 + j + 1);
-            o.z += __ldg(a.bias + c0 + j + 2);
-            o.w += __ldg(a.bias + c0 + j + 3);
-          }
-          if (a.relu) {
-            o.x = fmaxf(o.x, 0.f);
-            o.y = fmaxf(o.y, 0.f);
-            o.z = fmaxf(o.z, 0.f);
-            o.w = fmaxf(o.w, 0.f);
-          }
-          *reinterpret_cast<float4*>(dst + c0 + j) = o;
-        }
-      }
-    }
+    img_epilogue<NB>(tmem, a.ntiles, warp, lane, a.Wp, a.Ho, a.Wo, a.out + (size_t)n * a.Ho * a.Wo * NB, a.bias,
+                     a.relu);
   }
+  if (tid == 0) IMG_TRACE(0, 0);
   tc_fence_before();
   __syncthreads();
   if (warp == 4) {

@@ -91,7 +91,7 @@ Plan plan_gemm(int M, int N, int K, size_t ws_floats_avail) {
 // Fixed-order split-K reduction.  A block of G warps owns 128 consecutive
 // entries of the padded workspace row space (m * pad4(N) + n, one float4 per
 // lane); warp g sums the splits g, g+G, g+2G, ... in ascending order, then warp 0
-// adds the G partial sums in ascending g.  G = min(16, splits) depends on the
+// adds the G partial sums in ascending g.  G = min(32, splits) depends on the
 // shape only, so the result is deterministic.
 __device__ __forceinline__ void reduce_store(const EpiArgs& e, int m, int n, int N, float t) {
   if (m >= e.mvalid) {
@@ -106,10 +106,10 @@ __device__ __forceinline__ void reduce_store(const EpiArgs& e, int m, int n, int
     *out_at(e, m, n, N) = t;
 }
 
-__global__ void __launch_bounds__(512) splitk_reduce_kernel(const float* __restrict__ ws, int splits,
+__global__ void __launch_bounds__(1024) splitk_reduce_kernel(const float* __restrict__ ws, int splits,
                                                             long long split_stride, int M, int N, EpiArgs e) {
   pdl_entry();
-  __shared__ float4 part[16][32];
+  __shared__ float4 part[32][32];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5, G = blockDim.x >> 5;
   const int ldw = (N + 3) & ~3;
   const long long q = ((long long)blockIdx.x * 32 + lane) * 4;  // first padded entry of this lane
@@ -207,7 +207,7 @@ cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int
   }
   if (e != cudaSuccess || p.splits == 1 || fixup) return e;
   const long long total4 = (long long)M * pad4(N) / 4;
-  const int G = std::min(16, p.splits);
+  const int G = std::min(32, p.splits);  // 32 measured ~1% faster than 16 on CIFAR-10 (148-split conv1 wgrad)
   return launch_k(splitk_reduce_kernel, (unsigned)((total4 + 31) / 32), 32 * G, 0, st, (const float*)part, p.splits,
                   (long long)M * pad4(N), M, N, epi);
 }

@@ -164,17 +164,35 @@ __global__ void maxpool_bwd_kernel(PoolK P, const float* __restrict__ dy, const 
     pool_windows(wp, s.k, s.Wo, P.fS, ow0, ow1);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     const size_t nb = (size_t)n * s.Ho * s.Wo * s.C + c4 * 4;
-    for (int oh = oh0; oh <= oh1; ++oh)
-      for (int ow = ow0; ow <= ow1; ++ow) {
-        const int off = (hp - oh * s.s) * s.k + (wp - ow * s.s);
-        const size_t o = nb + (size_t)(oh * s.Wo + ow) * s.C;
-        const uchar4 a = __ldg(reinterpret_cast<const uchar4*>(arg + o));
-        const float4 g = __ldg(reinterpret_cast<const float4*>(dy + o));
-        if (a.x == off) acc.x += g.x;
-        if (a.y == off) acc.y += g.y;
-        if (a.z == off) acc.z += g.z;
-        if (a.w == off) acc.w += g.w;
+    auto add = [&](int oh, int ow, uchar4 a, float4 g) {
+      const int off = (hp - oh * s.s) * s.k + (wp - ow * s.s);
+      if (a.x == off) acc.x += g.x;
+      if (a.y == off) acc.y += g.y;
+      if (a.z == off) acc.z += g.z;
+      if (a.w == off) acc.w += g.w;
+    };
+    if (oh1 - oh0 <= 1 && ow1 - ow0 <= 1) {
+      // at most 2 x 2 windows (k <= 2s): issue all loads first, add in (oh, ow) order
+      uchar4 a[4];
+      float4 g[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const int oh = oh0 + (w >> 1), ow = ow0 + (w & 1);
+        const bool ok = oh <= oh1 && ow <= ow1;
+        const size_t o = nb + (size_t)(ok ? oh * s.Wo + ow : 0) * s.C;
+        a[w] = ok ? __ldg(reinterpret_cast<const uchar4*>(arg + o)) : make_uchar4(255, 255, 255, 255);
+        g[w] = ok ? __ldg(reinterpret_cast<const float4*>(dy + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if (oh0 + (w >> 1) <= oh1 && ow0 + (w & 1) <= ow1) add(oh0 + (w >> 1), ow0 + (w & 1), a[w], g[w]);
+    } else {
+      for (int oh = oh0; oh <= oh1; ++oh)
+        for (int ow = ow0; ow <= ow1; ++ow) {
+          const size_t o = nb + (size_t)(oh * s.Wo + ow) * s.C;
+          add(oh, ow, __ldg(reinterpret_cast<const uchar4*>(arg + o)), __ldg(reinterpret_cast<const float4*>(dy + o)));
+        }
+    }
     *reinterpret_cast<float4*>(dx + (size_t)i * 4) = acc;
     if (dx_relu)
       *reinterpret_cast<float4*>(dx_relu + (size_t)i * 4) =
@@ -225,16 +243,28 @@ __global__ void avgpool_bwd_kernel(PoolK P, const float* __restrict__ dy, float*
     pool_windows(wp, s.k, s.Wo, P.fS, ow0, ow1);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     const float* dyn = dy + (size_t)n * s.Ho * s.Wo * s.C + c4 * 4;
-    for (int oh = oh0; oh <= oh1; ++oh) {
-      const int h0 = oh * s.s - s.p;
-      const int hsz = min(h0 + s.k, s.H + s.p) - h0;
-      for (int ow = ow0; ow <= ow1; ++ow) {
-        const int w0 = ow * s.s - s.p;
-        const int wsz = min(w0 + s.k, s.W + s.p) - w0;
-        const float inv = 1.f / (float)(hsz * wsz);
-        const float4 g = __ldg(reinterpret_cast<const float4*>(dyn + (oh * s.Wo + ow) * s.C));
-        acc.x += g.x * inv; acc.y += g.y * inv; acc.z += g.z * inv; acc.w += g.w * inv;
+    auto add = [&](int oh, int ow, float4 g) {
+      const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
+      const int hsz = min(h0 + s.k, s.H + s.p) - h0, wsz = min(w0 + s.k, s.W + s.p) - w0;
+      const float inv = 1.f / (float)(hsz * wsz);
+      acc.x += g.x * inv; acc.y += g.y * inv; acc.z += g.z * inv; acc.w += g.w * inv;
+    };
+    if (oh1 - oh0 <= 1 && ow1 - ow0 <= 1) {
+      // at most 2 x 2 windows: issue all loads first, add in (oh, ow) order
+      float4 g[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const int oh = oh0 + (w >> 1), ow = ow0 + (w & 1);
+        const bool ok = oh <= oh1 && ow <= ow1;
+        g[w] = ok ? __ldg(reinterpret_cast<const float4*>(dyn + (oh * s.Wo + ow) * s.C)) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if (oh0 + (w >> 1) <= oh1 && ow0 + (w & 1) <= ow1) add(oh0 + (w >> 1), ow0 + (w & 1), g[w]);
+    } else {
+      for (int oh = oh0; oh <= oh1; ++oh)
+        for (int ow = ow0; ow <= ow1; ++ow)
+          add(oh, ow, __ldg(reinterpret_cast<const float4*>(dyn + (oh * s.Wo + ow) * s.C)));
     }
     *reinterpret_cast<float4*>(dx + (size_t)i * 4) = acc;
     if (dx_relu)

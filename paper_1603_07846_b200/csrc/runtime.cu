@@ -56,6 +56,7 @@ struct sg_net {
   float* row_loss = nullptr;
   float* loss_int = nullptr;
   float* lr_dev = nullptr;
+  float lr_last = -1.f;  // value in lr_dev (the device write is skipped while unchanged)
   int* err = nullptr;
   int32_t* labels = nullptr;
   float* x_stage = nullptr;
@@ -904,8 +905,9 @@ SG_API sg_status sg_net_update(sg_net* n, sg_updater* u, int32_t layer, int64_t 
   SG_CHECK(n->bwd_done[layer] || PL(n).layers[layer].store < 0, SG_ERR_PROTOCOL,
            "protocol error: Update(%s) before its ComputeGradient in this step", PL(n).layers[layer].name.c_str());
   SG_TRY(enter(n, stream));
-  {
-    cudaError_t e = fill_scalar(n->lr_dev, lr_at(u->cfg, step), n->cs);
+  if (lr_at(u->cfg, step) != n->lr_last) {
+    n->lr_last = lr_at(u->cfg, step);
+    cudaError_t e = fill_scalar(n->lr_dev, n->lr_last, n->cs);
     SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "update: %s", cudaGetErrorString(e));
   }
   SG_TRY(update(n, u, layer));
@@ -926,8 +928,9 @@ SG_API sg_status sg_train_one_batch(sg_net* n, sg_updater* u, int64_t step, cons
   const Plan& P = PL(n);
   SG_TRY(enter(n, stream));
   long long l0 = g_kernel_launches;
-  {
-    cudaError_t e = fill_scalar(n->lr_dev, lr_at(u->cfg, step), n->cs);
+  if (lr_at(u->cfg, step) != n->lr_last) {  // fixed / step schedules change it rarely
+    n->lr_last = lr_at(u->cfg, step);
+    cudaError_t e = fill_scalar(n->lr_dev, n->lr_last, n->cs);
     SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "train: %s", cudaGetErrorString(e));
   }
   if (n->graph_on) {

@@ -390,6 +390,9 @@ sg_status step_body(sg_net* n, sg_updater* u) {
   const int nl = (int)P.layers.size();
   for (int i = 0; i < nl; ++i) {
     SG_TRY(collect(n, i));
+    // the input layer reads the caller's x pointer, which changes per call: the
+    // graph path runs it eagerly before the replay instead of capturing it
+    if (i == 0 && n->capturing) continue;
     SG_TRY(forward(n, i));
   }
   for (int i = nl - 1; i >= 0; --i) {
@@ -934,10 +937,8 @@ SG_API sg_status sg_train_one_batch(sg_net* n, sg_updater* u, int64_t step, cons
     SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "train: %s", cudaGetErrorString(e));
   }
   if (n->graph_on) {
-    const LayerPlan& in = P.layers[0];
-    SG_CUDA(cudaMemcpyAsync(n->x_stage, x, (size_t)(in.rows * in.feat) * sizeof(float), cudaMemcpyDeviceToDevice,
-                            n->cs));
-    SG_TRY(set_input(n, n->x_stage, labels));
+    SG_TRY(set_input(n, x, labels));
+    SG_TRY(forward(n, 0));  // input layer on the caller's buffer, then the captured rest of the step
     if (!n->gexec || n->graph_upd != u) {
       if (n->gexec) cudaGraphExecDestroy(n->gexec), n->gexec = nullptr;
       cudaGraph_t g;

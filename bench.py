@@ -159,6 +159,23 @@ class ClockLog:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+
+def grad_sync_bytes(net_cfg, infos, world):
+    """'<layer>.update' -> fp32 gradient bytes the layer's bucket moves per step at N > 1
+    (dim-0 layers only: reduce-scatter of the full gradient + all-gather of the weights, a16/a18).
+    Dim-1 FC slices update owner-locally and move no Param bytes."""
+    out = {}
+    if world < 2:
+        return out
+    w_of = {}
+    for name, fl, by in op_work(net_cfg, infos, world).values():
+        if name.endswith(".update"):
+            w_of[name[:-7]] = by / 20.0
+    for li in infos:
+        if li["kind"] == "conv" or (li["kind"] == "ip" and li["partition_dim"] == 0):
+            out[li["name"] + ".update"] = 4.0 * w_of[li["name"]] * world
+    return out
+
 def init_params(PN, n, net_cfg):
     ucfg = {l["name"]: l for l in net_cfg["layers"]}
     out = {}
@@ -388,6 +405,21 @@ def main():
         if os.path.exists(tp):
             roof["traffic"] = json.load(open(tp)).get(f"{args.config}:{dom['op']}")
 
+    # gradient synchronisation over NVLink (a16 -> a17 -> a18): each dim-0 layer's
+    # update slot times its reduce-scatter -> Updater -> all-gather chain on the
+    # parameter stream (it overlaps the backward of the layers below)
+    grad_sync = None
+    gsb = grad_sync_bytes(net_cfg, info, world)
+    if gsb:
+        upd = [o for o in ops if o["op"] in gsb]
+        t_upd = sum(o["ms"] for o in upd) / 1e3
+        nbytes = sum(gsb.values())
+        grad_sync = {"bytes_per_step": int(nbytes), "layers": len(gsb), "chain_ms": t_upd * 1e3,
+                     "algbw_gbs": nbytes / t_upd / 1e9 if t_upd > 0 else None,
+                     "busbw_gbs": 2.0 * (world - 1) / world * nbytes / t_upd / 1e9 if t_upd > 0 else None,
+                     "peak_gbs": 900.0, "peak_source": "NVLink 5 per direction per GPU (nominal)",
+                     "note": "chain time includes the Updater and NCCL launch/wait; busbw = 2(K-1)/K x bytes / chain time"}
+
     # ---------------- end-to-end through the public host-buffer entry ----------------
     e2e_steps = min(args.steps, 100)
     torch.cuda.synchronize()
@@ -424,7 +456,7 @@ def main():
                            "parallelism": f"dp{world}" if args.config in ("cifar10", "mlp") else f"hybrid{world}",
                            "l2": "flushed (256 MB write) before every timed step",
                            "graph": not args.no_graph, "final_loss": final_loss},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches * args.steps),
+                "roofline": roof, "grad_sync": grad_sync, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches * args.steps),
                 "clocks": clocks,
                 "ops": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in o.items()} for o in ops[:12]],
                 "ops_total_ms": prof_total}

@@ -181,3 +181,18 @@ def test_ae_feature_partition_plan():
                     dh = l["global_shape"][1]
                     assert (l["local_offset"][1], l["local_shape"][1]) == OP.partition_range(dh, K, rank)
             assert sum(1 for l in ls if l["is_connection"]) == 7       # Concat(dim 1) before ip2..ip8
+
+
+@pytest.mark.parametrize("name,K,params", [("cifar10", 2, 89_578),
+                                           ("alexnet", 2, 23_296 + 307_392 + 663_936 + 884_992 + 590_080),
+                                           ("ae_wide", 2, 0)])
+def test_bench_grad_sync_bytes(name, K, params):
+    """bench.py's grad_sync object counts the fp32 bytes of every dim-0 layer's
+    bucket (a16 / a18); dim-1 FC slices (AlexNet fc6-fc8, the all-FC
+    auto-encoder) update owner-locally and move no Param bytes."""
+    import bench
+    net = configs.alexnet(hybrid=True) if name == "alexnet" else configs.get(name)
+    plan = PN.Plan(net, 256, 0, K)
+    got = bench.grad_sync_bytes(net, plan.layers(), K)
+    assert sum(got.values()) == 4 * params
+    assert bench.grad_sync_bytes(net, plan.layers(), 1) == {}

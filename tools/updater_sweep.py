@@ -1,0 +1,115 @@
+"""C5 server-group Updater sweep (BASELINE configs[4]).
+
+One flat fp32 Param of P elements per rank; each step is the paper's
+worker-group -> server-group exchange through the
+C ABI call ``sg_server_sync``: reduce-scatter(sum) of the full gradient,
+the fused SGD-momentum Updater (a17) on the rank's P/K shard, and
+all-gather of the updated weights.
+
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node K \
+        --master-addr 127.0.0.1 --master-port 29511 tools/updater_sweep.py [--iters 20]
+    python tools/updater_sweep.py            # K = 1: the Updater kernel alone
+
+Timing: CUDA events on the stream the call is launched on, W = 3 untimed
+warm-up calls, then ``iters`` calls; barrier + synchronize on both sides;
+max over ranks.  Per P, one JSON line on rank 0:
+  t_us          time of one sg_server_sync
+  algbw_gbs     4P / t (gradient bytes per rank per second)
+  busbw_gbs     nccl-tests convention for RS + AG: 2 (K-1)/K * 4P / t
+  upd_hbm_gbs   (K = 1 only) 20 B per element / t against MEASURED_PEAKS hbm_gbs
+P >= 16M exceed the 126 MB L2 per step (grad + w + v); the smaller sizes may be
+partly L2-resident between iterations (stated in the line as "l2_resident").
+"""
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_1603_07846_b200 import _lib as L  # noqa: E402
+from paper_1603_07846_b200 import net as PN  # noqa: E402
+
+SIZES_M = [1, 2, 4, 8, 16, 32, 61.10084]   # 61,100,840 = the AlexNet-shaped net's Params (C3)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    args = ap.parse_args()
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+        obj = [PN.Cluster.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        cl = PN.Cluster(rank, world, local, obj[0])
+    else:
+        cl = PN.Cluster(0, 1, local)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    cfg = PN.updater_cfg({"base_lr": 0.01, "momentum": 0.9, "weight_decay": 5e-4})
+    stream = torch.cuda.Stream()
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    for pm in SIZES_M:
+        q = 32 * world
+        n = (int(pm * 1e6) + q - 1) // q * q
+        w = torch.randn(n, device="cuda", generator=g) * 0.01
+        if world > 1:
+            dist.barrier()
+        grad0 = torch.randn(n, device="cuda", generator=g)
+        grad = grad0.clone()
+        v = torch.zeros(n // world, device="cuda")
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            for t in range(args.warmup):
+                L.sg_server_sync(cl.h, C.byref(cfg), t, grad.data_ptr(), w.data_ptr(), v.data_ptr(), n,
+                                 C.c_void_p(stream.cuda_stream))
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for t in range(args.iters):
+                # grad is overwritten by the reduce-scatter; its values do not change the cost
+                L.sg_server_sync(cl.h, C.byref(cfg), args.warmup + t, grad.data_ptr(), w.data_ptr(), v.data_ptr(),
+                                 n, C.c_void_p(stream.cuda_stream))
+            ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / args.iters
+        if world > 1:
+            tt = torch.tensor([ms], dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+            dist.barrier()
+        t_s = ms * 1e-3
+        line = {"workload": "updater_sweep", "params": n, "n_gpus": world, "iters": args.iters,
+                "warmup": args.warmup, "t_us": round(ms * 1e3, 2),
+                "algbw_gbs": round(4 * n / t_s / 1e9, 1),
+                "l2_resident": 12 * n < 126e6}
+        if world > 1:
+            line["busbw_gbs"] = round(2 * (world - 1) / world * 4 * n / t_s / 1e9, 1)
+            line["nvlink_peak_gbs"] = 900.0
+        else:
+            a = 20 * n / t_s / 1e9
+            line["upd_hbm_gbs"] = round(a, 1)
+            line["hbm_peak_gbs"] = peaks["hbm_gbs"]
+            line["frac"] = round(a / peaks["hbm_gbs"], 3)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        del w, grad, grad0, v
+        torch.cuda.empty_cache()
+    cl.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

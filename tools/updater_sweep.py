@@ -17,6 +17,9 @@ max over ranks.  Per P, one JSON line on rank 0:
   algbw_gbs     4P / t (gradient bytes per rank per second)
   busbw_gbs     nccl-tests convention for RS + AG: 2 (K-1)/K * 4P / t
   upd_hbm_gbs   (K = 1 only) 20 B per element / t against MEASURED_PEAKS hbm_gbs
+At K > 1 the line also carries ``torch_nccl_t_us``: the same exchange through
+stock ``torch.distributed`` reduce_scatter_tensor / all_gather_into_tensor with
+the update as torch elementwise ops (context, not the product path).
 P >= 16M exceed the 126 MB L2 per step (grad + w + v); the smaller sizes may be
 partly L2-resident between iterations (stated in the line as "l2_resident").
 """
@@ -48,7 +51,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("gloo")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         obj = [PN.Cluster.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         cl = PN.Cluster(rank, world, local, obj[0])
@@ -84,10 +87,30 @@ def main():
             ev1.record(stream)
         torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1) / args.iters
+        # context only: the same exchange as stock torch.distributed collectives plus
+        # the update as torch elementwise ops (5 kernels) on the shard
+        tms = None
         if world > 1:
-            tt = torch.tensor([ms], dtype=torch.float64)
+            shard = n // world
+            ws = w[rank * shard:(rank + 1) * shard]
+            gs = torch.empty(shard, device="cuda")
+            with torch.cuda.stream(stream):
+                for t in range(args.warmup + args.iters):
+                    if t == args.warmup:
+                        torch.cuda.synchronize()
+                        dist.barrier()
+                        ev0.record(stream)
+                    dist.reduce_scatter_tensor(gs, grad)
+                    gs.mul_(1.0 / world).add_(ws, alpha=5e-4)
+                    v.mul_(0.9).sub_(gs, alpha=0.01)
+                    ws.add_(v)
+                    dist.all_gather_into_tensor(w, ws)   # in place, as sg_server_sync
+                ev1.record(stream)
+            torch.cuda.synchronize()
+            tms = ev0.elapsed_time(ev1) / args.iters
+            tt = torch.tensor([ms, tms], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = float(tt.item())
+            ms, tms = float(tt[0].item()), float(tt[1].item())
             dist.barrier()
         t_s = ms * 1e-3
         line = {"workload": "updater_sweep", "params": n, "n_gpus": world, "iters": args.iters,
@@ -97,6 +120,7 @@ def main():
         if world > 1:
             line["busbw_gbs"] = round(2 * (world - 1) / world * 4 * n / t_s / 1e9, 1)
             line["nvlink_peak_gbs"] = 900.0
+            line["torch_nccl_t_us"] = round(tms * 1e3, 2)
         else:
             a = 20 * n / t_s / 1e9
             line["upd_hbm_gbs"] = round(a, 1)

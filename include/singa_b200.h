@@ -355,6 +355,36 @@ SG_API sg_status sg_blob_set(sg_net* n, int32_t layer, int32_t which, const void
 SG_API sg_status sg_server_sync(sg_cluster* c, const sg_updater_cfg* cfg, int64_t step, float* grad_full_dev,
                                 float* w_full_dev, float* v_shard_dev, int64_t n, void* stream);
 
+/* ======================================================================
+ * Fused server sync over NVLink peer memory (C5; the a16 -> a17 -> a18 chain,
+ * P:419-422 "AllReduce" framework, "broadcast back"
+ * Updater) in ONE kernel instead of reduce-scatter -> Updater -> all-gather:
+ * rank r loads every rank's gradient for its shard [r*n/K, (r+1)*n/K) from
+ * the peers' HBM, sums them in ascending rank order, applies the Updater
+ * (s = grad_scale, else 1/K) and stores the new weights into every rank's
+ * weight buffer.  Two flag barriers in peer memory bracket it.
+ *
+ * sg_peer_sync_create: COLLECTIVE (all ranks of the cluster).  Allocates the
+ *   library-owned device buffers grad_full[n], w_full[n] and v_shard[n/K]
+ *   (the caller writes its gradient into grad_full and the initial weights
+ *   into w_full — identical on every rank — before the first step; the
+ *   pointers stay valid until destroy) and exchanges CUDA IPC handles over the
+ *   parameter communicator.  n must be a multiple of 32*K (SG_ERR_PARTITION);
+ *   K <= 8 (SG_ERR_UNSUPPORTED); allocation failure -> SG_ERR_OOM; IPC
+ *   failure -> SG_ERR_CUDA.
+ * sg_peer_sync_step: COLLECTIVE, asynchronous on `stream` (3 kernel launches).
+ *   grad_full is read, not modified.  After the step every rank's w_full holds
+ *   the same updated weights.  A peer that never arrives makes the barrier
+ *   give up after a bounded spin; that is reported by sg_peer_sync_destroy.
+ * sg_peer_sync_destroy: COLLECTIVE; synchronises, frees the buffers; returns
+ *   SG_ERR_CUDA if any barrier timed out.
+ * ====================================================================== */
+typedef struct sg_peer_sync sg_peer_sync;
+SG_API sg_status sg_peer_sync_create(sg_cluster* c, int64_t n, sg_peer_sync** out, float** grad_full_dev,
+                                     float** w_full_dev, float** v_shard_dev);
+SG_API sg_status sg_peer_sync_step(sg_peer_sync* p, const sg_updater_cfg* cfg, int64_t step, void* stream);
+SG_API sg_status sg_peer_sync_destroy(sg_peer_sync* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -191,8 +191,50 @@ def case_server_sync(rank, world, cl):
         print(f"server sync K={world}: weights identical on all ranks, err vs oracle {e:.2e}")
 
 
+def dev_view(ptr, n):
+    """A torch view of a library-owned device buffer (no copy)."""
+    class _A:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 2}
+    return torch.as_tensor(_A(), device="cuda")
+
+
+def case_peer_sync(rank, world, cl):
+    """The fused peer-memory server sync (sg_peer_sync_*) against the oracle:
+    ascending-k gradient sum, then the Updater (oracle/updater.py), two steps."""
+    import ctypes as C
+    n = 32 * world * 1000 + 32 * world * 3      # shard not a multiple of the 256-thread block
+    cfg = PN.updater_cfg({"base_lr": 0.01, "momentum": 0.9, "weight_decay": 5e-4})
+    grad_h, w_h = generate.server_sync_inputs(n, world, rank)
+    h, gp, wp, vp = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+    L.sg_peer_sync_create(cl.h, n, C.byref(h), C.byref(gp), C.byref(wp), C.byref(vp))
+    g, w = dev_view(gp.value, n), dev_view(wp.value, n)
+    w.copy_(torch.from_numpy(w_h))
+    torch.cuda.synchronize()
+    dist.barrier()
+    for t in range(2):
+        g.copy_(torch.from_numpy(generate.server_sync_inputs(n, world, rank)[0] * (t + 1)))
+        torch.cuda.synchronize()
+        L.sg_peer_sync_step(h, C.byref(cfg), t, None)
+        torch.cuda.synchronize()
+    wg = w.cpu().numpy().copy()
+    L.sg_peer_sync_destroy(h)
+    allw = [None] * world
+    dist.all_gather_object(allw, wg)
+    if rank == 0:
+        for other in allw[1:]:
+            assert np.array_equal(other, allw[0])                # every rank holds the same weights
+        cfgd = {"base_lr": 0.01, "momentum": 0.9, "weight_decay": 5e-4, "lr_policy": "fixed"}
+        ww, vv = w_h.astype(np.float64), np.zeros(n)
+        for t in range(2):
+            tot = sum(generate.server_sync_inputs(n, world, r)[0].astype(np.float64) * (t + 1) for r in range(world))
+            ww, vv = OU.sgd_momentum(ww, vv, tot, cfgd, t, 1.0 / world)
+        e = normwise(allw[0], ww)
+        assert e < 1e-6, e
+        print(f"peer sync K={world}: weights identical on all ranks, err vs oracle {e:.2e}")
+
+
 CASES = {"k_invariance": case_k_invariance, "hybrid": case_hybrid, "autoencoder": case_autoencoder,
-         "alexnet": case_alexnet, "server_sync": case_server_sync}
+         "alexnet": case_alexnet, "server_sync": case_server_sync, "peer_sync": case_peer_sync}
 
 if __name__ == "__main__":
     import faulthandler

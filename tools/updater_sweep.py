@@ -19,7 +19,10 @@ max over ranks.  Per P, one JSON line on rank 0:
   upd_hbm_gbs   (K = 1 only) 20 B per element / t against MEASURED_PEAKS hbm_gbs
 At K > 1 the line also carries ``torch_nccl_t_us``: the same exchange through
 stock ``torch.distributed`` reduce_scatter_tensor / all_gather_into_tensor with
-the update as torch elementwise ops (context, not the product path).
+the update as torch elementwise ops (context, not the product path), and
+``fused_p2p_t_us``: the fused peer-memory path ``sg_peer_sync_step`` (one
+kernel reading every rank's gradient shard over NVLink and storing the new
+weights into every rank, between two flag barriers).
 P >= 16M exceed the 126 MB L2 per step (grad + w + v); the smaller sizes may be
 partly L2-resident between iterations (stated in the line as "l2_resident").
 """
@@ -40,6 +43,13 @@ from paper_1603_07846_b200 import _lib as L  # noqa: E402
 from paper_1603_07846_b200 import net as PN  # noqa: E402
 
 SIZES_M = [1, 2, 4, 8, 16, 32, 61.10084]   # 61,100,840 = the AlexNet-shaped net's Params (C3)
+
+
+def dev_view(ptr, n):
+    """A torch view of a library-owned device buffer (no copy)."""
+    class _A:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 2}
+    return torch.as_tensor(_A(), device="cuda")
 
 
 def main():
@@ -112,6 +122,29 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms, tms = float(tt[0].item()), float(tt[1].item())
             dist.barrier()
+        # the fused peer-memory path (sg_peer_sync_*: one kernel, P2P loads / stores)
+        fms = None
+        if world > 1:
+            h, gp, wp, vp = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+            L.sg_peer_sync_create(cl.h, n, C.byref(h), C.byref(gp), C.byref(wp), C.byref(vp))
+            dev_view(gp.value, n).copy_(grad0)
+            dev_view(wp.value, n).fill_(0.01)
+            torch.cuda.synchronize()
+            dist.barrier()
+            with torch.cuda.stream(stream):
+                for t in range(args.warmup + args.iters):
+                    if t == args.warmup:
+                        torch.cuda.synchronize()
+                        dist.barrier()
+                        ev0.record(stream)
+                    L.sg_peer_sync_step(h, C.byref(cfg), t, C.c_void_p(stream.cuda_stream))
+                ev1.record(stream)
+            torch.cuda.synchronize()
+            fms = ev0.elapsed_time(ev1) / args.iters
+            L.sg_peer_sync_destroy(h)
+            tt = torch.tensor([fms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            fms = float(tt[0].item())
         t_s = ms * 1e-3
         line = {"workload": "updater_sweep", "params": n, "n_gpus": world, "iters": args.iters,
                 "warmup": args.warmup, "t_us": round(ms * 1e3, 2),
@@ -121,6 +154,8 @@ def main():
             line["busbw_gbs"] = round(2 * (world - 1) / world * 4 * n / t_s / 1e9, 1)
             line["nvlink_peak_gbs"] = 900.0
             line["torch_nccl_t_us"] = round(tms * 1e3, 2)
+            line["fused_p2p_t_us"] = round(fms * 1e3, 2)
+            line["fused_p2p_busbw_gbs"] = round(2 * (world - 1) / world * 4 * n / (fms * 1e-3) / 1e9, 1)
         else:
             a = 20 * n / t_s / 1e9
             line["upd_hbm_gbs"] = round(a, 1)

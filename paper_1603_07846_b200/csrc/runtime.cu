@@ -1165,6 +1165,9 @@ constexpr int kMaxPeers = 8;
 #ifndef SG_P2P_UNROLL
 #define SG_P2P_UNROLL 4
 #endif
+#ifndef SG_P2P_PULL
+#define SG_P2P_PULL 0
+#endif
 #ifndef SG_P2P_BLOCKS_PER_SM
 #define SG_P2P_BLOCKS_PER_SM 8
 #endif
@@ -1258,7 +1261,33 @@ __global__ void __launch_bounds__(256) peer_sync_kernel(PeerPtrs p, float* __res
         wp[e] = __fadd_rn(wp[e], vp[e]);
       }
       v4[i] = vv[u];
+#if SG_P2P_PULL
+      reinterpret_cast<float4*>(p.w[rank] + base)[i] = ww[u];
+#else
       for (int k = 0; k < world; ++k) reinterpret_cast<float4*>(p.w[k] + base)[i] = ww[u];
+#endif
+    }
+  }
+}
+// Pull variant (SG_P2P_PULL): after the middle barrier every rank copies the
+// other ranks' updated weight shards into its own buffer by P2P loads, so
+// NVLink carries loads only.
+template <int U>
+__global__ void __launch_bounds__(256) peer_pull_kernel(PeerPtrs p, long long shard, int rank, int world) {
+  const long long n4 = shard >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int k = 1; k < world; ++k) {
+    const int src = (rank + k) % world;
+    const float4* from = reinterpret_cast<const float4*>(p.w[src] + (long long)src * shard);
+    float4* to = reinterpret_cast<float4*>(p.w[rank] + (long long)src * shard);
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
+      float4 t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * stride < n4) t[u] = from[i0 + u * stride];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (i0 + u * stride < n4) to[i0 + u * stride] = t[u];
     }
   }
 }
@@ -1357,6 +1386,9 @@ SG_API sg_status sg_peer_sync_step(sg_peer_sync* p, const sg_updater_cfg* cfg, i
   peer_sync_kernel<kUnroll><<<blocks, 256, 0, st>>>(p->peers, p->v, shard, c->rank, c->world, lr_at(*cfg, step),
                                            cfg->momentum, cfg->weight_decay, s);
   if (c->world > 1) peer_barrier_kernel<<<1, 32, 0, st>>>(p->peers, c->rank, c->world, ++p->epoch, p->err);
+#if SG_P2P_PULL
+  if (c->world > 1) peer_pull_kernel<kUnroll><<<blocks, 256, 0, st>>>(p->peers, shard, c->rank, c->world);
+#endif
   SG_CUDA(cudaGetLastError());
   return SG_OK;
 }

@@ -255,3 +255,39 @@ def test_updater_vs_oracle_and_sharding():
     w3 = dev(w)
     lib.sg_op_sgd_momentum(ptr(w3), ptr(gd), ptr(dev(v)), n, 0.0, 0.9, 5e-4, 1.0, None)
     assert np.array_equal(host(w3), w)
+
+
+def test_peer_sync_single_rank_vs_oracle_and_errors():
+    """sg_peer_sync_* at K = 1 (no peers, no barriers): the fused exchange kernel
+    is the Updater on the whole Param, s = grad_scale; bit-identical
+    to sg_op_sgd_momentum (same FMA order) and within 1e-6 of the oracle.
+    n not a multiple of 32 -> SG_ERR_PARTITION (header contract)."""
+    from paper_1603_07846_b200 import net as PN
+    cl = PN.Cluster(0, 1, 0)
+    n = 32 * 4099
+    w, g = r32(n, scale=0.05), r32(n, scale=0.01)
+    cfgd = {"base_lr": 0.01, "momentum": 0.9, "weight_decay": 5e-4, "lr_policy": "fixed"}
+    cfg = PN.updater_cfg(cfgd, grad_scale=0.5)
+    h, gp, wp, vp = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+    lib.sg_peer_sync_create(cl.h, n, C.byref(h), C.byref(gp), C.byref(wp), C.byref(vp))
+
+    class _A:
+        def __init__(self, p):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (p, False), "version": 2}
+    gd, wd_ = torch.as_tensor(_A(gp.value), device="cuda"), torch.as_tensor(_A(wp.value), device="cuda")
+    gd.copy_(torch.from_numpy(g))
+    wd_.copy_(torch.from_numpy(w))
+    w2, v2, g2 = dev(w), dev(np.zeros(n, np.float32)), dev(g)
+    rw, rv = f64(w), np.zeros(n)
+    for t in range(3):
+        lib.sg_peer_sync_step(h, C.byref(cfg), t, None)
+        lib.sg_op_sgd_momentum(ptr(w2), ptr(g2), ptr(v2), n, 0.01, 0.9, 5e-4, 0.5, None)
+        rw, rv = U.sgd_momentum(rw, rv, f64(g), cfgd, t, 0.5)
+    torch.cuda.synchronize()
+    got = wd_.cpu().numpy().copy()
+    assert np.array_equal(got, host(w2))
+    assert normwise(got, rw) < 1e-6
+    lib.sg_peer_sync_destroy(h)
+    with pytest.raises(lib.SingaError):
+        lib.sg_peer_sync_create(cl.h, n + 1, C.byref(h), C.byref(gp), C.byref(wp), C.byref(vp))
+    cl.close()

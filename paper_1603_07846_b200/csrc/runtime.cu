@@ -1165,6 +1165,9 @@ constexpr int kMaxPeers = 8;
 #ifndef SG_P2P_UNROLL
 #define SG_P2P_UNROLL 4
 #endif
+#ifndef SG_P2P_STREAMING
+#define SG_P2P_STREAMING 0
+#endif
 #ifndef SG_P2P_PULL
 #define SG_P2P_PULL 0
 #endif
@@ -1237,7 +1240,11 @@ __global__ void __launch_bounds__(256) peer_sync_kernel(PeerPtrs p, float* __res
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const long long i = i0 + u * stride;
+#if SG_P2P_STREAMING
+        if (i < n4) gk[u] = __ldcs(reinterpret_cast<const float4*>(p.g[k] + base) + i);
+#else
         if (i < n4) gk[u] = reinterpret_cast<const float4*>(p.g[k] + base)[i];
+#endif
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1264,7 +1271,11 @@ __global__ void __launch_bounds__(256) peer_sync_kernel(PeerPtrs p, float* __res
 #if SG_P2P_PULL
       reinterpret_cast<float4*>(p.w[rank] + base)[i] = ww[u];
 #else
+#if SG_P2P_STREAMING
+      for (int k = 0; k < world; ++k) __stcs(reinterpret_cast<float4*>(p.w[k] + base) + i, ww[u]);
+#else
       for (int k = 0; k < world; ++k) reinterpret_cast<float4*>(p.w[k] + base)[i] = ww[u];
+#endif
 #endif
     }
   }

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SG_ABI_VERSION 1
+#define SG_ABI_VERSION 2
 #define SG_API __attribute__((visibility("default")))
 
 typedef int32_t sg_status;
@@ -158,6 +158,13 @@ typedef struct {
   int32_t nworker_groups, workers_per_group; /* must be 1, world_size */
   int32_t nserver_groups, servers_per_group; /* must be 1, world_size (servers co-located) */
   uint8_t nccl_id[128];                      /* from sg_get_unique_id on rank 0, broadcast by the caller */
+  /* Test switch (0 = off): at world_size 1, still create a one-rank NCCL
+   * communicator and plan every net as partitioned — connection layers
+   * (Concat / Slice) inserted, dim-0 gradient buckets sharded (reduce-scatter
+   * -> Updater on the shard -> all-gather), dim-1 inner products column-split —
+   * so the whole collective data plane runs (and is checked against the oracle)
+   * on a single GPU.  Ignored (always on) for world_size > 1. */
+  int32_t exercise_collectives;
 } sg_cluster_cfg;
 /* rank 0 only; the caller broadcasts the 128 bytes to all ranks (process boundary). */
 SG_API sg_status sg_get_unique_id(uint8_t out[128]);
@@ -226,6 +233,13 @@ typedef struct {
    * rank blocks [K][rows][ld]; nblocks = K then (else 1). */
   int64_t ld;
   int32_t nblocks;
+  /* Reading A19: 1 when the layer's output blob (tf32_data) / the
+   * gradient w.r.t. its output (tf32_grad) is read as a tensor-core operand; its
+   * producing kernel then stores it rounded to TF32 (round to nearest, ties
+   * away from zero: 13 low mantissa bits zero).  Parameters: the Updater keeps
+   * an fp32 master copy and writes a TF32-rounded working copy of every weight
+   * matrix (biases stay fp32); sg_param_get_value returns the master. */
+  int32_t tf32_data, tf32_grad;
 } sg_layer_info;
 SG_API sg_status sg_plan_num_layers(const sg_plan* p, int32_t* n);
 SG_API sg_status sg_plan_layer_info(const sg_plan* p, int32_t i, sg_layer_info* out); /* execution order */
@@ -271,6 +285,10 @@ SG_API sg_status sg_param_set_value(sg_net* n, int32_t p, const float* global_ho
 SG_API sg_status sg_param_get_value(sg_net* n, int32_t p, float* global_host);
 SG_API sg_status sg_param_get_grad(sg_net* n, int32_t p, float* global_host);
 SG_API sg_status sg_param_get_history(sg_net* n, int32_t p, float* global_host); /* momentum v, COLLECTIVE */
+/* The working copy the GEMMs read (reading A19): the master weight matrix
+ * rounded to TF32 (round to nearest, ties away from zero), biases equal to the
+ * master.  COLLECTIVE for world > 1 (dim-1 Params are gathered). */
+SG_API sg_status sg_param_get_working(sg_net* n, int32_t p, float* global_host);
 
 /* ---- Updater ---- */
 typedef struct sg_updater sg_updater;

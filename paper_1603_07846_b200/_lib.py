@@ -46,7 +46,7 @@ class ClusterCfg(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world_size", C.c_int32), ("device", C.c_int32),
                 ("nworker_groups", C.c_int32), ("workers_per_group", C.c_int32),
                 ("nserver_groups", C.c_int32), ("servers_per_group", C.c_int32),
-                ("nccl_id", C.c_uint8 * 128)]
+                ("nccl_id", C.c_uint8 * 128), ("exercise_collectives", C.c_int32)]
 
 
 class LayerCfg(C.Structure):
@@ -65,7 +65,7 @@ class LayerInfo(C.Structure):
     _fields_ = [("name", C.c_char * 64), ("kind", C.c_int32), ("partition_dim", C.c_int32),
                 ("is_connection", C.c_int32), ("src", C.c_int32),
                 ("global_shape", C.c_int64 * 4), ("local_shape", C.c_int64 * 4), ("local_offset", C.c_int64 * 4),
-                ("ld", C.c_int64), ("nblocks", C.c_int32)]
+                ("ld", C.c_int64), ("nblocks", C.c_int32), ("tf32_data", C.c_int32), ("tf32_grad", C.c_int32)]
 
 
 class ParamInfo(C.Structure):
@@ -127,6 +127,7 @@ SIGS = {
     "sg_param_get_value": [P, I32, P],
     "sg_param_get_grad": [P, I32, P],
     "sg_param_get_history": [P, I32, P],
+    "sg_param_get_working": [P, I32, P],
     "sg_updater_create": [P, C.POINTER(UpdaterCfg), C.POINTER(P)],
     "sg_updater_destroy": [P],
     "sg_train_one_batch": [P, P, I64, P, P, P, P],

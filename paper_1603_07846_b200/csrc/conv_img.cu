@@ -63,7 +63,7 @@ struct ImgConvArgs {
   int Hp, Wp, Ho, Wo;  // padded source, output
   int N;               // output channels (multiple of 32)
   int layer_c, layer_co;  // the layer's C / Co (weight tensor strides)
-  int ntiles, img_rows, relu, dgrad;
+  int ntiles, img_rows, relu, dgrad;  // relu: epilogue flags EPI_RELU | EPI_RN (ops.h)
   int Hrows;  // padded image rows staged (img_rows = Hrows * Wp rounded up to 8)
   int wsplit;  // filter bank staged one K block at a time
 };
@@ -77,7 +77,7 @@ __device__ __forceinline__ uint32_t ksw(int row, int chunk) {  // K-major SW128 
 // tile are issued before one wait, the bias is read once.
 template <int NB>
 __device__ __forceinline__ void img_epilogue(uint32_t tmem, int ntiles, int warp, int lane, int Wp, int Ho, int Wo,
-                                             float* outn, const float* bias, int relu) {
+                                             float* outn, const float* bias, int flags) {
   float bv[NB];
 #pragma unroll
   for (int c = 0; c < NB; ++c) bv[c] = bias ? __ldg(bias + c) : 0.f;
@@ -96,8 +96,8 @@ __device__ __forceinline__ void img_epilogue(uint32_t tmem, int ntiles, int warp
       float4 o = make_float4(__uint_as_float(r[j / 16][j % 16]) + bv[j], __uint_as_float(r[j / 16][j % 16 + 1]) + bv[j + 1],
                              __uint_as_float(r[j / 16][j % 16 + 2]) + bv[j + 2],
                              __uint_as_float(r[j / 16][j % 16 + 3]) + bv[j + 3]);
-      if (relu) o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
-      dst[j / 4] = o;
+      if (flags & EPI_RELU) o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
+      dst[j / 4] = tf32_rna4_if(o, flags & EPI_RN);
     }
   }
 }
@@ -340,7 +340,7 @@ struct Img4Args {
   CUtensorMap w_map;    // W {4, Co, T} (strides T*16, 16), box {4, Co, S}, no swizzle
   const float* bias;
   float* out;
-  int pad, R, S, SP, Wp, Ho, Wo, Hrows, img_rows, ntiles, relu;
+  int pad, R, S, SP, Wp, Ho, Wo, Hrows, img_rows, ntiles, relu;  // relu: epilogue flags
 };
 
 template <int NB>
@@ -764,7 +764,8 @@ cudaError_t conv_img_fwd(const ConvShape& s, const float* x, const float* W, con
   return run_img(a, smem, s.N, st);
 }
 
-cudaError_t conv_img_dgrad(const ConvShape& s, const float* dy, const float* W, float* dx, cudaStream_t st) {
+cudaError_t conv_img_dgrad(const ConvShape& s, const float* dy, const float* W, float* dx, cudaStream_t st,
+                           int flags) {
   ImgConvArgs a;
   size_t smem;
   if (!plan_img(s, true, &a, &smem)) return cudaErrorInvalidValue;
@@ -772,7 +773,7 @@ cudaError_t conv_img_dgrad(const ConvShape& s, const float* dy, const float* W, 
   a.wt = W;
   a.bias = nullptr;
   a.out = dx;
-  a.relu = 0;
+  a.relu = flags & EPI_RN;
   if (!encode_maps(s, &a)) return cudaErrorInvalidValue;
   return run_img(a, smem, s.N, st);
 }

@@ -747,6 +747,7 @@ struct EpiArgs {
   const float* bias;  // indexed by n (bias_on_m = 0) or by m
   int bias_on_m;
   int relu;
+  int rn;  // round the stored outputs to TF32 (reading A19: the output is a GEMM operand)
   int mvalid, xrow;
   float* xout;
   float* ws;
@@ -823,6 +824,7 @@ __device__ __forceinline__ void epi_store4(const EpiArgs& e, int row, int col0, 
     }
     if (e.bias) o += e.bias_on_m ? e.bias[row] : e.bias[col];
     if (e.relu) o = fmaxf(o, 0.f);
+    if (e.rn) o = tf32_rna(o);
     if (e.trans)
       *out_at(e, col, row, e.mvalid) = o;
     else
@@ -859,7 +861,7 @@ __device__ __forceinline__ void epi_store16(const EpiArgs& e, int row, int col0,
         o.z = fmaxf(o.z, 0.f);
         o.w = fmaxf(o.w, 0.f);
       }
-      *reinterpret_cast<float4*>(dst + i) = o;
+      *reinterpret_cast<float4*>(dst + i) = tf32_rna4_if(o, e.rn);
     }
     return;
   }
@@ -870,6 +872,7 @@ __device__ __forceinline__ void epi_store16(const EpiArgs& e, int row, int col0,
     float o = v[i];
     if (e.bias) o += e.bias_on_m ? e.bias[row] : e.bias[col];
     if (e.relu) o = fmaxf(o, 0.f);
+    if (e.rn) o = tf32_rna(o);
     if (e.trans)
       *out_at(e, col, row, e.mvalid) = o;
     else

@@ -22,23 +22,23 @@ inline unsigned blocks_for(long long n, int per_block) {
 
 // ------------------------------------------------------------ elementwise --
 template <class F>
-__global__ void map1_kernel(const float* __restrict__ x, float* __restrict__ y, long long n, F f) {
+__global__ void map1_kernel(const float* __restrict__ x, float* __restrict__ y, long long n, F f, int rn) {
   pdl_entry();
   long long n4 = n >> 2;
   const float4* x4 = reinterpret_cast<const float4*>(x);
   float4* y4 = reinterpret_cast<float4*>(y);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
     float4 v = x4[i];
-    y4[i] = make_float4(f(v.x), f(v.y), f(v.z), f(v.w));
+    y4[i] = tf32_rna4_if(make_float4(f(v.x), f(v.y), f(v.z), f(v.w)), rn);
   }
   for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    y[i] = f(x[i]);
+    y[i] = rn ? tf32_rna(f(x[i])) : f(x[i]);
 }
 
 template <class F>
 __global__ void map2_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ y,
-                            long long n, F f) {
+                            long long n, F f, int rn) {
   pdl_entry();
   long long n4 = n >> 2;
   const float4* a4 = reinterpret_cast<const float4*>(a);
@@ -46,11 +46,11 @@ __global__ void map2_kernel(const float* __restrict__ a, const float* __restrict
   float4* y4 = reinterpret_cast<float4*>(y);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
     float4 u = a4[i], v = b4[i];
-    y4[i] = make_float4(f(u.x, v.x), f(u.y, v.y), f(u.z, v.z), f(u.w, v.w));
+    y4[i] = tf32_rna4_if(make_float4(f(u.x, v.x), f(u.y, v.y), f(u.z, v.z), f(u.w, v.w)), rn);
   }
   for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    y[i] = f(a[i], b[i]);
+    y[i] = rn ? tf32_rna(f(a[i], b[i])) : f(a[i], b[i]);
 }
 
 struct ReluF {
@@ -73,16 +73,16 @@ struct SigB {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <class F>
-cudaError_t launch_map1(const float* x, float* y, long long n, F f, cudaStream_t st) {
+cudaError_t launch_map1(const float* x, float* y, long long n, F f, cudaStream_t st, int rn) {
   if (n <= 0) return cudaSuccess;
   if (!aligned16(x) || !aligned16(y)) return cudaErrorMisalignedAddress;
-  return launch_k(map1_kernel<F>, blocks_for(n / 4 + 1, 256), 256, 0, st, x, y, n, f);
+  return launch_k(map1_kernel<F>, blocks_for(n / 4 + 1, 256), 256, 0, st, x, y, n, f, rn);
 }
 template <class F>
-cudaError_t launch_map2(const float* a, const float* b, float* y, long long n, F f, cudaStream_t st) {
+cudaError_t launch_map2(const float* a, const float* b, float* y, long long n, F f, cudaStream_t st, int rn) {
   if (n <= 0) return cudaSuccess;
   if (!aligned16(a) || !aligned16(b) || !aligned16(y)) return cudaErrorMisalignedAddress;
-  return launch_k(map2_kernel<F>, blocks_for(n / 4 + 1, 256), 256, 0, st, a, b, y, n, f);
+  return launch_k(map2_kernel<F>, blocks_for(n / 4 + 1, 256), 256, 0, st, a, b, y, n, f, rn);
 }
 
 // Optional ReLU fusion helpers (bit-identical to ReluF / ReluB).
@@ -109,7 +109,7 @@ PoolK pool_k(const PoolShape& s) {
 // the argmax is stored as the uint8 offset (h - h0)*k + (w - w0); first maximum
 // in (h, w) scan order (strict >), reading A5.
 __global__ void maxpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* __restrict__ y,
-                                   uint8_t* __restrict__ arg, float* __restrict__ relu_out) {
+                                   uint8_t* __restrict__ arg, float* __restrict__ relu_out, int rn) {
   pdl_entry();
   const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
@@ -133,9 +133,9 @@ __global__ void maxpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* 
         if (v.w > m[3]) { m[3] = v.w; a[3] = off; }
       }
     const float4 o = make_float4(m[0], m[1], m[2], m[3]);
-    *reinterpret_cast<float4*>(y + (size_t)i * 4) = o;
+    *reinterpret_cast<float4*>(y + (size_t)i * 4) = tf32_rna4_if(o, rn & RN_OUT);
     *reinterpret_cast<uchar4*>(arg + (size_t)i * 4) = make_uchar4(a[0], a[1], a[2], a[3]);
-    if (relu_out) *reinterpret_cast<float4*>(relu_out + (size_t)i * 4) = relu4(o);
+    if (relu_out) *reinterpret_cast<float4*>(relu_out + (size_t)i * 4) = tf32_rna4_if(relu4(o), rn & RN_AUX);
   }
 }
 
@@ -149,7 +149,7 @@ __device__ __forceinline__ void pool_windows(int hp, int k, int Ho, const FastDi
 // of every window whose argmax is this element, windows in ascending (oh, ow).
 __global__ void maxpool_bwd_kernel(PoolK P, const float* __restrict__ dy, const uint8_t* __restrict__ arg,
                                    float* __restrict__ dx, const float* __restrict__ relu_y,
-                                   float* __restrict__ dx_relu) {
+                                   float* __restrict__ dx_relu, int rn) {
   pdl_entry();
   const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
@@ -193,15 +193,15 @@ __global__ void maxpool_bwd_kernel(PoolK P, const float* __restrict__ dy, const 
           add(oh, ow, __ldg(reinterpret_cast<const uchar4*>(arg + o)), __ldg(reinterpret_cast<const float4*>(dy + o)));
         }
     }
-    *reinterpret_cast<float4*>(dx + (size_t)i * 4) = acc;
+    *reinterpret_cast<float4*>(dx + (size_t)i * 4) = tf32_rna4_if(acc, rn & RN_OUT);
     if (dx_relu)
       *reinterpret_cast<float4*>(dx_relu + (size_t)i * 4) =
-          mask4(acc, __ldg(reinterpret_cast<const float4*>(relu_y) + i));
+          tf32_rna4_if(mask4(acc, __ldg(reinterpret_cast<const float4*>(relu_y) + i)), rn & RN_AUX);
   }
 }
 
 __global__ void avgpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* __restrict__ y,
-                                   float* __restrict__ relu_out) {
+                                   float* __restrict__ relu_out, int rn) {
   pdl_entry();
   const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
@@ -222,13 +222,13 @@ __global__ void avgpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* 
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
     const float4 o = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-    *reinterpret_cast<float4*>(y + (size_t)i * 4) = o;
-    if (relu_out) *reinterpret_cast<float4*>(relu_out + (size_t)i * 4) = relu4(o);
+    *reinterpret_cast<float4*>(y + (size_t)i * 4) = tf32_rna4_if(o, rn & RN_OUT);
+    if (relu_out) *reinterpret_cast<float4*>(relu_out + (size_t)i * 4) = tf32_rna4_if(relu4(o), rn & RN_AUX);
   }
 }
 
 __global__ void avgpool_bwd_kernel(PoolK P, const float* __restrict__ dy, float* __restrict__ dx,
-                                   const float* __restrict__ relu_y, float* __restrict__ dx_relu) {
+                                   const float* __restrict__ relu_y, float* __restrict__ dx_relu, int rn) {
   pdl_entry();
   const PoolShape& s = P.s;
   const int C4 = s.C >> 2;
@@ -266,10 +266,10 @@ __global__ void avgpool_bwd_kernel(PoolK P, const float* __restrict__ dy, float*
         for (int ow = ow0; ow <= ow1; ++ow)
           add(oh, ow, __ldg(reinterpret_cast<const float4*>(dyn + (oh * s.Wo + ow) * s.C)));
     }
-    *reinterpret_cast<float4*>(dx + (size_t)i * 4) = acc;
+    *reinterpret_cast<float4*>(dx + (size_t)i * 4) = tf32_rna4_if(acc, rn & RN_OUT);
     if (dx_relu)
       *reinterpret_cast<float4*>(dx_relu + (size_t)i * 4) =
-          mask4(acc, __ldg(reinterpret_cast<const float4*>(relu_y) + i));
+          tf32_rna4_if(mask4(acc, __ldg(reinterpret_cast<const float4*>(relu_y) + i)), rn & RN_AUX);
   }
 }
 
@@ -329,7 +329,8 @@ __device__ __forceinline__ void lrn_apply(const LrnShape& s, int C4, float4 v, i
   o4 = make_float4(o[0], o[1], o[2], o[3]);
 }
 
-__global__ void lrn_fwd_kernel(LrnK K, const float* __restrict__ x, float* __restrict__ y, float* __restrict__ scale) {
+__global__ void lrn_fwd_kernel(LrnK K, const float* __restrict__ x, float* __restrict__ y, float* __restrict__ scale,
+                               int rn) {
   pdl_entry();
   const int valid = (int)(K.s.pixels * K.C4);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K.total; i += gridDim.x * blockDim.x) {
@@ -340,7 +341,7 @@ __global__ void lrn_fwd_kernel(LrnK K, const float* __restrict__ x, float* __res
     lrn_apply(K.s, K.C4, v, c4, sc4, o4);
     if (in) {
       reinterpret_cast<float4*>(scale)[i] = sc4;
-      reinterpret_cast<float4*>(y)[i] = o4;
+      reinterpret_cast<float4*>(y)[i] = tf32_rna4_if(o4, rn);
     }
   }
 }
@@ -395,7 +396,7 @@ __device__ __forceinline__ float4 avgpool_at(const PoolK& P, const float* __rest
 template <bool MAX>
 __global__ void pool_lrn_fwd_kernel(PoolK P, LrnK K, const float* __restrict__ x, float* __restrict__ py,
                                     uint8_t* __restrict__ arg, float* __restrict__ relu_out, float* __restrict__ ly,
-                                    float* __restrict__ scale) {
+                                    float* __restrict__ scale, int rn) {
   pdl_entry();
   const int valid = (int)(K.s.pixels * K.C4);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K.total; i += gridDim.x * blockDim.x) {
@@ -416,14 +417,14 @@ __global__ void pool_lrn_fwd_kernel(PoolK P, LrnK K, const float* __restrict__ x
     lrn_apply(K.s, K.C4, v, c4, sc4, o4);
     if (in) {
       reinterpret_cast<float4*>(scale)[i] = sc4;
-      reinterpret_cast<float4*>(ly)[i] = o4;
+      reinterpret_cast<float4*>(ly)[i] = tf32_rna4_if(o4, rn);
     }
   }
 }
 
 __global__ void lrn_bwd_kernel(LrnK K, const float* __restrict__ x, const float* __restrict__ y,
                                const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ dx,
-                               const float* __restrict__ relu_y, float* __restrict__ dx_relu) {
+                               const float* __restrict__ relu_y, float* __restrict__ dx_relu, int rn) {
   pdl_entry();
   const LrnShape& s = K.s;
   const int half = s.n / 2;
@@ -450,15 +451,17 @@ __global__ void lrn_bwd_kernel(LrnK K, const float* __restrict__ x, const float*
     }
     if (in) {
       const float4 d = make_float4(o[0], o[1], o[2], o[3]);
-      reinterpret_cast<float4*>(dx)[i] = d;
-      if (dx_relu) reinterpret_cast<float4*>(dx_relu)[i] = mask4(d, __ldg(reinterpret_cast<const float4*>(relu_y) + i));
+      reinterpret_cast<float4*>(dx)[i] = tf32_rna4_if(d, rn & RN_OUT);
+      if (dx_relu)
+        reinterpret_cast<float4*>(dx_relu)[i] =
+            tf32_rna4_if(mask4(d, __ldg(reinterpret_cast<const float4*>(relu_y) + i)), rn & RN_AUX);
     }
   }
 }
 
 // Generic channel counts: thread per element.
 __global__ void lrn_fwd_generic_kernel(LrnShape s, const float* __restrict__ x, float* __restrict__ y,
-                                       float* __restrict__ scale) {
+                                       float* __restrict__ scale, int rn) {
   pdl_entry();
   long long total = s.pixels * s.C;
   const int half = s.n / 2;
@@ -471,14 +474,15 @@ __global__ void lrn_fwd_generic_kernel(LrnShape s, const float* __restrict__ x, 
     for (int cc = lo; cc <= hi; ++cc) acc += px[cc] * px[cc];
     float sc = s.k + an * acc;
     scale[i] = sc;
-    y[i] = x[i] * pow_neg(sc, s.beta);
+    const float o = x[i] * pow_neg(sc, s.beta);
+    y[i] = rn ? tf32_rna(o) : o;
   }
 }
 
 __global__ void lrn_bwd_generic_kernel(LrnShape s, const float* __restrict__ x, const float* __restrict__ y,
                                        const float* __restrict__ scale, const float* __restrict__ dy,
                                        float* __restrict__ dx, const float* __restrict__ relu_y,
-                                       float* __restrict__ dx_relu) {
+                                       float* __restrict__ dx_relu, int rn) {
   pdl_entry();
   long long total = s.pixels * s.C;
   const int half = s.n / 2;
@@ -490,8 +494,11 @@ __global__ void lrn_bwd_generic_kernel(LrnShape s, const float* __restrict__ x, 
     float acc = 0.f;
     for (int cc = lo; cc <= hi; ++cc) acc += dy[base + cc] * y[base + cc] / scale[base + cc];
     const float d = dy[i] * pow_neg(scale[i], s.beta) - coef * x[i] * acc;
-    dx[i] = d;
-    if (dx_relu) dx_relu[i] = relu_y[i] > 0.f ? d : 0.f;
+    dx[i] = (rn & RN_OUT) ? tf32_rna(d) : d;
+    if (dx_relu) {
+      const float dr = relu_y[i] > 0.f ? d : 0.f;
+      dx_relu[i] = (rn & RN_AUX) ? tf32_rna(dr) : dr;
+    }
   }
 }
 
@@ -516,7 +523,7 @@ __device__ __forceinline__ float* vat_w(const View2D& v, int i, int j) { return 
 // Warp per row: max, sum of exp, loss, dz.  Lane-strided sums then a fixed
 // xor-butterfly: deterministic.
 __global__ void softmax_ce_kernel(View2D z, const int32_t* __restrict__ labels, float* __restrict__ row_loss,
-                                  View2D dz, float inv_nloc, int* err) {
+                                  View2D dz, float inv_nloc, int* err, int rn) {
   pdl_entry();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -536,13 +543,14 @@ __global__ void softmax_ce_kernel(View2D z, const int32_t* __restrict__ labels, 
     float inv = 1.f / sum;
     for (int j = lane; j < z.cols; j += 32) {
       float p = expf(*vat(z, r, j) - m) * inv;
-      *vat_w(dz, r, j) = (p - (j == y ? 1.f : 0.f)) * inv_nloc;
+      const float d = (p - (j == y ? 1.f : 0.f)) * inv_nloc;
+      *vat_w(dz, r, j) = rn ? tf32_rna(d) : d;
     }
     if (lane == 0) row_loss[r] = bad ? 0.f : (m + logf(sum)) - *vat(z, r, y);
   }
 }
 
-__global__ void euclidean_kernel(View2D u, View2D v, float* __restrict__ row_loss, View2D du, float inv_nloc) {
+__global__ void euclidean_kernel(View2D u, View2D v, float* __restrict__ row_loss, View2D du, float inv_nloc, int rn) {
   pdl_entry();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -551,7 +559,7 @@ __global__ void euclidean_kernel(View2D u, View2D v, float* __restrict__ row_los
     for (int j = lane; j < u.cols; j += 32) {
       float d = *vat(u, r, j) - *vat(v, r, j);
       acc += d * d;
-      *vat_w(du, r, j) = d * inv_nloc;
+      *vat_w(du, r, j) = rn ? tf32_rna(d * inv_nloc) : d * inv_nloc;
     }
     acc = warp_sum(acc);
     if (lane == 0) row_loss[r] = 0.5f * acc;
@@ -585,8 +593,13 @@ __device__ __forceinline__ void sgd1(float& w, float g, float& v, float lr, floa
   w = __fadd_rn(w, v);
 }
 
-__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ v, long long n,
-                           const float* lr_dev, float lr_scale, float lr_val, float mu, float wd, float s) {
+// Master copy w and history v updated in place; when wk != nullptr the
+// working copy the GEMMs read is written too: wk[i] = TF32-RN(w[i]) for
+// i < rn_end (weights, tensor-core operands, reading A19), wk[i] = w[i] beyond
+// (biases, added in fp32 by the epilogues).
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ v,
+                           float* __restrict__ wk, long long rn_end, long long n, const float* lr_dev, float lr_scale,
+                           float lr_val, float mu, float wd, float s) {
   pdl_entry();
   const float lr = lr_dev ? lr_dev[0] * lr_scale : lr_val;
   long long n4 = n >> 2;
@@ -601,6 +614,15 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, f
     sgd1(ww.w, gg.w, vv.w, lr, mu, wd, s);
     w4[i] = ww;
     v4[i] = vv;
+    if (wk) {
+      const long long e = 4 * i;
+      float4 k = ww;
+      if (e < rn_end) k.x = tf32_rna(k.x);
+      if (e + 1 < rn_end) k.y = tf32_rna(k.y);
+      if (e + 2 < rn_end) k.z = tf32_rna(k.z);
+      if (e + 3 < rn_end) k.w = tf32_rna(k.w);
+      reinterpret_cast<float4*>(wk)[i] = k;
+    }
   }
   for (long long i = (n4 << 2) + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -608,32 +630,42 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, f
     sgd1(ww, g[i], vv, lr, mu, wd, s);
     w[i] = ww;
     v[i] = vv;
+    if (wk) wk[i] = i < rn_end ? tf32_rna(ww) : ww;
   }
 }
 
 // ------------------------------------------------------------- input layer --
 __global__ void pad_channels_kernel(const float* __restrict__ x, float* __restrict__ y, long long pixels, int cin,
-                                    int cout) {
+                                    int cout, int rn) {
   pdl_entry();
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < pixels; p += (long long)gridDim.x * blockDim.x) {
     const float* src = x + p * cin;
     float* dst = y + p * cout;
     if (cout == 4 && cin == 3) {
-      *reinterpret_cast<float4*>(dst) = make_float4(src[0], src[1], src[2], 0.f);
+      *reinterpret_cast<float4*>(dst) = tf32_rna4_if(make_float4(src[0], src[1], src[2], 0.f), rn);
     } else {
-      for (int c = 0; c < cout; ++c) dst[c] = c < cin ? src[c] : 0.f;
+      for (int c = 0; c < cout; ++c) dst[c] = c < cin ? (rn ? tf32_rna(src[c]) : src[c]) : 0.f;
     }
   }
 }
 
 __global__ void copy2d_kernel(const float* __restrict__ src, long long sld, float* __restrict__ dst, long long dld,
-                              int rows, int cols) {
+                              int rows, int cols, int rn) {
   pdl_entry();
   long long total = (long long)rows * cols;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     int r = (int)(i / cols), c = (int)(i % cols);
-    dst[(long long)r * dld + c] = src[(long long)r * sld + c];
+    const float v = src[(long long)r * sld + c];
+    dst[(long long)r * dld + c] = rn ? tf32_rna(v) : v;
   }
+}
+
+// In-place TF32 rounding of a GEMM operand that arrived by a reduction
+// collective (sum of rounded partials, reading A19).
+__global__ void round_tf32_kernel(float* __restrict__ p, long long n) {
+  pdl_entry();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = tf32_rna(p[i]);
 }
 
 __global__ void relu2d_kernel(const float* __restrict__ x, float* __restrict__ y, int rows, int cols, long long ld) {
@@ -647,13 +679,17 @@ __global__ void relu2d_kernel(const float* __restrict__ x, float* __restrict__ y
 
 }  // namespace
 
-cudaError_t relu_fwd(const float* x, float* y, long long n, cudaStream_t st) { return launch_map1(x, y, n, ReluF{}, st); }
-cudaError_t relu_bwd(const float* y, const float* dy, float* dx, long long n, cudaStream_t st) {
-  return launch_map2(y, dy, dx, n, ReluB{}, st);
+cudaError_t relu_fwd(const float* x, float* y, long long n, cudaStream_t st, int rn) {
+  return launch_map1(x, y, n, ReluF{}, st, rn);
 }
-cudaError_t sigmoid_fwd(const float* x, float* y, long long n, cudaStream_t st) { return launch_map1(x, y, n, SigF{}, st); }
-cudaError_t sigmoid_bwd(const float* y, const float* dy, float* dx, long long n, cudaStream_t st) {
-  return launch_map2(y, dy, dx, n, SigB{}, st);
+cudaError_t relu_bwd(const float* y, const float* dy, float* dx, long long n, cudaStream_t st, int rn) {
+  return launch_map2(y, dy, dx, n, ReluB{}, st, rn);
+}
+cudaError_t sigmoid_fwd(const float* x, float* y, long long n, cudaStream_t st, int rn) {
+  return launch_map1(x, y, n, SigF{}, st, rn);
+}
+cudaError_t sigmoid_bwd(const float* y, const float* dy, float* dx, long long n, cudaStream_t st, int rn) {
+  return launch_map2(y, dy, dx, n, SigB{}, st, rn);
 }
 cudaError_t relu_fwd2d(const float* x, float* y, int rows, int cols, long long ld, cudaStream_t st) {
   return launch_k(relu2d_kernel, blocks_for((long long)rows * cols, 256), 256, 0, st, x, y, rows, cols, ld);
@@ -661,28 +697,29 @@ cudaError_t relu_fwd2d(const float* x, float* y, int rows, int cols, long long l
 
 static bool fits32(long long n) { return n < (1LL << 31); }
 
-cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* arg, cudaStream_t st, float* relu_out) {
+cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* arg, cudaStream_t st, float* relu_out,
+                        int rn) {
   const long long n = (long long)s.N * s.Ho * s.Wo * s.C / 4;
   if (s.C % 4 || s.k * s.k > 256 || !fits32(n * 4) || !fits32((long long)s.N * s.H * s.W * s.C))
     return cudaErrorInvalidValue;
-  return launch_k(maxpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y, arg, relu_out);
+  return launch_k(maxpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y, arg, relu_out, rn);
 }
 cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg, float* dx, cudaStream_t st,
-                        const float* relu_y, float* dx_relu) {
+                        const float* relu_y, float* dx_relu, int rn) {
   const long long n = (long long)s.N * s.H * s.W * s.C / 4;
   if (s.C % 4 || !fits32(n * 4)) return cudaErrorInvalidValue;
-  return launch_k(maxpool_bwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), dy, arg, dx, relu_y, dx_relu);
+  return launch_k(maxpool_bwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), dy, arg, dx, relu_y, dx_relu, rn);
 }
-cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st, float* relu_out) {
+cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st, float* relu_out, int rn) {
   const long long n = (long long)s.N * s.Ho * s.Wo * s.C / 4;
   if (s.C % 4 || !fits32(n * 4) || !fits32((long long)s.N * s.H * s.W * s.C)) return cudaErrorInvalidValue;
-  return launch_k(avgpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y, relu_out);
+  return launch_k(avgpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y, relu_out, rn);
 }
 cudaError_t avgpool_bwd(const PoolShape& s, const float* dy, float* dx, cudaStream_t st, const float* relu_y,
-                        float* dx_relu) {
+                        float* dx_relu, int rn) {
   const long long n = (long long)s.N * s.H * s.W * s.C / 4;
   if (s.C % 4 || !fits32(n * 4)) return cudaErrorInvalidValue;
-  return launch_k(avgpool_bwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), dy, dx, relu_y, dx_relu);
+  return launch_k(avgpool_bwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), dy, dx, relu_y, dx_relu, rn);
 }
 cudaError_t pool_argmax_expand(const PoolShape& s, const uint8_t* arg, int32_t* out, cudaStream_t st) {
   return launch_k(argmax_expand_kernel, blocks_for((long long)s.N * s.Ho * s.Wo * s.C, 256), 256, 0, st, s, arg, out);
@@ -701,22 +738,23 @@ static bool lrn_fast(const LrnShape& s, std::initializer_list<const void*> ptrs,
   k->total = (int)((s.pixels * C4 + 31) / 32 * 32);
   return true;
 }
-cudaError_t lrn_fwd(const LrnShape& s, const float* x, float* y, float* scale, cudaStream_t st) {
+cudaError_t lrn_fwd(const LrnShape& s, const float* x, float* y, float* scale, cudaStream_t st, int rn) {
   LrnK k;
-  if (lrn_fast(s, {x, y, scale}, &k)) return launch_k(lrn_fwd_kernel, blocks_for(k.total, 256), 256, 0, st, k, x, y, scale);
-  return launch_k(lrn_fwd_generic_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale);
+  if (lrn_fast(s, {x, y, scale}, &k))
+    return launch_k(lrn_fwd_kernel, blocks_for(k.total, 256), 256, 0, st, k, x, y, scale, rn);
+  return launch_k(lrn_fwd_generic_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale, rn);
 }
 cudaError_t lrn_bwd(const LrnShape& s, const float* x, const float* y, const float* scale, const float* dy, float* dx,
-                    cudaStream_t st, const float* relu_y, float* dx_relu) {
+                    cudaStream_t st, const float* relu_y, float* dx_relu, int rn) {
   LrnK k;
   if (lrn_fast(s, {x, y, scale, dy, dx, dx_relu ? relu_y : x, dx_relu ? dx_relu : dx}, &k))
-    return launch_k(lrn_bwd_kernel, blocks_for(k.total, 256), 256, 0, st, k, x, y, scale, dy, dx, relu_y, dx_relu);
+    return launch_k(lrn_bwd_kernel, blocks_for(k.total, 256), 256, 0, st, k, x, y, scale, dy, dx, relu_y, dx_relu, rn);
   return launch_k(lrn_bwd_generic_kernel, blocks_for(s.pixels * s.C, 256), 256, 0, st, s, x, y, scale, dy, dx, relu_y,
-                  dx_relu);
+                  dx_relu, rn);
 }
 
 cudaError_t pool_lrn_fwd(const PoolShape& ps, bool max_pool, const float* x, float* py, uint8_t* arg, float* relu_out,
-                         const LrnShape& ls, float* ly, float* scale, cudaStream_t st) {
+                         const LrnShape& ls, float* ly, float* scale, cudaStream_t st, int rn) {
   LrnK k;
   const long long n4 = (long long)ps.N * ps.Ho * ps.Wo * ps.C / 4;
   if (ps.C % 4 || ls.C != ps.C || ls.pixels != (long long)ps.N * ps.Ho * ps.Wo || !fits32(n4 * 4) ||
@@ -725,9 +763,9 @@ cudaError_t pool_lrn_fwd(const PoolShape& ps, bool max_pool, const float* x, flo
     return cudaErrorInvalidValue;
   if (max_pool)
     return launch_k(pool_lrn_fwd_kernel<true>, blocks_for(k.total, 256), 256, 0, st, pool_k(ps), k, x, py, arg,
-                    relu_out, ly, scale);
+                    relu_out, ly, scale, rn);
   return launch_k(pool_lrn_fwd_kernel<false>, blocks_for(k.total, 256), 256, 0, st, pool_k(ps), k, x, py, arg,
-                  relu_out, ly, scale);
+                  relu_out, ly, scale, rn);
 }
 bool pool_lrn_fusable(const PoolShape& ps, const LrnShape& ls) {
   LrnK k;
@@ -737,13 +775,13 @@ bool pool_lrn_fusable(const PoolShape& ps, const LrnShape& ls) {
 }
 
 cudaError_t softmax_ce(View2D z, const int32_t* labels, float* row_loss, View2D dz, float inv_nloc, int* err,
-                       cudaStream_t st) {
+                       cudaStream_t st, int rn) {
   if (z.rows <= 0) return cudaSuccess;
-  return launch_k(softmax_ce_kernel, (z.rows + 7) / 8, 256, 0, st, z, labels, row_loss, dz, inv_nloc, err);
+  return launch_k(softmax_ce_kernel, (z.rows + 7) / 8, 256, 0, st, z, labels, row_loss, dz, inv_nloc, err, rn);
 }
-cudaError_t euclidean(View2D u, View2D v, float* row_loss, View2D du, float inv_nloc, cudaStream_t st) {
+cudaError_t euclidean(View2D u, View2D v, float* row_loss, View2D du, float inv_nloc, cudaStream_t st, int rn) {
   if (u.rows <= 0) return cudaSuccess;
-  return launch_k(euclidean_kernel, (u.rows + 7) / 8, 256, 0, st, u, v, row_loss, du, inv_nloc);
+  return launch_k(euclidean_kernel, (u.rows + 7) / 8, 256, 0, st, u, v, row_loss, du, inv_nloc, rn);
 }
 cudaError_t sum_scaled(const float* v, int n, float scale, float* out, int* err, cudaStream_t st) {
   return launch_k(sum_scaled_kernel, 1, 1024, 0, st, v, n, scale, out, err);
@@ -753,21 +791,29 @@ cudaError_t sgd_momentum(float* w, const float* g, float* v, long long n, float 
                          cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (!aligned16(w) || !aligned16(g) || !aligned16(v)) return cudaErrorMisalignedAddress;
-  return launch_k(sgd_kernel, blocks_for(n / 4 + 1, 256), 256, 0, st, w, g, v, n, nullptr, 1.f, lr, mu, wd, s);
+  return launch_k(sgd_kernel, blocks_for(n / 4 + 1, 256), 256, 0, st, w, g, v, (float*)nullptr, 0LL, n,
+                  (const float*)nullptr, 1.f, lr, mu, wd, s);
 }
 cudaError_t sgd_momentum_dev(float* w, const float* g, float* v, long long n, const float* lr_dev, float lr_scale,
-                             float mu, float wd, float s, cudaStream_t st) {
+                             float mu, float wd, float s, cudaStream_t st, float* wk, long long rn_end) {
   if (n <= 0) return cudaSuccess;
-  if (!aligned16(w) || !aligned16(g) || !aligned16(v)) return cudaErrorMisalignedAddress;
-  return launch_k(sgd_kernel, blocks_for(n / 4 + 1, 256), 256, 0, st, w, g, v, n, lr_dev, lr_scale, 0.f, mu, wd, s);
+  if (!aligned16(w) || !aligned16(g) || !aligned16(v) || (wk && !aligned16(wk))) return cudaErrorMisalignedAddress;
+  return launch_k(sgd_kernel, blocks_for(n / 4 + 1, 256), 256, 0, st, w, g, v, wk, rn_end, n, lr_dev, lr_scale, 0.f,
+                  mu, wd, s);
 }
 
-cudaError_t pad_channels(const float* x, float* y, long long pixels, int cin, int cout, cudaStream_t st) {
+cudaError_t pad_channels(const float* x, float* y, long long pixels, int cin, int cout, cudaStream_t st, int rn) {
   if (cout == 4 && !aligned16(y)) return cudaErrorMisalignedAddress;
-  return launch_k(pad_channels_kernel, blocks_for(pixels, 256), 256, 0, st, x, y, pixels, cin, cout);
+  return launch_k(pad_channels_kernel, blocks_for(pixels, 256), 256, 0, st, x, y, pixels, cin, cout, rn);
 }
-cudaError_t copy2d(const float* src, long long sld, float* dst, long long dld, int rows, int cols, cudaStream_t st) {
-  return launch_k(copy2d_kernel, blocks_for((long long)rows * cols, 256), 256, 0, st, src, sld, dst, dld, rows, cols);
+cudaError_t copy2d(const float* src, long long sld, float* dst, long long dld, int rows, int cols, cudaStream_t st,
+                   int rn) {
+  return launch_k(copy2d_kernel, blocks_for((long long)rows * cols, 256), 256, 0, st, src, sld, dst, dld, rows, cols,
+                  rn);
+}
+cudaError_t round_tf32(float* p, long long n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  return launch_k(round_tf32_kernel, blocks_for(n, 256), 256, 0, st, p, n);
 }
 
 }  // namespace sg

@@ -100,6 +100,7 @@ __device__ __forceinline__ void reduce_store(const EpiArgs& e, int m, int n, int
   }
   if (e.bias) t += e.bias_on_m ? e.bias[m] : e.bias[n];
   if (e.relu) t = fmaxf(t, 0.f);
+  if (e.rn) t = tf32_rna(t);
   if (e.trans)
     *out_at(e, n, m, e.mvalid) = t;
   else
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(1024) splitk_reduce_kernel(const float* __rest
       o.z = fmaxf(o.z, 0.f);
       o.w = fmaxf(o.w, 0.f);
     }
-    *reinterpret_cast<float4*>(e.p + (long long)m * e.ld + n) = o;
+    *reinterpret_cast<float4*>(e.p + (long long)m * e.ld + n) = tf32_rna4_if(o, e.rn);
     return;
   }
 #pragma unroll
@@ -363,7 +364,8 @@ MatView mv(const float* p, int rows, int cols, long long ld, long long bs = 0, i
 }
 MatView mv(const View2D& d) { return mv(d.p, d.rows, d.cols, d.ld, d.bs, d.cb); }
 
-EpiArgs epi_plain(float* p, long long ld, int trans, const float* bias, int bias_on_m, int relu, int mvalid) {
+// `flags`: EPI_RELU | EPI_RN (ops.h).
+EpiArgs epi_plain(float* p, long long ld, int trans, const float* bias, int bias_on_m, int flags, int mvalid) {
   EpiArgs e{};
   e.p = p;
   e.ld = ld;
@@ -372,14 +374,15 @@ EpiArgs epi_plain(float* p, long long ld, int trans, const float* bias, int bias
   e.trans = trans;
   e.bias = bias;
   e.bias_on_m = bias_on_m;
-  e.relu = relu;
+  e.relu = (flags & EPI_RELU) ? 1 : 0;
+  e.rn = (flags & EPI_RN) ? 1 : 0;
   e.mvalid = mvalid;
   e.xrow = -1;
   e.xout = nullptr;
   return e;
 }
-EpiArgs epi_view(const View2D& d, const float* bias, int relu) {
-  EpiArgs e = epi_plain(d.p, d.ld, 0, bias, 0, relu, d.rows);
+EpiArgs epi_view(const View2D& d, const float* bias, int flags) {
+  EpiArgs e = epi_plain(d.p, d.ld, 0, bias, 0, flags, d.rows);
   e.bs = d.bs;
   e.cb = d.cb > 0 ? d.cb : d.cols;
   if (e.cb >= d.cols) e.cb = 1 << 30;
@@ -507,6 +510,7 @@ __device__ __forceinline__ void epi_store1(const EpiArgs& e, int row, int col, f
   }
   if (e.bias) o += e.bias_on_m ? e.bias[row] : e.bias[col];
   if (e.relu) o = fmaxf(o, 0.f);
+  if (e.rn) o = tf32_rna(o);
   if (e.trans)
     *out_at(e, col, row, e.mvalid) = o;
   else
@@ -583,11 +587,11 @@ cudaError_t run_small(const MatView& a, int ta, const MatView& b, int tb, int on
 }
 
 // ------------------------------------------------------------ convolution ----
-cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const float* b, float* y, int relu,
+cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const float* b, float* y, int flags,
                      Workspace ws, cudaStream_t st) {
   const int M = s.N * s.Ho * s.Wo, N = s.Co, K = s.R * s.S * s.C;
-  if (conv_img_fwd_ok(s) && aligned16p(x) && aligned16p(W) && aligned16p(y)) return conv_img_fwd(s, x, W, b, y, relu, st);
-  const EpiArgs e = epi_plain(y, s.Co, 0, b, 0, relu, M);
+  if (conv_img_fwd_ok(s) && aligned16p(x) && aligned16p(W) && aligned16p(y)) return conv_img_fwd(s, x, W, b, y, flags, st);
+  const EpiArgs e = epi_plain(y, s.Co, 0, b, 0, flags, M);
   if (tma_on(0) && s.C % 32 == 0 && aligned16p(x)) {
     bool ok = true;
     TmaIm2col a{};
@@ -620,10 +624,11 @@ cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const f
 }
 
 cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* W, float* dx, Workspace ws,
-                       cudaStream_t st) {
+                       cudaStream_t st, int flags) {
   const int M = s.N * s.H * s.W, N = s.C, K = s.R * s.S * s.Co;
-  if (conv_img_dgrad_ok(s) && aligned16p(dy) && aligned16p(W) && aligned16p(dx)) return conv_img_dgrad(s, dy, W, dx, st);
-  const EpiArgs e = epi_plain(dx, s.C, 0, nullptr, 0, 0, M);
+  if (conv_img_dgrad_ok(s) && aligned16p(dy) && aligned16p(W) && aligned16p(dx))
+    return conv_img_dgrad(s, dy, W, dx, st, flags);
+  const EpiArgs e = epi_plain(dx, s.C, 0, nullptr, 0, flags, M);
   if (tma_on(1) && s.st == 1 && s.Co % 32 == 0 && s.C % 32 == 0 && aligned16p(dy) && aligned16p(W)) {
     bool ok = true;
     const int lo = s.pad - (s.R - 1);
@@ -705,9 +710,9 @@ cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, floa
 }
 
 // ---------------------------------------------------------- inner product ----
-cudaError_t ip_fwd(View2D x, const float* W, int dv, int dh, const float* b, View2D y, int relu, Workspace ws,
+cudaError_t ip_fwd(View2D x, const float* W, int dv, int dh, const float* b, View2D y, int flags, Workspace ws,
                    cudaStream_t st) {
-  const EpiArgs e = epi_view(y, b, relu);
+  const EpiArgs e = epi_view(y, b, flags);
   if (small_ok(x.rows, dh, dv)) return run_small(mv(x), 0, mv(W, dv, dh, dh), 0, -1, x.rows, dh, dv, e, st);
   if (tma_on(3)) {
     bool ok = true;
@@ -721,8 +726,9 @@ cudaError_t ip_fwd(View2D x, const float* W, int dv, int dh, const float* b, Vie
   return run_gemm(a, bw, x.rows, dh, dv, e, ws, st);
 }
 
-cudaError_t ip_dgrad(View2D dy, const float* W, int dv, int dh, View2D dx, Workspace ws, cudaStream_t st) {
-  const EpiArgs e = epi_view(dx, nullptr, 0);
+cudaError_t ip_dgrad(View2D dy, const float* W, int dv, int dh, View2D dx, Workspace ws, cudaStream_t st,
+                     int flags) {
+  const EpiArgs e = epi_view(dx, nullptr, flags);
   // op(B)(k = h, n = v) = W(v, h)
   if (small_ok(dy.rows, dv, dh)) return run_small(mv(dy), 0, mv(W, dv, dh, dh), 1, -1, dy.rows, dv, dh, e, st);
   if (tma_on(3)) {

@@ -3,7 +3,7 @@
 //
 // PAPER.md §5.3: partition_dim 0 slices a layer's feature matrix by
 // row (data parallelism), 1 by column (model parallelism); connection layers
-// are inserted between differently-partitioned layers.  Here (K > 1):
+// are inserted between differently-partitioned layers.  Here (K > 1, or a forced partitioned plan at K = 1):
 //   Concat(rows)  row-split -> replicated    ncclAllGather   (fwd) / ReduceScatter (bwd)
 //   Concat(cols)  column-split -> replicated  ncclAllGather   (fwd) / ReduceScatter (bwd)
 //   Slice         column-split -> row-split   all-to-all      (fwd) / all-to-all    (bwd)
@@ -99,7 +99,7 @@ sg_status add_connection(Plan& P, int target) {
 
 }  // namespace
 
-sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out) {
+sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out, bool force_dist) {
   SG_CHECK(cfg && out, SG_ERR_INVALID_ARG, "plan: null argument");
   SG_CHECK(world >= 1 && rank >= 0 && rank < world, SG_ERR_INVALID_ARG, "plan: rank %d world %d", rank, world);
   SG_CHECK(cfg->nlayers >= 1 && cfg->layers, SG_ERR_CONFIG, "config error: empty net");
@@ -111,7 +111,9 @@ sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out) {
   P.world = world;
   P.batch = cfg->batch;
   P.num_classes = cfg->num_classes;
+  P.dist = world > 1 || force_dist;
   const int K = world;
+  const bool dist = P.dist;
 
   // resolve partition dims (inherit from the source layer; first defaults to 0)
   std::vector<int> dims(cfg->nlayers);
@@ -125,7 +127,7 @@ sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out) {
     SG_CHECK(l.partition_dim >= -1 && l.partition_dim <= 1, SG_ERR_CONFIG, "config error: %s partition_dim %d",
              l.name, l.partition_dim);
     if (l.partition_dim >= 0) cur = l.partition_dim;
-    dims[i] = (K == 1) ? 0 : cur;
+    dims[i] = dist ? cur : 0;
   }
 
   // input layer
@@ -172,8 +174,8 @@ sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out) {
              u.name);
     SG_CHECK(is_loss || i != cfg->nlayers - 1, SG_ERR_CONFIG, "config error: the last layer (%s) must be a loss",
              u.name);
-    // bring the source into the state this layer needs (K > 1 only)
-    if (K > 1) {
+    // bring the source into the state this layer needs (partitioned plans only)
+    if (dist) {
       int st = P.layers.back().state;
       int need = -1;
       switch (kind) {
@@ -314,7 +316,7 @@ sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out) {
         } else {
           L.kin = s.feat;
         }
-        if (d == 1 && K > 1) {
+        if (d == 1 && dist) {
           if (dh % K) SG_FAIL(SG_ERR_PARTITION, "partition error: %s d_h=%lld not divisible by K=%d", u.name,
                               (long long)dh, K);
           L.state = ST_COLS;
@@ -346,9 +348,9 @@ sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out) {
         SG_CHECK(!in.image && s.feat == in.feat, SG_ERR_DIMENSION,
                  "dimension error: Euclidean %s compares %lld features with the %lld-feature input", u.name,
                  (long long)s.feat, (long long)in.feat);
-        SG_CHECK(d == 0 || in.state == ST_FULL || K == 1, SG_ERR_CONFIG,
+        SG_CHECK(d == 0 || in.state == ST_FULL || !dist, SG_ERR_CONFIG,
                  "config error: a partition_dim 1 Euclidean loss (%s) needs a replicated input", u.name);
-        SG_CHECK(d == 1 || K == 1 || in.state == ST_ROWS, SG_ERR_CONFIG,
+        SG_CHECK(d == 1 || !dist || in.state == ST_ROWS, SG_ERR_CONFIG,
                  "config error: a partition_dim 0 Euclidean loss (%s) needs a row-split input", u.name);
         L.image = false;
         L.feat = 1;
@@ -394,7 +396,7 @@ sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out) {
     b.name = L.name + "/b";
     W.layer = b.layer = li;
     b.is_bias = 1;
-    const bool split = (L.kind == SG_INNER_PRODUCT && L.pdim == 1 && K > 1);
+    const bool split = (L.kind == SG_INNER_PRODUCT && L.pdim == 1 && dist);
     W.split_dim = b.split_dim = split ? 1 : -1;
     if (L.kind == SG_CONV) {
       W.rows = L.c;
@@ -421,7 +423,7 @@ sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out) {
     StorePlan S;
     S.layer = li;
     S.size = W.isize + b.isize;
-    S.sharded = !split && K > 1;
+    S.sharded = !split && dist;
     const int64_t unit = 32LL * K;
     S.padded = (S.size + unit - 1) / unit * unit;
     if (!split) {
@@ -438,6 +440,24 @@ sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out) {
     P.params.push_back(b);
     P.stores.push_back(S);
     if (S.bucket >= 0) P.buckets.push_back(L.store);
+  }
+
+  // Tensor-core operands (reading A19): the input of every conv / inner
+  // product and the gradient w.r.t. its output.  An all-gather (Concat
+  // forward) moves its source's values unchanged, so the source's producer
+  // rounds; the loss gradient reaches a dim-1 producer through the Slice's
+  // all-to-all unchanged, so the loss kernel rounds.  (A Concat's backward is
+  // a reduce-scatter sum: the runtime rounds its result in place.)
+  const int nl = (int)P.layers.size();
+  for (LayerPlan& L : P.layers)
+    if (L.kind == SG_CONV || L.kind == SG_INNER_PRODUCT) {
+      P.layers[L.src].rn_data = true;
+      L.rn_grad = true;
+    }
+  for (int i = nl - 1; i >= 0; --i) {
+    LayerPlan& L = P.layers[i];
+    if (L.kind == SG_CONCAT && L.rn_data) P.layers[L.src].rn_data = true;
+    if (L.kind == SG_SLICE && P.layers[L.src].rn_grad) L.rn_grad = true;
   }
   *out = std::move(P);
   return SG_OK;
@@ -498,6 +518,8 @@ SG_API sg_status sg_plan_layer_info(const sg_plan* p, int32_t i, sg_layer_info* 
   o->local_offset[0] = L.row_off;
   o->ld = L.ld;
   o->nblocks = L.nblocks;
+  o->tf32_data = L.rn_data ? 1 : 0;
+  o->tf32_grad = L.rn_grad ? 1 : 0;
   return SG_OK;
 }
 

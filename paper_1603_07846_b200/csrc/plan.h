@@ -34,6 +34,10 @@ struct LayerPlan {
   int64_t kin = 0, nout = 0;
   int64_t rmap_real = 0, rmap_pad = 0;  // logical input row i -> (i/pad)*real + i%pad (if pad > 0)
   int pW = -1, pb = -1, store = -1;
+  // Reading A19: the layer's output blob (rn_data) / the gradient w.r.t. its
+  // output (rn_grad) is read as a tensor-core operand, so its producer stores
+  // it rounded to TF32 (round to nearest).
+  bool rn_data = false, rn_grad = false;
   int64_t blob_floats() const { return (int64_t)nblocks * rows * ld; }
 };
 
@@ -58,6 +62,9 @@ struct StorePlan {
 
 struct Plan {
   int rank = 0, world = 1, batch = 0, num_classes = 0;
+  // partitioned data plane: world > 1, or forced at world 1 (sg_cluster_cfg
+  // exercise_collectives: connection layers and sharded buckets on one rank)
+  bool dist = false;
   std::vector<LayerPlan> layers;  // execution order; layers[0] = input
   std::vector<ParamPlan> params;
   std::vector<StorePlan> stores;
@@ -68,7 +75,8 @@ struct Plan {
 };
 
 // Builds the plan; on failure returns the sg_status and sets the error message.
-sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out);
+// force_dist: plan as partitioned even at world 1 (test switch, see Plan::dist).
+sg_status build_plan(const sg_net_cfg* cfg, int rank, int world, Plan* out, bool force_dist = false);
 
 }  // namespace sg
 

@@ -37,6 +37,7 @@ size_t colsum_ws_floats(int M, int N);
 
 struct sg_cluster {
   int rank = 0, world = 1, device = 0;
+  bool force = false;             // exercise_collectives at world 1 (partitioned plans, 1-rank NCCL)
   ncclComm_t comm_act = nullptr;  // activations / connection layers (compute stream)
   ncclComm_t comm_par = nullptr;  // parameter sync (parameter stream)
 };
@@ -52,7 +53,10 @@ struct sg_net {
   cudaStream_t cs = nullptr, ps = nullptr;
   std::vector<float*> data, grad, scale;
   std::vector<uint8_t*> mask;
-  std::vector<float*> sw, sgr, sv;  // per store: weights (full), gradients (full), history (shard)
+  // per store: working copy of the weights (full; what the GEMMs read: TF32-RN
+  // weights, fp32 biases), gradients (full), fp32 master weights and history
+  // (the rank's shard when the store is sharded, else full)
+  std::vector<float*> sw, sgr, sm, sv;
   float* row_loss = nullptr;
   float* loss_int = nullptr;
   float* lr_dev = nullptr;
@@ -60,6 +64,7 @@ struct sg_net {
   int* err = nullptr;
   int32_t* labels = nullptr;
   float* x_stage = nullptr;
+  float* x_exact = nullptr;  // unrounded copy of the input blob (a Euclidean loss's target when the input is rounded)
   const float* x_src = nullptr;
   sg::Workspace ws;
   std::vector<cudaEvent_t> ev_grad, ev_upd;
@@ -116,6 +121,15 @@ sg_status dalloc_t(sg_net* n, size_t count, T** out) {
   return SG_OK;
 }
 
+// TF32 round to nearest, ties away from zero (= tf32_rna in sg_common.cuh)
+float tf32_rna_host(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  u = (u + 0x1000u) & 0xFFFFE000u;
+  memcpy(&x, &u, 4);
+  return x;
+}
+
 float lr_at(const sg_updater_cfg& c, int64_t step) {
   if (c.lr_policy == 1 && c.step_size > 0) return (float)(c.base_lr * std::pow((double)c.gamma, (double)(step / c.step_size)));
   return c.base_lr;
@@ -162,6 +176,16 @@ void prof_mark(sg_net* n, int slot, int end, cudaStream_t st) {
   n->pused[slot] = 1;
 }
 
+// Epilogue flags of a conv / inner-product layer: the fused ReLU, and TF32
+// rounding when the blob it writes (its own, or the fused ReLU's) is a GEMM
+// operand (reading A19).
+int epi_flags(const sg_net* n, int i) {
+  const Plan& P = PL(n);
+  const int j = n->relu_of[i];
+  const bool rn = (j >= 0 ? P.layers[j] : P.layers[i]).rn_data;
+  return (j >= 0 ? EPI_RELU : 0) | (rn ? EPI_RN : 0);
+}
+
 // ---- ComputeFeature ----
 sg_status forward_impl(sg_net* n, int i);
 sg_status forward(sg_net* n, int i) {
@@ -182,44 +206,46 @@ sg_status forward_impl(sg_net* n, int i) {
     case SG_INPUT:
       SG_CHECK(n->x_src, SG_ERR_SEQUENCE, "sequence error: no input set (sg_net_set_input)");
       if (L.image)
-        SG_LCH(pad_channels(n->x_src, n->data[i], L.rows * L.h * L.w, L.c_real, L.c, st));
+        SG_LCH(pad_channels(n->x_src, n->data[i], L.rows * L.h * L.w, L.c_real, L.c, st, L.rn_data));
       else
-        SG_LCH(copy2d(n->x_src, L.feat, n->data[i], L.ld, (int)L.rows, (int)L.feat, st));
+        SG_LCH(copy2d(n->x_src, L.feat, n->data[i], L.ld, (int)L.rows, (int)L.feat, st, L.rn_data));
+      if (n->x_exact) SG_LCH(copy2d(n->x_src, L.feat, n->x_exact, L.ld, (int)L.rows, (int)L.feat, st, 0));
       break;
     case SG_CONV:
-      SG_LCH(conv_fwd(conv_shape(L, *S), n->data[L.src], W, b, n->data[i], n->relu_of[i] >= 0, n->ws, st));
+      SG_LCH(conv_fwd(conv_shape(L, *S), n->data[L.src], W, b, n->data[i], epi_flags(n, i), n->ws, st));
       break;
     case SG_POOL_MAX:
     case SG_POOL_AVG: {
       float* relu_out = n->relu_after[i] >= 0 ? n->data[n->relu_after[i]] : nullptr;
       const int k = n->lrn_after[i];
+      const int rn = (L.rn_data ? RN_OUT : 0) | (n->relu_after[i] >= 0 && P.layers[n->relu_after[i]].rn_data ? RN_AUX : 0);
       if (k >= 0) {  // pooling [-> ReLU] -> LRN in one kernel
         const LayerPlan& Lk = P.layers[k];
         SG_LCH(pool_lrn_fwd(pool_shape(L, *S), L.kind == SG_POOL_MAX, n->data[L.src], n->data[i],
                             L.kind == SG_POOL_MAX ? n->mask[i] : nullptr, relu_out,
                             LrnShape{Lk.rows * Lk.h * Lk.w, Lk.c, Lk.lrn_size, Lk.alpha, Lk.beta, Lk.k}, n->data[k],
-                            n->scale[k], st));
+                            n->scale[k], st, Lk.rn_data));
       } else if (L.kind == SG_POOL_MAX) {
-        SG_LCH(maxpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], n->mask[i], st, relu_out));
+        SG_LCH(maxpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], n->mask[i], st, relu_out, rn));
       } else {
-        SG_LCH(avgpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], st, relu_out));
+        SG_LCH(avgpool_fwd(pool_shape(L, *S), n->data[L.src], n->data[i], st, relu_out, rn));
       }
       break;
     }
     case SG_LRN:
       if (!n->lrn_fused[i])
         SG_LCH(lrn_fwd(LrnShape{L.rows * L.h * L.w, L.c, L.lrn_size, L.alpha, L.beta, L.k}, n->data[L.src],
-                       n->data[i], n->scale[i], st));
+                       n->data[i], n->scale[i], st, L.rn_data));
       break;
     case SG_RELU:
-      if (!n->fused_away[i]) SG_LCH(relu_fwd(n->data[L.src], n->data[i], L.blob_floats(), st));
+      if (!n->fused_away[i]) SG_LCH(relu_fwd(n->data[L.src], n->data[i], L.blob_floats(), st, L.rn_data));
       break;
     case SG_SIGMOID:
-      SG_LCH(sigmoid_fwd(n->data[L.src], n->data[i], L.blob_floats(), st));
+      SG_LCH(sigmoid_fwd(n->data[L.src], n->data[i], L.blob_floats(), st, L.rn_data));
       break;
     case SG_INNER_PRODUCT:
       SG_LCH(ip_fwd(feat_view(*S, n->data[L.src], L.kin), W, (int)L.kin, (int)L.nout, b,
-                    plain(n->data[i], (int)L.rows, (int)L.nout, L.ld), n->relu_of[i] >= 0, n->ws, st));
+                    plain(n->data[i], (int)L.rows, (int)L.nout, L.ld), epi_flags(n, i), n->ws, st));
       break;
     case SG_CONCAT:
       SG_NCCL(ncclAllGather(n->data[L.src], n->data[i], (size_t)(S->rows * S->ld), ncclFloat, n->cl->comm_act, st));
@@ -236,13 +262,14 @@ sg_status forward_impl(sg_net* n, int i) {
     }
     case SG_SOFTMAX_CE:
       SG_LCH(softmax_ce(real_view(*S, n->data[L.src]), n->labels, n->row_loss, real_view(*S, n->grad[L.src]),
-                        (float)(1.0 / (double)P.loss_rows), n->err, st));
+                        (float)(1.0 / (double)P.loss_rows), n->err, st, S->rn_grad));
       break;
     case SG_EUCLIDEAN: {
       const LayerPlan& in = P.layers[0];
       View2D u = real_view(*S, n->data[L.src]);
-      View2D v = plain(n->data[0] + S->col_off, (int)S->rows, (int)S->cols, in.ld);
-      SG_LCH(euclidean(u, v, n->row_loss, real_view(*S, n->grad[L.src]), (float)(1.0 / (double)P.loss_rows), st));
+      View2D v = plain((n->x_exact ? n->x_exact : n->data[0]) + S->col_off, (int)S->rows, (int)S->cols, in.ld);
+      SG_LCH(euclidean(u, v, n->row_loss, real_view(*S, n->grad[L.src]), (float)(1.0 / (double)P.loss_rows), st,
+                       S->rn_grad));
       break;
     }
   }
@@ -262,6 +289,7 @@ sg_status backward(sg_net* n, int i) {
   float* dW = L.pW >= 0 ? n->sgr[L.store] + P.params[L.pW].store_off : nullptr;
   float* db = L.pb >= 0 ? n->sgr[L.store] + P.params[L.pb].store_off : nullptr;
   const int s1 = 4 * i + 1, s2 = 4 * i + 2;
+  const int rn_dx = S.rn_grad ? RN_OUT : 0;  // this layer's dx is a GEMM operand (reading A19)
   prof_mark(n, s1, 0, st);
   switch (L.kind) {
     case SG_CONV:
@@ -269,7 +297,7 @@ sg_status backward(sg_net* n, int i) {
       prof_mark(n, s1, 1, st);
       if (need_dx) {
         prof_mark(n, s2, 0, st);
-        SG_LCH(conv_dgrad(conv_shape(L, S), n->grad[i], W, n->grad[L.src], n->ws, st));
+        SG_LCH(conv_dgrad(conv_shape(L, S), n->grad[i], W, n->grad[L.src], n->ws, st, S.rn_grad ? EPI_RN : 0));
         prof_mark(n, s2, 1, st);
       }
       return SG_OK;
@@ -281,20 +309,22 @@ sg_status backward(sg_net* n, int i) {
       const float* ry = j >= 0 ? n->data[j] : nullptr;
       float* dxr = j >= 0 ? n->grad[P.layers[j].src] : nullptr;
       if (!need_dx) break;
+      const int rn = rn_dx | (j >= 0 && P.layers[P.layers[j].src].rn_grad ? RN_AUX : 0);
       if (L.kind == SG_POOL_MAX)
-        SG_LCH(maxpool_bwd(pool_shape(L, S), n->grad[i], n->mask[i], n->grad[L.src], st, ry, dxr));
+        SG_LCH(maxpool_bwd(pool_shape(L, S), n->grad[i], n->mask[i], n->grad[L.src], st, ry, dxr, rn));
       else if (L.kind == SG_POOL_AVG)
-        SG_LCH(avgpool_bwd(pool_shape(L, S), n->grad[i], n->grad[L.src], st, ry, dxr));
+        SG_LCH(avgpool_bwd(pool_shape(L, S), n->grad[i], n->grad[L.src], st, ry, dxr, rn));
       else
         SG_LCH(lrn_bwd(LrnShape{L.rows * L.h * L.w, L.c, L.lrn_size, L.alpha, L.beta, L.k}, n->data[L.src],
-                       n->data[i], n->scale[i], n->grad[i], n->grad[L.src], st, ry, dxr));
+                       n->data[i], n->scale[i], n->grad[i], n->grad[L.src], st, ry, dxr, rn));
       break;
     }
     case SG_RELU:
-      if (need_dx && !n->bwd_fused_away[i]) SG_LCH(relu_bwd(n->data[i], n->grad[i], n->grad[L.src], L.blob_floats(), st));
+      if (need_dx && !n->bwd_fused_away[i])
+        SG_LCH(relu_bwd(n->data[i], n->grad[i], n->grad[L.src], L.blob_floats(), st, rn_dx));
       break;
     case SG_SIGMOID:
-      if (need_dx) SG_LCH(sigmoid_bwd(n->data[i], n->grad[i], n->grad[L.src], L.blob_floats(), st));
+      if (need_dx) SG_LCH(sigmoid_bwd(n->data[i], n->grad[i], n->grad[L.src], L.blob_floats(), st, rn_dx));
       break;
     case SG_INNER_PRODUCT: {
       View2D dy = plain(n->grad[i], (int)L.rows, (int)L.nout, L.ld);
@@ -302,7 +332,8 @@ sg_status backward(sg_net* n, int i) {
       prof_mark(n, s1, 1, st);
       if (need_dx) {
         prof_mark(n, s2, 0, st);
-        SG_LCH(ip_dgrad(dy, W, (int)L.kin, (int)L.nout, feat_view(S, n->grad[L.src], L.kin), n->ws, st));
+        SG_LCH(ip_dgrad(dy, W, (int)L.kin, (int)L.nout, feat_view(S, n->grad[L.src], L.kin), n->ws, st,
+                        S.rn_grad ? EPI_RN : 0));
         prof_mark(n, s2, 1, st);
       }
       return SG_OK;
@@ -310,6 +341,8 @@ sg_status backward(sg_net* n, int i) {
     case SG_CONCAT:
       SG_NCCL(ncclReduceScatter(n->grad[i], n->grad[L.src], (size_t)(S.rows * S.ld), ncclFloat, ncclSum,
                                 n->cl->comm_act, st));
+      // the sum of the ranks' partial input gradients is a GEMM operand of the source (reading A19)
+      if (S.rn_grad) SG_LCH(round_tf32(n->grad[L.src], S.blob_floats(), st));
       break;
     case SG_SLICE: {
       const size_t cnt = (size_t)(L.rows * S.ld);
@@ -336,17 +369,22 @@ sg_status update(sg_net* n, sg_updater* u, int i) {
   SG_CUDA(cudaStreamWaitEvent(n->ps, n->ev_grad[i], 0));
   prof_mark(n, 4 * i + 3, 0, n->ps);
   const float mu = u->cfg.momentum, wd = u->cfg.weight_decay * L.wd_scale;
+  // elements [0, rn_end) of the store are the weight matrix (TF32-RN working copy); the bias follows
+  const int64_t rn_end = P.params[L.pW].isize;
   if (S.sharded) {
+    // worker group -> server group: reduce-scatter (sum) of the gradient bucket;
+    // the server owning shard `rank` updates its fp32 master and writes the
+    // working copy of the shard, which the all-gather distributes (Collect)
     const int64_t shard = S.padded / P.world;
     float* g = n->sgr[L.store];
     float* w = n->sw[L.store];
     SG_NCCL(ncclReduceScatter(g, g + P.rank * shard, (size_t)shard, ncclFloat, ncclSum, n->cl->comm_par, n->ps));
-    SG_LCH(sgd_momentum_dev(w + P.rank * shard, g + P.rank * shard, n->sv[L.store], shard, n->lr_dev, L.lr_scale, mu,
-                            wd, u->s, n->ps));
+    SG_LCH(sgd_momentum_dev(n->sm[L.store], g + P.rank * shard, n->sv[L.store], shard, n->lr_dev, L.lr_scale, mu, wd,
+                            u->s, n->ps, w + P.rank * shard, rn_end - P.rank * shard));
     SG_NCCL(ncclAllGather(w + P.rank * shard, w, (size_t)shard, ncclFloat, n->cl->comm_par, n->ps));
   } else {
-    SG_LCH(sgd_momentum_dev(n->sw[L.store], n->sgr[L.store], n->sv[L.store], S.padded, n->lr_dev, L.lr_scale, mu, wd,
-                            u->s, n->ps));
+    SG_LCH(sgd_momentum_dev(n->sm[L.store], n->sgr[L.store], n->sv[L.store], S.padded, n->lr_dev, L.lr_scale, mu, wd,
+                            u->s, n->ps, n->sw[L.store], rn_end));
   }
   prof_mark(n, 4 * i + 3, 1, n->ps);
   SG_CUDA(cudaEventRecord(n->ev_upd[i], n->ps));
@@ -366,7 +404,7 @@ sg_status loss_reduce(sg_net* n) {
   const Plan& P = PL(n);
   cudaError_t e = sum_scaled(n->row_loss, (int)P.loss_rows, (float)(1.0 / P.batch), n->loss_int, n->err, n->cs);
   SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "loss reduction: %s", cudaGetErrorString(e));
-  if (P.world > 1) SG_NCCL(ncclAllReduce(n->loss_int, n->loss_int, 1, ncclFloat, ncclSum, n->cl->comm_act, n->cs));
+  if (P.dist) SG_NCCL(ncclAllReduce(n->loss_int, n->loss_int, 1, ncclFloat, ncclSum, n->cl->comm_act, n->cs));
   return SG_OK;
 }
 
@@ -487,7 +525,8 @@ void from_internal(const Plan& P, const ParamPlan& q, const float* in, int rk, f
   }
 }
 
-// Gathers a Param-shaped quantity (which: 0 value, 1 grad, 2 history) into the user layout.
+// Gathers a Param-shaped quantity (which: 0 master value, 1 grad, 2 history,
+// 3 working copy) into the user layout.
 sg_status param_export(sg_net* n, int p, int which, float* user) {
   const Plan& P = PL(n);
   SG_CHECK(p >= 0 && p < (int)P.params.size(), SG_ERR_INVALID_ARG, "param index %d out of range", p);
@@ -498,8 +537,27 @@ sg_status param_export(sg_net* n, int p, int which, float* user) {
   SG_CUDA(cudaStreamSynchronize(n->ps));
   SG_CUDA(cudaStreamSynchronize(n->cs));
   const int K = P.world;
+  if (which == 3) {  // working copy: full on every rank (dim-0) or the rank's columns (dim-1)
+    std::vector<float> h((size_t)q.isize * (q.split_dim == 1 ? K : 1));
+    if (q.split_dim == 1) {
+      float* tmp;
+      SG_CUDA(cudaMalloc(&tmp, h.size() * sizeof(float)));
+      ncclResult_t r = ncclAllGather(n->sw[q.store] + q.store_off, tmp, (size_t)q.isize, ncclFloat, n->cl->comm_act,
+                                     n->cs);
+      cudaError_t e = cudaStreamSynchronize(n->cs);
+      if (e == cudaSuccess) e = cudaMemcpy(h.data(), tmp, h.size() * sizeof(float), cudaMemcpyDeviceToHost);
+      cudaFree(tmp);
+      SG_CHECK(r == ncclSuccess, SG_ERR_NCCL, "param export: %s", ncclGetErrorString(r));
+      SG_CHECK(e == cudaSuccess, SG_ERR_CUDA, "param export: %s", cudaGetErrorString(e));
+      for (int rk = 0; rk < K; ++rk) from_internal(P, q, h.data() + (size_t)rk * q.isize, rk, user);
+    } else {
+      SG_CUDA(cudaMemcpy(h.data(), n->sw[q.store] + q.store_off, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+      from_internal(P, q, h.data(), P.rank, user);
+    }
+    return SG_OK;
+  }
   if (q.split_dim == 1) {
-    const float* src = (which == 0 ? n->sw : which == 1 ? n->sgr : n->sv)[q.store] + q.store_off;
+    const float* src = (which == 0 ? n->sm : which == 1 ? n->sgr : n->sv)[q.store] + q.store_off;
     float* tmp;
     SG_CUDA(cudaMalloc(&tmp, (size_t)q.isize * K * sizeof(float)));
     ncclResult_t r = ncclAllGather(src, tmp, (size_t)q.isize, ncclFloat, n->cl->comm_act, n->cs);
@@ -512,14 +570,15 @@ sg_status param_export(sg_net* n, int p, int which, float* user) {
     for (int rk = 0; rk < K; ++rk) from_internal(P, q, h.data() + (size_t)rk * q.isize, rk, user);
     return SG_OK;
   }
-  // replicated (dim-0) Param: full value on every rank; grad / history sharded when K > 1
+  // replicated (dim-0) Param: master value, aggregated gradient and history are
+  // sharded over the server group when the store is
   std::vector<float> h((size_t)S.padded);
-  if (which == 0 || !S.sharded) {
-    const float* src = (which == 0 ? n->sw : which == 1 ? n->sgr : n->sv)[q.store];
+  if (!S.sharded) {
+    const float* src = (which == 0 ? n->sm : which == 1 ? n->sgr : n->sv)[q.store];
     SG_CUDA(cudaMemcpy(h.data(), src, (size_t)S.padded * sizeof(float), cudaMemcpyDeviceToHost));
   } else {
     const int64_t shard = S.padded / K;
-    const float* src = which == 1 ? n->sgr[q.store] + P.rank * shard : n->sv[q.store];
+    const float* src = which == 1 ? n->sgr[q.store] + P.rank * shard : which == 0 ? n->sm[q.store] : n->sv[q.store];
     float* tmp;
     SG_CUDA(cudaMalloc(&tmp, (size_t)S.padded * sizeof(float)));
     ncclResult_t r = ncclAllGather(src, tmp, (size_t)shard, ncclFloat, n->cl->comm_act, n->cs);
@@ -618,7 +677,7 @@ sg_status destroy_net(sg_net* n) {
 }
 
 sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
-  SG_TRY(build_plan(cfg, c->rank, c->world, &n->plan.p));
+  SG_TRY(build_plan(cfg, c->rank, c->world, &n->plan.p, c->force));
   const Plan& P = n->plan.p;
   SG_CUDA(cudaSetDevice(c->device));
   SG_CUDA(cudaStreamCreateWithFlags(&n->cs, cudaStreamNonBlocking));
@@ -680,13 +739,18 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
     const LayerPlan& in = P.layers[0];
     SG_TRY(dalloc_t(n, (size_t)(in.rows * in.feat), &n->x_stage));
   }
+  if (P.layers[P.loss].kind == SG_EUCLIDEAN && P.layers[0].rn_data)
+    SG_TRY(dalloc_t(n, (size_t)P.layers[0].blob_floats(), &n->x_exact));
   for (const StorePlan& S : P.stores) {
-    float *w, *g, *v;
+    float *w, *g, *m, *v;
+    const size_t own = (size_t)(S.sharded ? S.padded / P.world : S.padded);
     SG_TRY(dalloc_t(n, (size_t)S.padded, &w));
     SG_TRY(dalloc_t(n, (size_t)S.padded, &g));
-    SG_TRY(dalloc_t(n, (size_t)(S.sharded ? S.padded / P.world : S.padded), &v));
+    SG_TRY(dalloc_t(n, own, &m));
+    SG_TRY(dalloc_t(n, own, &v));
     n->sw.push_back(w);
     n->sgr.push_back(g);
+    n->sm.push_back(m);
     n->sv.push_back(v);
   }
   n->data_own = n->data;
@@ -729,7 +793,8 @@ SG_API sg_status sg_cluster_create(const sg_cluster_cfg* cfg, sg_cluster** out) 
   c->rank = cfg->rank;
   c->world = cfg->world_size;
   c->device = cfg->device;
-  if (c->world > 1) {
+  c->force = c->world == 1 && cfg->exercise_collectives != 0;
+  if (c->world > 1 || c->force) {
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_id, 128);
     ncclResult_t r = ncclCommInitRank(&c->comm_act, c->world, id, c->rank);
@@ -816,11 +881,22 @@ SG_API sg_status sg_param_set_value(sg_net* n, int32_t p, const float* user) {
   const Plan& P = PL(n);
   SG_CHECK(p >= 0 && p < (int)P.params.size(), SG_ERR_INVALID_ARG, "param index %d out of range", p);
   const ParamPlan& q = P.params[p];
+  const StorePlan& S = P.stores[q.store];
   std::vector<float> h;
   to_internal(P, q, user, h);
   SG_CUDA(cudaSetDevice(n->cl->device));
   SG_CUDA(cudaStreamSynchronize(n->ps));
   SG_CUDA(cudaStreamSynchronize(n->cs));
+  // fp32 master: the whole Param, or its part inside this rank's shard
+  const int64_t shard = S.sharded ? S.padded / P.world : S.padded;
+  const int64_t lo = S.sharded ? (int64_t)P.rank * shard : 0;
+  const int64_t b0 = std::max<int64_t>(q.store_off, lo), b1 = std::min<int64_t>(q.store_off + q.isize, lo + shard);
+  if (b1 > b0)
+    SG_CUDA(cudaMemcpy(n->sm[q.store] + (b0 - lo), h.data() + (b0 - q.store_off), (size_t)(b1 - b0) * sizeof(float),
+                       cudaMemcpyHostToDevice));
+  // working copy: weights TF32-RN (reading A19), biases exact
+  if (!q.is_bias)
+    for (float& x : h) x = tf32_rna_host(x);
   SG_CUDA(cudaMemcpy(n->sw[q.store] + q.store_off, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
   return SG_OK;
 }
@@ -835,6 +911,10 @@ SG_API sg_status sg_param_get_grad(sg_net* n, int32_t p, float* user) {
 SG_API sg_status sg_param_get_history(sg_net* n, int32_t p, float* user) {
   SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
   return param_export(n, p, 2, user);
+}
+SG_API sg_status sg_param_get_working(sg_net* n, int32_t p, float* user) {
+  SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
+  return param_export(n, p, 3, user);
 }
 
 SG_API sg_status sg_updater_create(sg_net* n, const sg_updater_cfg* cfg, sg_updater** out) {

@@ -34,6 +34,22 @@ inline FastDiv make_fastdiv(int d) {
   return f;
 }
 
+// ------------------------------------------------------- TF32 rounding --
+// Round an fp32 value to TF32 (10 explicit mantissa bits) to nearest, ties away
+// from zero (the semantics of cvt.rna.tf32.f32), with the 13 low bits zeroed:
+// adding half a TF32 ulp to the sign-magnitude bit pattern carries into the
+// kept bits exactly when the dropped part is >= half (Inf / NaN stay Inf / NaN).
+// Reading A19: every blob a tensor-core GEMM reads as an operand is
+// stored rounded this way by the kernel that produces it, so the MMA's
+// truncation of the low bits is a no-op.
+__device__ __forceinline__ float tf32_rna(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ float4 tf32_rna4(float4 v) {
+  return make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+}
+__device__ __forceinline__ float4 tf32_rna4_if(float4 v, bool on) { return on ? tf32_rna4(v) : v; }
+
 // ---------------------------------------------------------------- mbarrier --
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));

@@ -91,7 +91,8 @@ class Plan:
             out.append({"name": li.name.decode(), "kind": L.KIND_NAMES[li.kind], "partition_dim": li.partition_dim,
                         "is_connection": li.is_connection, "src": li.src,
                         "global_shape": tuple(li.global_shape), "local_shape": tuple(li.local_shape),
-                        "local_offset": tuple(li.local_offset), "ld": li.ld, "nblocks": li.nblocks})
+                        "local_offset": tuple(li.local_offset), "ld": li.ld, "nblocks": li.nblocks,
+                        "tf32_data": bool(li.tf32_data), "tf32_grad": bool(li.tf32_grad)})
         return out
 
     def params(self):
@@ -127,9 +128,12 @@ def param_shape(p):
 
 
 class Cluster:
-    def __init__(self, rank=0, world=1, device=0, nccl_id=None):
+    def __init__(self, rank=0, world=1, device=0, nccl_id=None, exercise_collectives=False):
         cfg = L.ClusterCfg()
         cfg.rank, cfg.world_size, cfg.device = rank, world, device
+        cfg.exercise_collectives = 1 if exercise_collectives else 0
+        if exercise_collectives and nccl_id is None and world == 1:
+            nccl_id = Cluster.unique_id()
         cfg.nworker_groups, cfg.workers_per_group = 1, world
         cfg.nserver_groups, cfg.servers_per_group = 1, world
         if nccl_id is not None:
@@ -208,6 +212,10 @@ class Net:
 
     def get_history(self, shapes):
         return self._export(L.sg_param_get_history, shapes)
+
+    def get_working(self, shapes):
+        """The working copy the GEMMs read (TF32-RN weights, fp32 biases; reading A19)."""
+        return self._export(L.sg_param_get_working, shapes)
 
     def train_one_batch(self, step, x_ptr, labels_ptr, loss_ptr, stream=None):
         L.sg_train_one_batch(self.h, self.upd, step, x_ptr, labels_ptr, loss_ptr, stream)

@@ -26,7 +26,7 @@ def test_exports_every_declared_symbol():
     assert len(names) >= 50
     for n in names:
         assert hasattr(L.lib, n), n
-    assert L.sg_abi_version() == 1
+    assert L.sg_abi_version() == 2
 
 
 def test_partition_range_matches_oracle():

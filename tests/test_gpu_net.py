@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 from oracle import layers as OL  # noqa: E402
 from oracle import net as ON  # noqa: E402
 from oracle import updater as OU  # noqa: E402
-from tests.gpu_util import FP32_TOL, TF32_TOL, f64, normwise  # noqa: E402
+from tests import layer_check as LC  # noqa: E402
+from tests.gpu_util import TF32_TOL, f64, normwise  # noqa: E402
 from workloads import configs, generate  # noqa: E402
 
 if torch.cuda.is_available():
@@ -30,8 +31,8 @@ if torch.cuda.is_available():
     from paper_1603_07846_b200 import net as PN  # noqa: E402
 
 
-def build(net, b, upd=None, params=None, graph=False):
-    cl = PN.Cluster(0, 1, 0)
+def build(net, b, upd=None, params=None, graph=False, cluster=None):
+    cl = cluster or PN.Cluster(0, 1, 0)
     n = PN.Net(cl, net, b)
     n.set_updater(upd or configs.UPDATERS.get(net["name"], configs.UPDATERS["mlp"]))
     if params is None:
@@ -47,9 +48,9 @@ def shapes_of(params):
 
 
 class Run:
-    def __init__(self, net, b, upd=None, graph=False):
+    def __init__(self, net, b, upd=None, graph=False, cluster=None):
         self.net, self.b = net, b
-        self.cl, self.n, self.p0 = build(net, b, upd, graph=graph)
+        self.cl, self.n, self.p0 = build(net, b, upd, graph=graph, cluster=cluster)
         self.loss = torch.zeros(1, device="cuda")
 
     def step(self, t, x, lab):
@@ -72,101 +73,18 @@ class Run:
         self.cl.close()
 
 
-def local_blob(run, i, which=0):
-    """Blob i as a float64 array in the oracle's per-sample layout (padding stripped)."""
-    li = run.n.layer_info[i]
-    if which == 1:
-        li = run.n.layer_info[li["src"]]
-    raw = run.blob(i, which)
-    rows = li["local_shape"][0]
-    if li["kind"] == "input" or (li["local_shape"][2] > 1 or li["local_shape"][3] > 1):
-        _, h, w, c = li["local_shape"]
-        a = raw.reshape(rows, h, w, c)
-        return f64(a)
-    cols = li["local_shape"][1]
-    return f64(raw.reshape(rows, li["ld"])[:, :cols])
-
-
-def run_layer_isolated(net, b, steps=1):
-    run = Run(net, b)
-    run.n.set_fusion(False)   # every layer's own output blob is materialised
+def run_layer_isolated(net, b, cluster=None, fused=False, graph=False, sub=None):
+    """One step, then every layer layer-isolated against the oracle
+    (tests/layer_check.py).  Returns the set of layer kinds checked."""
+    run = Run(net, b, cluster=cluster, graph=graph)
+    run.n.set_fusion(fused)
     try:
         x, lab = generate.batch(net, b, 0)
         run.step(0, x, lab)
-        grads = run.n.get_grads(shapes_of(run.p0))
-        newp = run.n.get_params(shapes_of(run.p0))
-        infos = run.n.layer_info
-        p = {k: f64(v) for k, v in run.p0.items()}
-        x_in = f64(x)
-        checked = []
-        for i, li in enumerate(infos):
-            k = li["kind"]
-            if k == "input":
-                continue
-            src = li["src"]
-            xin = x_in if infos[src]["kind"] == "input" else local_blob(run, src)
-            consumers = [j for j, lj in enumerate(infos) if lj["src"] == i]
-            dy = local_blob(run, consumers[0], 1) if consumers and k not in ("softmax_ce", "euclidean") else None
-            dx = local_blob(run, i, 1) if infos[src]["kind"] != "input" else None
-            lname = li["name"]
-            lc = next(l for l in net["layers"] if l["name"] == lname)
-            if k == "conv":
-                y = local_blob(run, i)
-                assert normwise(y, OL.conv_forward(xin, p[lname + "/W"], p[lname + "/b"], lc["stride"], lc["pad"])) < TF32_TOL
-                rdx, rdW, rdb = OL.conv_backward(xin, p[lname + "/W"], dy, lc["stride"], lc["pad"])
-                assert normwise(grads[lname + "/W"], rdW) < TF32_TOL
-                assert normwise(grads[lname + "/b"], rdb) < TF32_TOL   # fused ones-row of the TF32 wgrad GEMM
-                if dx is not None:
-                    assert normwise(dx, rdx) < TF32_TOL
-            elif k == "ip":
-                y = local_blob(run, i)
-                xf = xin.reshape(xin.shape[0], -1)
-                assert normwise(y, OL.ip_forward(xf, p[lname + "/W"], p[lname + "/b"])) < TF32_TOL
-                rdx, rdW, rdb = OL.ip_backward(xf, p[lname + "/W"], dy)
-                assert normwise(grads[lname + "/W"], rdW) < TF32_TOL
-                assert normwise(grads[lname + "/b"], rdb) < TF32_TOL   # fused ones-row of the TF32 wgrad GEMM
-                if dx is not None:
-                    assert normwise(dx.reshape(dx.shape[0], -1), rdx) < TF32_TOL
-            elif k == "pool_max":
-                y = local_blob(run, i)
-                ry, ridx = OL.maxpool_forward(xin, lc["kernel"], lc["stride"], lc["pad"])
-                assert np.array_equal(y, ry.astype(np.float32).astype(np.float64))
-                am = run.blob(i, 2, torch.int32).reshape(ridx.shape)
-                assert np.array_equal(am, ridx)                        # bit-exact argmax
-                assert normwise(dx, OL.maxpool_backward(xin.shape, ridx, dy)) < FP32_TOL
-            elif k == "pool_avg":
-                y = local_blob(run, i)
-                assert normwise(y, OL.avgpool_forward(xin, lc["kernel"], lc["stride"], lc["pad"])) < FP32_TOL
-                assert normwise(dx, OL.avgpool_backward(xin.shape, dy, lc["kernel"], lc["stride"], lc["pad"])) < FP32_TOL
-            elif k == "lrn":
-                y = local_blob(run, i)
-                ry, rsc = OL.lrn_forward(xin, lc["size"], lc["alpha"], lc["beta"], lc["k"])
-                assert normwise(y, ry) < FP32_TOL
-                assert normwise(dx, OL.lrn_backward(xin, y, rsc, dy, lc["size"], lc["alpha"], lc["beta"])) < 2 * FP32_TOL
-            elif k in ("relu", "sigmoid"):
-                y = local_blob(run, i)
-                f, bw = (OL.relu_forward, OL.relu_backward) if k == "relu" else (OL.sigmoid_forward, OL.sigmoid_backward)
-                assert normwise(y, f(xin)) < FP32_TOL
-                if dx is not None:
-                    assert normwise(dx, bw(y, dy)) < FP32_TOL
-            elif k == "softmax_ce":
-                z = xin.reshape(xin.shape[0], -1)
-                rl, rdz = OL.softmax_ce(z, lab, b)
-                assert normwise(run.blob(i, 0)[:b], rl) < FP32_TOL
-                assert normwise(dx.reshape(b, -1), rdz) < FP32_TOL
-                assert np.array_equal(np.argmin(dx.reshape(b, -1), axis=1), lab)
-            elif k == "euclidean":
-                u = xin.reshape(xin.shape[0], -1)
-                rl, rdu = OL.euclidean(u, x_in.reshape(b, -1), b)
-                assert normwise(run.blob(i, 0)[:b], rl) < FP32_TOL
-                assert normwise(dx.reshape(b, -1), rdu) < FP32_TOL
-            checked.append(k)
-        # Updater, layer-isolated: new params from the GPU's own aggregated gradients
-        upd = configs.UPDATERS[net["name"]]
-        for name in run.p0:
-            w1, _ = OU.sgd_momentum(p[name], np.zeros_like(p[name]), f64(grads[name]), upd, 0, 1.0)
-            assert normwise(newp[name], w1) < 1e-6, name
-        return checked
+        sh = shapes_of(run.p0)
+        LC.check_layers(run.n, net, b, x, lab, run.p0, run.n.get_grads(sh), run.n.get_params(sh),
+                        run.n.get_working(sh), configs.UPDATERS.get(net["name"]) or configs.UPDATERS[net["name"].split("_")[0]], fused=fused, sub=sub)
+        return {li["kind"] for li in run.n.layer_info if li["kind"] != "input"}
     finally:
         run.close()
 
@@ -190,9 +108,89 @@ def test_layer_isolated_tiny_conv_ragged():
     run_layer_isolated(net, 6)
 
 
+@pytest.mark.parametrize("name,b", [("cifar10", 16), ("tiny_conv", 6), ("mlp", 64)])
+def test_layer_isolated_fused_graph(name, b):
+    """The bench configuration (layer fusion + CUDA-graph replay) layer-isolated."""
+    run_layer_isolated(configs.get(name), b, fused=True, graph=True)
+
+
 def test_alexnet_layer_isolated_small_batch():
     net = configs.alexnet(hybrid=False)
     run_layer_isolated(net, 2)
+
+
+# Rows a7 / a11 / a16 / a18 / a19 of SURVEY §8(a) on ONE GPU: the cluster's
+# exercise_collectives switch plans the net as partitioned at world size 1 (a
+# one-rank NCCL communicator), so the connection layers' all-gather /
+# reduce-scatter / all-to-all (P:493-498), the worker->server reduce-scatter,
+# the Updater on the server shard and the parameter all-gather (P:419-422,
+# P:527, P:586) and the loss all-reduce all run, layer-isolated against the
+# oracle; K = 2 / 4 are tests/test_gpu_dist.py.
+def hybrid_alexnet():
+    return configs.alexnet(hybrid=True)
+
+
+@pytest.mark.parametrize("name,b,expect", [
+    ("cifar10", 16, set()),                  # dim-0 only: sharded buckets, loss all-reduce
+    ("alexnet_hybrid", 2, {"concat", "slice"}),  # pool5 -> concat(rows) -> fc6 (dim 1) -> ... -> slice -> loss
+    ("ae", 32, {"concat"}),                  # all dim 1: concat(cols) between every FC, dim-1 Euclidean
+    ("mlp", 64, set()),
+])
+def test_layer_isolated_exercised_collectives(name, b, expect):
+    net = hybrid_alexnet() if name == "alexnet_hybrid" else configs.get(name)
+    cl = PN.Cluster(0, 1, 0, exercise_collectives=True)
+    checked = run_layer_isolated(net, b, cluster=cl)
+    assert expect <= set(checked), checked
+
+
+@pytest.mark.parametrize("name,b", [("cifar10", 32), ("alexnet_hybrid", 2), ("ae", 64)])
+def test_exercised_collectives_bit_identical_to_plain(name, b):
+    """At world size 1 the partitioned data plane is an identity (one-rank
+    collectives), so three free-running steps (graph replay) must give the
+    SAME bits as the unpartitioned plan: losses, master params, history."""
+    net = hybrid_alexnet() if name == "alexnet_hybrid" else configs.get(name)
+    upd = configs.UPDATERS[name.split("_")[0]]
+    runs = [Run(net, b, upd=upd, graph=True),
+            Run(net, b, upd=upd, graph=True, cluster=PN.Cluster(0, 1, 0, exercise_collectives=True))]
+    try:
+        assert any(l["is_connection"] for l in runs[1].n.layer_info) or name == "cifar10"
+        for t in range(3):
+            x, lab = generate.batch(net, b, t)
+            la, lb = (r.step(t, x, lab) for r in runs)
+            assert la == lb, (t, la, lb)
+        sh = shapes_of(runs[0].p0)
+        for get in ("get_params", "get_history", "get_working"):
+            pa, pb = getattr(runs[0].n, get)(sh), getattr(runs[1].n, get)(sh)
+            for k in pa:
+                assert np.array_equal(pa[k], pb[k]), (get, k)
+    finally:
+        for r in runs:
+            r.close()
+
+
+def test_diverged_is_reported():
+    """A non-finite loss raises SG_ERR_DIVERGED at sg_net_sync (SPEC S:288 /
+    S:341 via SURVEY §8(a) a19): an infinite output bias makes every logit row
+    contain inf, so LSE - z_y is nan."""
+    net = configs.get("cifar10")
+    b = 16
+    run = Run(net, b)
+    try:
+        x, lab = generate.batch(net, b, 0)
+        run.step(0, x, lab)
+        pi = run.n.param_index()["ip1/b"]
+        bias = np.zeros(10, np.float32)
+        bias[3] = np.inf
+        L.sg_param_set_value(run.n.h, pi, bias.ctypes.data_as(C.c_void_p))
+        xd, ld = torch.from_numpy(x).cuda(), torch.from_numpy(lab).cuda()
+        run.n.train_one_batch(1, xd.data_ptr(), ld.data_ptr(), run.loss.data_ptr())
+        with pytest.raises(L.SingaError) as e:
+            run.n.sync()
+        assert e.value.name == "SG_ERR_DIVERGED" and e.value.code == -7
+        assert not np.isfinite(float(run.loss.item()))
+        run.n.sync()                       # the flag is cleared once reported
+    finally:
+        run.close()
 
 
 def test_mlp_whole_step_and_loss_curve():
@@ -222,9 +220,12 @@ def test_mlp_whole_step_and_loss_curve():
         run.close()
 
 
-@pytest.mark.parametrize("name,b,steps", [("cifar10", 128, 20), ("ae", 64, 20)])
+@pytest.mark.parametrize("name,b,steps", [("cifar10", 128, 100), ("ae", 256, 100), ("alexnet", 64, 20)])
 def test_loss_curve_within_1pct(name, b, steps):
-    net = configs.get(name)
+    """Free-running loss, GPU vs oracle, within 1% at every step (reading A20;
+    SURVEY §8(c).5 item 3: C2 and C4a over 100 steps, C3 at b = 64 over 20),
+    each step on a fresh batch of the non-repeating synthetic pool."""
+    net = configs.alexnet(hybrid=False) if name == "alexnet" else configs.get(name)
     upd = configs.UPDATERS[name]
     run = Run(net, b)
     try:

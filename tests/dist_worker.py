@@ -21,6 +21,7 @@ from oracle import net as ON  # noqa: E402
 from oracle import updater as OU  # noqa: E402
 from paper_1603_07846_b200 import _lib as L  # noqa: E402
 from paper_1603_07846_b200 import net as PN  # noqa: E402
+from tests import layer_check as LC  # noqa: E402
 from workloads import configs, generate  # noqa: E402
 
 # Smooth nets (sigmoid / avg-pool: no decision flips) so that chained gradients
@@ -108,11 +109,13 @@ def run_smooth(net, b, steps, rank, world, cl, graph=False):
     return (net, b, steps) + run_net(cl, net, b, steps, UPD, rank, world, graph)
 
 
-def check_smooth(res, world, gtol=1e-2):
-    """Chained (not layer-isolated) comparison: losses within 2e-3; gradients
-    and parameter updates of every layer within 1e-2 (TF32 operand rounding
-    accumulates through the chain of layers; layer-isolated parity is
-    tests/test_gpu_net.py)."""
+def check_smooth(res, world, gtol=2e-3):
+    """Chained (not layer-isolated) comparison on nets without ReLU / max-pool
+    decisions: losses, first-step gradients and the parameter updates of every
+    layer within 2e-3 (north star).  With TF32 round-to-nearest operands
+    (reading A19) the chained error stays below the tolerance (SURVEY
+    Appendix A: 8.3e-4 after 8 layers); layer-isolated parity is
+    case_isolated below and tests/test_gpu_net.py."""
     net, b, steps, params, losses, g0, final = res
     ol, og, op = oracle_run(net, b, steps, UPD, world, params)
     for t, (a, c) in enumerate(zip(losses, ol)):
@@ -151,6 +154,9 @@ def case_autoencoder(rank, world, cl):
 
 
 def case_alexnet(rank, world, cl):
+    """AlexNet hybrid (dim-0 conv, dim-1 fc6-fc8, dim-0 loss): the loss
+    of two free-running steps within 1% (A20), and every layer of the first
+    step layer-isolated at 2e-3 (case_isolated's checks)."""
     net = configs.alexnet(hybrid=True)
     b = 2 * world
     params, losses, g0, final = run_net(cl, net, b, 2, configs.UPDATERS["alexnet"], rank, world)
@@ -158,9 +164,59 @@ def case_alexnet(rank, world, cl):
         ol, og, _ = oracle_run(net, b, 2, configs.UPDATERS["alexnet"], world, params)
         for t, (a, c) in enumerate(zip(losses, ol)):
             assert abs(a - c) <= 0.01 * abs(c), (t, a, c)      # reading A20
-        e = normwise(g0["fc8/W"], og["fc8/W"])
-        assert e < 5e-2, e    # chained through ReLU / max-pool decisions (reading A10)
-        print(f"alexnet hybrid K={world}: losses {losses} vs oracle {ol}; fc8/W grad err {e:.2e}", flush=True)
+        print(f"alexnet hybrid K={world}: losses {losses} vs oracle {ol}", flush=True)
+    isolated(cl, net, b, rank, world, configs.UPDATERS["alexnet"], fused=True, graph=True)
+
+
+def isolated(cl, net, b, rank, world, upd, fused=False, graph=False):
+    """One step; every rank checks its local layers against the oracle fed its
+    own blobs (tests/layer_check.check_layers_dist), cross-rank sums and
+    gathers over gloo; 2e-3 for TF32 contractions, 1e-5 for SIMT kernels,
+    argmax / label / connection layers bit-exact."""
+    n = PN.Net(cl, net, b)
+    n.set_updater(upd)
+    params = generate.init_params(ON.param_specs(net))
+    n.set_params(params)
+    n.set_fusion(fused)
+    if graph:
+        n.enable_graph(True)
+    info = n.layer_info
+    r0, rl = info[0]["local_offset"][0], info[0]["local_shape"][0]
+    lsrc = info[info[-1]["src"]]
+    l0, ll = lsrc["local_offset"][0], lsrc["local_shape"][0]
+    x, lab = generate.batch(net, b, 0)
+    sh = {k: v.shape for k, v in params.items()}
+    work0 = n.get_working(sh)
+    xd = torch.from_numpy(np.ascontiguousarray(x[r0:r0 + rl])).cuda()
+    ld = torch.from_numpy(np.ascontiguousarray(lab[l0:l0 + ll])).cuda() if net["num_classes"] else None
+    loss = torch.zeros(1, device="cuda")
+    n.train_one_batch(0, xd.data_ptr(), ld.data_ptr() if ld is not None else None, loss.data_ptr())
+    n.sync()
+    grads, newp = n.get_grads(sh), n.get_params(sh)
+    rep = LC.check_layers_dist(n, net, b, x, lab, params, work0, grads, newp, upd, rank, world, fused=fused)
+    n.close()
+    worst = {}
+    for _, q, e in rep:
+        worst[q] = max(worst.get(q, 0.0), e)
+    allw = [None] * world
+    dist.all_gather_object(allw, worst)
+    if rank == 0:
+        tot = {}
+        for w in allw:
+            for q, e in w.items():
+                tot[q] = max(tot.get(q, 0.0), e)
+        kinds = sorted({l["kind"] for l in info})
+        print(f"{net['name']} K={world} layer-isolated ({len(rep)} checks/rank, kinds {kinds}): worst "
+              + ", ".join(f"{q} {e:.2e}" for q, e in sorted(tot.items())), flush=True)
+
+
+def case_isolated(rank, world, cl):
+    isolated(cl, configs.get("cifar10"), 8 * world, rank, world, configs.UPDATERS["cifar10"], fused=True, graph=True)
+    isolated(cl, HYBRID_SMOOTH, 4 * world, rank, world, UPD)
+    # the paper's auto-encoder (2-unit code layer) partitions over K <= 2 only
+    ae = configs.get("ae") if world <= 2 else configs.autoencoder([784, 256, 64, 8, 64, 256, 784], "ae_k4")
+    isolated(cl, ae, 16, rank, world, configs.UPDATERS["ae"], fused=True)
+    isolated(cl, configs.get("mlp"), 8 * world, rank, world, configs.UPDATERS["mlp"])
 
 
 def case_server_sync(rank, world, cl):
@@ -234,6 +290,7 @@ def case_peer_sync(rank, world, cl):
 
 
 CASES = {"k_invariance": case_k_invariance, "hybrid": case_hybrid, "autoencoder": case_autoencoder,
+         "isolated": case_isolated,
          "alexnet": case_alexnet, "server_sync": case_server_sync, "peer_sync": case_peer_sync}
 
 if __name__ == "__main__":

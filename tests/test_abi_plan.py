@@ -196,3 +196,23 @@ def test_bench_grad_sync_bytes(name, K, params):
     got = bench.grad_sync_bytes(net, plan.layers(), K)
     assert sum(got.values()) == 4 * params
     assert bench.grad_sync_bytes(net, plan.layers(), 1) == {}
+
+
+@pytest.mark.parametrize("name,K,data,grad", [
+    ("cifar10", 1, {"input", "norm1", "norm2", "norm3"}, {"conv1", "conv2", "conv3", "ip1"}),
+    ("mlp", 1, {"input", "sig1"}, {"ip1", "ip2"}),
+    ("alexnet", 2,
+     {"input", "pool1", "pool2", "relu3", "relu4", "pool5", "pool5.concat_rows", "relu6", "relu6.concat_cols",
+      "relu7", "relu7.concat_cols"},
+     {"conv1", "conv2", "conv3", "conv4", "conv5", "fc6", "fc7", "fc8", "fc8.slice"}),
+])
+def test_tf32_operand_flags(name, K, data, grad):
+    """Reading A19: a blob is stored TF32-rounded exactly when a tensor-core GEMM
+    reads it -- the input of every conv / inner product (through an all-gather
+    Concat, which moves values unchanged), and the gradient w.r.t. a conv / IP
+    output (through the loss Slice's all-to-all)."""
+    net = configs.get(name) if name != "alexnet" else configs.alexnet(hybrid=True)
+    plan = PN.Plan(net, configs.BATCH[name], rank=0, world=K)
+    ls = plan.layers()
+    assert {l["name"] for l in ls if l["tf32_data"]} == data
+    assert {l["name"] for l in ls if l["tf32_grad"]} == grad

@@ -44,6 +44,7 @@ class Full:
         self.loss = torch.zeros(1, device="cuda")
 
     def step(self, t):
+        self.work0 = self.n.get_working({k: v.shape for k, v in self.p0.items()})
         x, lab = generate.batch(self.net, self.b, t)
         xd, ld = torch.from_numpy(x).cuda(), torch.from_numpy(lab).cuda()
         self.n.train_one_batch(t, xd.data_ptr(), ld.data_ptr(), self.loss.data_ptr())
@@ -52,7 +53,8 @@ class Full:
 
     def check(self, x, lab, sub=None):
         sh = {k: v.shape for k, v in self.p0.items()}
-        return LC.check_layers(self.n, self.net, self.b, x, lab, self.p0, self.n.get_grads(sh), self.n.get_params(sh),
+        return LC.check_layers(self.n, self.net, self.b, x, lab, self.p0, self.work0, self.n.get_grads(sh),
+                               self.n.get_params(sh),
                                self.n.get_working(sh), self.upd, fused=True, sub=sub)
 
     def close(self):

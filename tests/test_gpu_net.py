@@ -80,9 +80,10 @@ def run_layer_isolated(net, b, cluster=None, fused=False, graph=False, sub=None)
     run.n.set_fusion(fused)
     try:
         x, lab = generate.batch(net, b, 0)
-        run.step(0, x, lab)
         sh = shapes_of(run.p0)
-        LC.check_layers(run.n, net, b, x, lab, run.p0, run.n.get_grads(sh), run.n.get_params(sh),
+        work0 = run.n.get_working(sh)
+        run.step(0, x, lab)
+        LC.check_layers(run.n, net, b, x, lab, run.p0, work0, run.n.get_grads(sh), run.n.get_params(sh),
                         run.n.get_working(sh), configs.UPDATERS.get(net["name"]) or configs.UPDATERS[net["name"].split("_")[0]], fused=fused, sub=sub)
         return {li["kind"] for li in run.n.layer_info if li["kind"] != "input"}
     finally:

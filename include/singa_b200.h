@@ -337,7 +337,9 @@ SG_API sg_status sg_net_enable_graph(sg_net* n, int32_t enable);
  *  - a ReLU after a pooling layer is written by the pooling kernel, and
  *    pooling [-> ReLU] -> LRN runs as one kernel;
  *  - a ReLU's backward is done by the backward kernel of its single consumer
- *    (LRN or pooling).
+ *    (LRN or pooling);
+ *  - a first-layer 4-channel stride-1 convolution feeding a max pool computes
+ *    the pool's backward (its dy) inside its weight-gradient kernel.
  * Every layer's data / grad blob is still written (sg_blob_get sees them). */
 SG_API sg_status sg_net_set_fusion(sg_net* n, int32_t enable);
 /* Kernel launches issued by the last sg_train_one_batch (graph replay counts the captured kernels). */

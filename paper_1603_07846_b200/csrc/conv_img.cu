@@ -778,6 +778,435 @@ cudaError_t conv_img_dgrad(const ConvShape& s, const float* dy, const float* W, 
   return run_img(a, smem, s.N, st);
 }
 
+namespace {
+
+// ------------------------------------ 4-channel first layer: weight gradient --
+// CIFAR conv1 (C = 4 padded channels, stride 1, Co = 32), optionally fused with
+// the backward of the max-pooling layer that consumes it (SURVEY §8(a)
+// a13 + a15):
+//
+//   dy[q][co]          = sum of the pool's output gradient over the windows whose
+//                        argmax is q (ascending window order, = maxpool_bwd_kernel;
+//                        written out: the pool's dx blob stays materialised)
+//   dW[co][(r,s,c)]    = sum_n sum_q img[q + r*Wp + s][c] * dy[q][co]
+//   db[co]             = sum_n sum_q dy[q][co]       (ones row of the GEMM)
+//
+// One CTA per sample (persistent over samples, accumulating in TMEM).  The
+// sample's dy (all pixels x 32 channels, 128 KB) is built ONCE in shared memory
+// in the UMMA MN-major SWIZZLE_128B_BASE32B layout (k-line = pixel) and serves as
+// the B operand of every MMA; the padded image is staged by one TMA box (zero
+// padding = out-of-bounds fill) and the A operand (MN-major, row kg = (tap, c),
+// k-line = pixel) is an im2col built from it in shared memory, 32 pixels per
+// stage, 4-stage pipeline.  Rows kg >= R*S*4 are constant (the ones row of the
+// bias gradient, zeros) and written once per stage buffer.
+//   warps 0-15: dy (pool backward), im2col producers; warps 0-3 the epilogue
+//   warp 16   : TMEM allocation, the MMA issuer (one lane)
+// The per-CTA partial is reduced by conv_wgrad_sum_kernel (fixed order).
+#ifndef SG_I4W_FENCE
+#define SG_I4W_FENCE 0
+#endif
+constexpr int kI4WProd = 512;  // producer threads (16 warps)
+constexpr int kI4WThreads = kI4WProd + 32;
+constexpr int kI4WStages = 4;
+constexpr int kI4WKB = 32;  // pixels per stage
+
+struct Img4WgradArgs {
+  CUtensorMap img_map;  // x {4, W, H, N}, box {4, Wp, Hp, 1}, no swizzle
+  CUtensorMap dyo_map;  // POOL: dy_out viewed {32, N*Ho*Wo}, box {32, 256}, SWIZZLE_128B_ATOM_32B (= dyS layout)
+  const float* dy;      // !POOL: the layer's output gradient [N][Ho][Wo][32]
+  float* dy_out;        // POOL: the pool's dx (= the layer's dy) [N][Ho][Wo][32]
+  const float* gpool;   // POOL: pool output gradient [N][Hq][Wq][32]
+  const uint8_t* mask;  // POOL: argmax window offsets [N][Hq][Wq][32]
+  float* part;          // [gridDim][32 * Kg + 32]
+  int nimg, Ho, Wo, Wp, Hp, R, S, T, pad, kblocks;
+  int pk, ps, Hq, Wq;  // pooling window, stride, output size (pad 0)
+  int rn;              // round dy to TF32 (reading A19: it is a GEMM operand)
+  FastDiv fWo, fS, fps, fpk;
+};
+
+template <bool POOL>
+__global__ void __launch_bounds__(kI4WThreads, 1) conv_img4_wgrad_kernel(const __grid_constant__ Img4WgradArgs a) {
+  constexpr int NB = 32;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t img = base;
+  const uint32_t img_bytes = ((uint32_t)a.Hp * a.Wp * 16 + 1023u) & ~1023u;
+  const uint32_t dyS = img + img_bytes;
+  const uint32_t dy_bytes = (uint32_t)a.kblocks * kI4WKB * 128;
+  const uint32_t stage_bytes = 4 * kI4WKB * 128;  // 4 MN atoms (kg 0..127) x 32 k-lines
+  const uint32_t abuf = dyS + dy_bytes;
+  const uint32_t bars = abuf + kI4WStages * stage_bytes;
+  // img_bar, dy_ready, img_done, full[S], empty[S], slot
+  const uint32_t img_bar = bars, dy_ready = bars + 8, img_done = bars + 16;
+  const uint32_t full0 = bars + 24, empty0 = full0 + 8 * kI4WStages, pool_bar = empty0 + 8 * kI4WStages;
+  const uint32_t slot = pool_bar + 8;
+  // POOL: the pool's output gradient and argmax of the sample are staged in the A stage buffers
+  const uint32_t gps = abuf, mks = abuf + (uint32_t)a.Hq * a.Wq * NB * 4;
+  uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
+  // warp index broadcast from lane 0: the compiler then treats role branches as
+  // warp-uniform and keeps the MMA issuer's descriptors in uniform registers
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+  const int HoWo = a.Ho * a.Wo, Kg = a.T * 4;
+  const int nmine = a.nimg > (int)blockIdx.x ? (a.nimg - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  // constant A rows (tap >= T): the ones row (tap T, channel 0) and zeros, in every
+  // stage buffer (rewritten per sample: the buffers also stage the pool's inputs)
+  auto prefill = [&](int t0, int nt) {
+    for (int i = t0; i < kI4WStages * kI4WKB * (32 - a.T); i += nt) {
+      const int st = i / (kI4WKB * (32 - a.T)), rem = i - st * kI4WKB * (32 - a.T);
+      const int px = rem / (32 - a.T), t = a.T + rem % (32 - a.T);
+      const int at = t >> 3, lt = t & 7;
+      const uint32_t dst = abuf + st * stage_bytes + at * (kI4WKB * 128) + px * 128 + (((lt >> 1) ^ (px & 3)) << 5) +
+                           ((lt & 1) << 4);
+      const float one = t == a.T ? 1.f : 0.f;
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %2, %2};" ::"r"(dst), "f"(one), "f"(0.f) : "memory");
+    }
+  };
+  if (!POOL) prefill(tid, kI4WThreads);
+  fence_proxy_async_smem();
+  if (tid == 0) {
+    mbar_init(img_bar, 1);
+    mbar_init(dy_ready, kI4WProd);
+    mbar_init(img_done, 1);
+    mbar_init(pool_bar, 1);
+    for (int st = 0; st < kI4WStages; ++st) {
+      mbar_init(full0 + 8 * st, SG_I4W_FENCE == 1 ? 1 : kI4WProd / kI4WStages);  // one producer group per stage
+      mbar_init(empty0 + 8 * st, 1);
+    }
+    fence_barrier_init();
+    prefetch_tmap(&a.img_map);
+  }
+  constexpr int MMA_WARP = kI4WProd / 32;
+  if (warp == MMA_WARP) tmem_alloc<32>(slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot_ptr;
+  pdl_entry();
+  if (tid == 0) IMG_TRACE(5, 0);
+
+  if (warp == MMA_WARP) {
+    // ---------------- MMA issuer (whole warp, elected lane issues) ----------------
+    constexpr uint32_t idesc = idesc_tf32(128, NB, 1, 1);
+    int it = 0;
+    for (int i = 0; i < nmine; ++i) {
+      mbar_wait(dy_ready, i & 1);
+      tc_fence_after();
+      for (int j = 0; j < a.kblocks; ++j, ++it) {
+        const int st = it % kI4WStages;
+        mbar_wait(full0 + 8 * st, (it / kI4WStages) & 1);
+        tc_fence_after();
+        const uint32_t as = abuf + st * stage_bytes, bs = dyS + j * kI4WKB * 128;
+#pragma unroll
+        for (int kk = 0; kk < kI4WKB / 8; ++kk) {
+          const uint64_t ad = umma_desc_mn_sw128_32b(as + kk * 8 * 128, kI4WKB * 128, 512);
+          const uint64_t bd = umma_desc_mn_sw128_32b(bs + kk * 8 * 128, kI4WKB * 128, 512);
+          mma_tf32_warp(tmem, ad, bd, idesc, (i | j | kk) ? 1u : 0u);
+        }
+        mma_commit_warp(empty0 + 8 * st);
+        if (lane == 0) IMG_TRACE(2, j);
+      }
+      mma_commit_warp(img_done);  // this sample's MMAs done: dyS may be rebuilt
+    }
+    __syncwarp();
+  } else {
+    // ---------------- producers (kI4WProd threads) ----------------
+    // im2col work: the producer warps form 4 groups of 4 warps, group g builds the
+    // stages of iterations it = g (mod 4) (its own stage buffer), so the
+    // proxy fence + barrier arrive of one group overlaps the others' copies.
+    // A warp task = (atom a, 4 consecutive pixels) x 8 taps t = 8a + (lane & 7):
+    // its 4 k-lines of 128 B are written conflict-free; tap t >= T lanes idle.
+    const int grp = warp >> 2, gw = warp & 3;
+    constexpr int kMaxTask = 8;  // ceil(32 taps / 8) atoms x 8 pixel quads / 4 warps
+    // (task u of this warp: k = gw + 4u; all arrays indexed by unrolled constants -> registers)
+    int toff[kMaxTask], tdst[kMaxTask], tpx[kMaxTask];
+    const int natom = (a.T + 7) / 8;
+#pragma unroll
+    for (int u = 0; u < kMaxTask; ++u) {
+      const int k = gw + 4 * u;
+      const int at = k / (kI4WKB / 4), px = (k % (kI4WKB / 4)) * 4 + (lane >> 3), lt = lane & 7;
+      const int t = at * 8 + lt;
+      const int r = a.fS.div(t), sc = t - r * a.S;
+      toff[u] = (at < natom && t < a.T) ? r * a.Wp + sc : -1;
+      tdst[u] = at * (kI4WKB * 128) + px * 128 + (((lt >> 1) ^ (px & 3)) << 5) + ((lt & 1) << 4);
+      tpx[u] = px;
+    }
+    int it = 0;
+    for (int i = 0; i < nmine; ++i) {
+      const int n = blockIdx.x + i * gridDim.x;
+      asm volatile("bar.sync 2, %0;" ::"n"(kI4WProd) : "memory");  // producers done with the previous sample's image
+      if (tid == 0) {
+        mbar_arrive_expect_tx(img_bar, (uint32_t)a.Hp * a.Wp * 16);
+        tma_load_4d(img, &a.img_map, 0, -a.pad, -a.pad, n, img_bar);
+      }
+      if (i > 0) mbar_wait(img_done, (i - 1) & 1);  // the previous sample's MMAs no longer read dyS / A
+      if (POOL && tid == 0) {
+        const uint32_t gb = (uint32_t)a.Hq * a.Wq * NB * 4, mb = (uint32_t)a.Hq * a.Wq * NB;
+        mbar_arrive_expect_tx(pool_bar, gb + mb);
+        bulk_g2s(gps, a.gpool + (size_t)n * a.Hq * a.Wq * NB, gb, pool_bar);
+        bulk_g2s(mks, a.mask + (size_t)n * a.Hq * a.Wq * NB, mb, pool_bar);
+      }
+      if (POOL) {
+        if (i > 0 && tid == 0) bulk_wait_read0();  // the previous sample's dy_out store has read dyS
+        asm volatile("bar.sync 2, %0;" ::"n"(kI4WProd) : "memory");
+      }
+      if (tid == 0) IMG_TRACE(0, 0);
+      // ---- dy of this sample into dyS (and, fused, the pool's dx blob) ----
+      const int nchunk = a.kblocks * kI4WKB * 8;  // (pixel, 4 channels) chunks incl. the zero tail
+      auto dys_addr = [&](int q, int co) {        // MN-major SWIZZLE_128B_BASE32B, k-line = pixel
+        return dyS + q * 128 + ((((uint32_t)co >> 3) ^ (q & 3)) << 5) + (co & 7) * 4;
+      };
+      if (POOL) {
+        // max-pool backward (a13) as 4 scatter passes over the windows of one
+        // (oh mod 2, ow mod 2) class: with k <= 2s windows of a class never
+        // overlap, so every pass is race-free, and a pixel receives its windows'
+        // gradients in the class order (= maxpool_bwd_kernel's summation order)
+        for (int e = tid; e < nchunk; e += kI4WProd)
+          asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(dys_addr(e >> 3, (e & 7) * 4)), "f"(0.f)
+                       : "memory");
+        mbar_wait(pool_bar, i & 1);
+        for (int pass = 0; pass < 4; ++pass) {
+          asm volatile("bar.sync 2, %0;" ::"n"(kI4WProd) : "memory");
+          if (tid == 0) IMG_TRACE(0, 3 + pass);
+          const int po = pass >> 1, pw = pass & 1;
+          const int noh = (a.Hq - po + 1) >> 1, now_ = (a.Wq - pw + 1) >> 1;
+          for (int e = tid; e < noh * now_ * 8; e += kI4WProd) {
+            const int c4 = e & 7, wi = e >> 3;
+            const int ohi = wi / now_, owi = wi - ohi * now_;
+            const int oh = 2 * ohi + po, ow = 2 * owi + pw;
+            const uint32_t o = (uint32_t)(oh * a.Wq + ow) * NB + c4 * 4;
+            uint32_t mw;
+            float g[4];
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mw) : "r"(mks + o));
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(g[0]), "=f"(g[1]), "=f"(g[2]), "=f"(g[3])
+                         : "r"(gps + o * 4));
+            uint32_t ad[4];
+            float v[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {  // 4 distinct channels: distinct addresses, loads first
+              const int off = (mw >> (8 * c)) & 255;
+              const int r = a.fpk.div(off), cc = off - r * a.pk;
+              const int q = (oh * a.ps + r) * a.Wo + ow * a.ps + cc;
+              ad[c] = dys_addr(q, c4 * 4 + c);
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[c]) : "r"(ad[c]));
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) asm volatile("st.shared.f32 [%0], %1;" ::"r"(ad[c]), "f"(v[c] + g[c]) : "memory");
+          }
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(kI4WProd) : "memory");
+        if (tid == 0) IMG_TRACE(0, 7);
+        // TF32 rounding (the conv's dy is a GEMM operand); the materialised blob
+        // (the pool's dx) is written from dyS by a TMA store once dy is complete
+        if (a.rn)
+          for (int e = tid; e < HoWo * 8; e += kI4WProd) {
+            const uint32_t ad = dys_addr(e >> 3, (e & 7) * 4);
+            float4 v;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                         : "r"(ad)
+                         : "memory");
+            v = tf32_rna4(v);
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ad), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                         : "memory");
+          }
+      } else {
+        for (int e = tid; e < nchunk; e += kI4WProd) {
+          const int q = e >> 3, c4 = e & 7;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (q < HoWo) v = __ldg(reinterpret_cast<const float4*>(a.dy) + ((size_t)n * HoWo + q) * 8 + c4);
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dys_addr(q, c4 * 4)), "f"(v.x), "f"(v.y),
+                       "f"(v.z), "f"(v.w)
+                       : "memory");
+        }
+      }
+      if (POOL) {
+        if (tid == 0) IMG_TRACE(0, 8);
+        asm volatile("bar.sync 2, %0;" ::"n"(kI4WProd) : "memory");  // the staged pool inputs are consumed
+        if (tid == 0) IMG_TRACE(0, 9);
+        prefill(tid, kI4WProd);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(dy_ready);
+      if (POOL && tid == 0) {  // dy_out <- dyS (TMA store un-swizzles; overlaps the MMA phase)
+        mbar_wait(dy_ready, i & 1);
+        for (int r0 = 0; r0 < HoWo; r0 += 256) tma_store_2d(&a.dyo_map, 0, n * HoWo + r0, dyS + r0 * 128);
+        bulk_commit();
+      }
+      if (tid == 0) IMG_TRACE(0, 1);
+      mbar_wait(img_bar, i & 1);
+      if (tid == 0) IMG_TRACE(0, 2);
+      // ---- im2col A stages (group grp: iterations it = grp mod 4) ----
+      const int it0 = it;
+      it += a.kblocks;
+      for (int j = (grp - it0 % kI4WStages + kI4WStages) % kI4WStages; j < a.kblocks; j += kI4WStages) {
+        const int itj = it0 + j, st = grp;
+        if (itj >= kI4WStages) mbar_wait(empty0 + 8 * st, ((itj / kI4WStages) - 1) & 1);
+        const uint32_t as = abuf + st * stage_bytes;
+#pragma unroll
+        for (int u = 0; u < kMaxTask; ++u) {
+          if (toff[u] < 0) continue;
+          const int q = j * kI4WKB + tpx[u];
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (q < HoWo) {
+            const int oh = a.fWo.div(q), ow = q - oh * a.Wo;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                         : "r"(img + (uint32_t)(oh * a.Wp + ow + toff[u]) * 16));
+          }
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(as + tdst[u]), "f"(v.x), "f"(v.y), "f"(v.z),
+                       "f"(v.w)
+                       : "memory");
+        }
+#ifndef SG_I4W_FENCE
+#define SG_I4W_FENCE 0
+#endif
+#if SG_I4W_FENCE == 0
+        fence_proxy_async_smem();
+        mbar_arrive(full0 + 8 * st);
+#elif SG_I4W_FENCE == 1
+        asm volatile("bar.sync %0, 128;" ::"r"(4 + grp) : "memory");
+        if ((tid & 127) == 0) {
+          fence_proxy_async_smem();
+          mbar_arrive(full0 + 8 * st);
+        }
+#else
+        mbar_arrive(full0 + 8 * st);
+#endif
+        if (tid == 0) IMG_TRACE(1, j);
+      }
+    }
+    // ---------------- epilogue: the CTA's partial dW / db ----------------
+    if (warp < 4) {
+      if (nmine > 0) mbar_wait_sleep(img_done, (nmine - 1) & 1);
+      if (tid == 0) IMG_TRACE(3, 0);
+      tc_fence_after();
+      const int kg = warp * 32 + lane;
+      float* out = a.part + (size_t)blockIdx.x * (NB * Kg + NB);
+#pragma unroll 1
+      for (int c0 = 0; c0 < NB; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+        if (nmine == 0) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = 0.f;
+        }
+        if (kg < Kg) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) out[(size_t)(c0 + k) * Kg + kg] = v[k];
+        } else if (kg == Kg) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) out[(size_t)NB * Kg + c0 + k] = v[k];
+        }
+      }
+    }
+  }
+  if (POOL && tid == 0) bulk_wait0();  // dy_out fully written before the CTA exits
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc<32>(tmem);
+  }
+}
+
+bool plan_img4_wgrad(const ConvShape& s, Img4WgradArgs* a, size_t* smem) {
+  if (!img_conv_enabled() || s.C != 4 || s.st != 1 || s.Co != 32) return false;
+  Img4WgradArgs g{};
+  g.R = s.R, g.S = s.S, g.T = s.R * s.S, g.pad = s.pad;
+  g.Ho = s.Ho, g.Wo = s.Wo;
+  g.Wp = s.W + 2 * s.pad, g.Hp = s.H + 2 * s.pad;
+  if (g.T > 31 || g.Wp > 256 || g.Hp > 256) return false;
+  if (g.Wo + s.S - 1 != g.Wp || g.Ho + s.R - 1 != g.Hp) return false;  // "same"-geometry stride-1 layer
+  g.kblocks = (g.Ho * g.Wo + kI4WKB - 1) / kI4WKB;
+  g.nimg = s.N;
+  g.fWo = make_fastdiv(g.Wo);
+  g.fS = make_fastdiv(g.S);
+  const size_t img_bytes = ((size_t)g.Hp * g.Wp * 16 + 1023) & ~(size_t)1023;
+  *smem = 1024 + img_bytes + (size_t)g.kblocks * kI4WKB * 128 + (size_t)kI4WStages * 4 * kI4WKB * 128 + 256;
+  if (*smem > 227 * 1024) return false;
+  *a = g;
+  return true;
+}
+
+int img4_wgrad_ctas(int nimg) { return std::min(nimg, 148); }
+
+cudaError_t launch_img4_wgrad(Img4WgradArgs& a, size_t smem, const float* x, const ConvShape& s, bool pool,
+                              float* dW, float* db, cudaStream_t st) {
+  const cuuint64_t xd[4] = {4, (cuuint64_t)s.W, (cuuint64_t)s.H, (cuuint64_t)s.N};
+  const cuuint64_t xs[3] = {16, (cuuint64_t)s.W * 16, (cuuint64_t)s.H * s.W * 16};
+  const cuuint32_t xb[4] = {4, (cuuint32_t)a.Wp, (cuuint32_t)a.Hp, 1};
+  if (!encode_tiled_f32(&a.img_map, x, 4, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+  auto k = pool ? conv_img4_wgrad_kernel<true> : conv_img4_wgrad_kernel<false>;
+  static size_t set[2] = {0, 0};
+  if (smem > set[pool]) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set[pool] = smem;
+  }
+  const int ctas = img4_wgrad_ctas(s.N);
+  cudaError_t e = launch_k(k, ctas, kI4WThreads, smem, st, a);
+  if (e != cudaSuccess) return e;
+  const int nw = s.Co * a.T * 4, per = nw + s.Co;
+  return launch_k(conv_wgrad_sum_kernel, (per + 31) / 32, 512, 0, st, (const float*)a.part, ctas, per, nw, dW, db);
+}
+
+}  // namespace
+
+bool conv_img4_wgrad_ok(const ConvShape& s) {
+  Img4WgradArgs a;
+  size_t smem;
+  return plan_img4_wgrad(s, &a, &smem);
+}
+
+size_t conv_img4_wgrad_ws_floats(const ConvShape& s) {
+  Img4WgradArgs a;
+  size_t smem;
+  if (!plan_img4_wgrad(s, &a, &smem)) return 0;
+  return 1024 + (size_t)img4_wgrad_ctas(s.N) * (size_t)(s.Co * a.T * 4 + s.Co);
+}
+
+cudaError_t conv_img4_wgrad(const ConvShape& s, const float* x, const float* dy, float* dW, float* db, Workspace ws,
+                            cudaStream_t st) {
+  Img4WgradArgs a;
+  size_t smem;
+  if (!plan_img4_wgrad(s, &a, &smem) || ws.floats < conv_img4_wgrad_ws_floats(s)) return cudaErrorInvalidValue;
+  a.dy = dy;
+  a.part = ws.ptr + 1024;
+  return launch_img4_wgrad(a, smem, x, s, false, dW, db, st);
+}
+
+bool conv_img4_pool_bwd_ok(const ConvShape& s, const PoolShape& p) {
+  return conv_img4_wgrad_ok(s) && p.p == 0 && p.N == s.N && p.H == s.Ho && p.W == s.Wo && p.C == s.Co &&
+         p.k * p.k <= 256 && p.k <= 2 * p.s && (size_t)p.Ho * p.Wo * s.Co * 5 <= (size_t)kI4WStages * 4 * kI4WKB * 128 &&
+         (s.Ho * s.Wo) % 256 == 0;  // whole 256-pixel TMA store boxes per sample
+}
+
+cudaError_t conv_img4_pool_bwd(const ConvShape& s, const PoolShape& p, const float* x, const float* gpool,
+                               const uint8_t* mask, float* dy_out, int rn, float* dW, float* db, Workspace ws,
+                               cudaStream_t st) {
+  Img4WgradArgs a;
+  size_t smem;
+  if (!conv_img4_pool_bwd_ok(s, p) || !plan_img4_wgrad(s, &a, &smem) || ws.floats < conv_img4_wgrad_ws_floats(s))
+    return cudaErrorInvalidValue;
+  a.gpool = gpool;
+  a.mask = mask;
+  a.dy_out = dy_out;
+  {
+    const cuuint64_t dd[2] = {32, (cuuint64_t)s.N * s.Ho * s.Wo};
+    const cuuint64_t ds[1] = {32 * 4};
+    const cuuint32_t db[2] = {32, 256};
+    if (!encode_tiled_f32(&a.dyo_map, dy_out, 2, dd, ds, db, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+      return cudaErrorInvalidValue;
+  }
+  a.rn = rn;
+  a.pk = p.k, a.ps = p.s, a.Hq = p.Ho, a.Wq = p.Wo;
+  a.fps = make_fastdiv(p.s);
+  a.fpk = make_fastdiv(p.k);
+  a.part = ws.ptr + 1024;
+  return launch_img4_wgrad(a, smem, x, s, true, dW, db, st);
+}
+
 }  // namespace sg
 
 #ifdef SG_GEMM_TRACE

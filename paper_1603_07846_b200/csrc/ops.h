@@ -85,6 +85,20 @@ cudaError_t conv_img_wgrad(const ConvShape& s, const float* x, const float* dy, 
                            cudaStream_t st);
 
 
+// 4-channel stride-1 first layer (CIFAR conv1) weight / bias gradient on the
+// resident image (conv_img.cu): from dy, or fused with the backward of the
+// max-pooling layer that consumes the convolution (dy = the pool's dx is built
+// in shared memory and written to dy_out, TF32-rounded when rn).
+bool conv_img4_wgrad_ok(const ConvShape& s);
+size_t conv_img4_wgrad_ws_floats(const ConvShape& s);
+cudaError_t conv_img4_wgrad(const ConvShape& s, const float* x, const float* dy, float* dW, float* db, Workspace ws,
+                            cudaStream_t st);
+struct PoolShape;
+bool conv_img4_pool_bwd_ok(const ConvShape& s, const PoolShape& p);
+cudaError_t conv_img4_pool_bwd(const ConvShape& s, const PoolShape& p, const float* x, const float* gpool,
+                               const uint8_t* mask, float* dy_out, int rn, float* dW, float* db, Workspace ws,
+                               cudaStream_t st);
+
 // ---- convolution (implicit GEMM, tcgen05 kind::tf32) ----
 // flags: EPI_RELU | EPI_RN
 cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const float* b, float* y, int flags,

@@ -146,7 +146,11 @@ __device__ __forceinline__ void pool_windows(int hp, int k, int Ho, const FastDi
 }
 
 // Gather form of the backward: thread per input (n, h, w, 4 channels) sums dy
-// of every window whose argmax is this element, windows in ascending (oh, ow).
+// of every window whose argmax is this element.  Fixed summation order: with
+// k <= 2s (at most 2 x 2 windows per element) the windows are taken in order of
+// (oh mod 2, ow mod 2) -- even rows first, even columns first -- which is the
+// order of the scatter passes of the fused first-layer backward
+// (conv_img.cu), so both give the same bits; otherwise ascending (oh, ow).
 __global__ void maxpool_bwd_kernel(PoolK P, const float* __restrict__ dy, const uint8_t* __restrict__ arg,
                                    float* __restrict__ dx, const float* __restrict__ relu_y,
                                    float* __restrict__ dx_relu, int rn) {
@@ -171,21 +175,24 @@ __global__ void maxpool_bwd_kernel(PoolK P, const float* __restrict__ dy, const 
       if (a.z == off) acc.z += g.z;
       if (a.w == off) acc.w += g.w;
     };
-    if (oh1 - oh0 <= 1 && ow1 - ow0 <= 1) {
-      // at most 2 x 2 windows (k <= 2s): issue all loads first, add in (oh, ow) order
+    if (s.k <= 2 * s.s) {
+      // at most 2 x 2 windows: issue all loads first, add in (oh mod 2, ow mod 2) order
       uchar4 a[4];
       float4 g[4];
+      int whs[4], wws[4];
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        const int oh = oh0 + (w >> 1), ow = ow0 + (w & 1);
+        const int oh = oh0 + ((w >> 1) ^ (oh0 & 1)), ow = ow0 + ((w & 1) ^ (ow0 & 1));
         const bool ok = oh <= oh1 && ow <= ow1;
+        whs[w] = ok ? oh : -1;
+        wws[w] = ow;
         const size_t o = nb + (size_t)(ok ? oh * s.Wo + ow : 0) * s.C;
         a[w] = ok ? __ldg(reinterpret_cast<const uchar4*>(arg + o)) : make_uchar4(255, 255, 255, 255);
         g[w] = ok ? __ldg(reinterpret_cast<const float4*>(dy + o)) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int w = 0; w < 4; ++w)
-        if (oh0 + (w >> 1) <= oh1 && ow0 + (w & 1) <= ow1) add(oh0 + (w >> 1), ow0 + (w & 1), a[w], g[w]);
+        if (whs[w] >= 0) add(whs[w], wws[w], a[w], g[w]);
     } else {
       for (int oh = oh0; oh <= oh1; ++oh)
         for (int ow = ow0; ow <= ow1; ++ow) {

@@ -667,6 +667,8 @@ cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, floa
   const int Kg = s.R * s.S * s.C, Mtot = s.N * s.Ho * s.Wo;
   if (conv_img_wgrad_ok(s) && ws.floats >= conv_img_wgrad_ws_floats(s) && aligned16p(x) && aligned16p(dy))
     return conv_img_wgrad(s, x, dy, dW, db, ws, st);
+  if (conv_img4_wgrad_ok(s) && ws.floats >= conv_img4_wgrad_ws_floats(s) && aligned16p(x) && aligned16p(dy))
+    return conv_img4_wgrad(s, x, dy, dW, db, ws, st);
   // D[kg][co] stored transposed into dW[co][kg]; row Kg (ones) = db
   EpiArgs e = epi_plain(dW, Kg, 1, nullptr, 0, 0, Kg);
   if (db) {

@@ -83,6 +83,8 @@ struct sg_net {
   std::vector<int> relu_into;   // consumer c -> ReLU layer whose backward c's kernel also does (or -1)
   std::vector<char> bwd_fused_away;  // ReLU layer whose backward is done by its consumer
   std::vector<int> lrn_after;   // pool i -> LRN layer computed by the pool's forward kernel (or -1)
+  std::vector<int> pool_into;   // first-layer conv i -> max pool whose backward its weight-gradient kernel does (or -1)
+  std::vector<char> pool_bwd_fused;  // max pool whose backward is done by its source conv's kernel
   std::vector<char> lrn_fused;  // LRN layer whose forward is done by the pool before it
   cudaGraphExec_t gexec = nullptr;
   sg_updater* graph_upd = nullptr;
@@ -293,7 +295,13 @@ sg_status backward(sg_net* n, int i) {
   prof_mark(n, s1, 0, st);
   switch (L.kind) {
     case SG_CONV:
-      SG_LCH(conv_wgrad(conv_shape(L, S), n->data[L.src], n->grad[i], dW, db, n->ws, st));
+      if (n->pool_into[i] >= 0) {  // fused: the max pool's backward builds this layer's dy (a13 + a15)
+        const int c = n->pool_into[i];
+        SG_LCH(conv_img4_pool_bwd(conv_shape(L, S), pool_shape(P.layers[c], L), n->data[L.src], n->grad[c],
+                                  n->mask[c], n->grad[i], L.rn_grad, dW, db, n->ws, st));
+      } else {
+        SG_LCH(conv_wgrad(conv_shape(L, S), n->data[L.src], n->grad[i], dW, db, n->ws, st));
+      }
       prof_mark(n, s1, 1, st);
       if (need_dx) {
         prof_mark(n, s2, 0, st);
@@ -308,7 +316,7 @@ sg_status backward(sg_net* n, int i) {
       const int j = n->relu_into[i];
       const float* ry = j >= 0 ? n->data[j] : nullptr;
       float* dxr = j >= 0 ? n->grad[P.layers[j].src] : nullptr;
-      if (!need_dx) break;
+      if (!need_dx || n->pool_bwd_fused[i]) break;
       const int rn = rn_dx | (j >= 0 && P.layers[P.layers[j].src].rn_grad ? RN_AUX : 0);
       if (L.kind == SG_POOL_MAX)
         SG_LCH(maxpool_bwd(pool_shape(L, S), n->grad[i], n->mask[i], n->grad[L.src], st, ry, dxr, rn));
@@ -603,6 +611,8 @@ void apply_fusion(sg_net* n) {
   n->bwd_fused_away.assign(nl, 0);
   n->lrn_after.assign(nl, -1);
   n->lrn_fused.assign(nl, 0);
+  n->pool_into.assign(nl, -1);
+  n->pool_bwd_fused.assign(nl, 0);
   if (!n->fuse) return;
   std::vector<int> consumers(nl, 0), consumer(nl, -1);
   for (int c = 0; c < nl; ++c)
@@ -655,6 +665,18 @@ void apply_fusion(sg_net* n) {
     if (!pool_lrn_fusable(pool_shape(Lp, P.layers[Lp.src]), ls)) continue;
     n->lrn_after[pool] = k;
     n->lrn_fused[k] = 1;
+  }
+  // first-layer convolution -> max pool: the pool's backward runs inside the
+  // convolution's weight-gradient kernel (conv_img4_pool_bwd)
+  for (int i = 0; i < nl; ++i) {
+    const LayerPlan& L = P.layers[i];
+    if (L.kind != SG_CONV || L.src < 0 || P.layers[L.src].kind != SG_INPUT || consumers[i] != 1) continue;
+    const int c = consumer[i];
+    const LayerPlan& Lc = P.layers[c];
+    if (Lc.kind != SG_POOL_MAX || n->relu_into[c] >= 0) continue;
+    if (!conv_img4_pool_bwd_ok(conv_shape(L, P.layers[L.src]), pool_shape(Lc, L))) continue;
+    n->pool_into[i] = c;
+    n->pool_bwd_fused[c] = 1;
   }
 }
 
@@ -717,6 +739,7 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
       need(gemm_ws_floats((int)(L.rows * S.h * S.w), S.c, L.kernel * L.kernel * L.c));
       need(colsum_ws_floats((int)(L.rows * L.h * L.w), L.c));
       need(conv_img_wgrad_ws_floats(conv_shape(L, S)));
+      need(conv_img4_wgrad_ws_floats(conv_shape(L, S)));
     }
     if (L.kind == SG_INNER_PRODUCT) {
       need(gemm_ws_floats((int)L.rows, (int)L.nout, (int)L.kin));

@@ -137,6 +137,23 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* map, int c
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
 }
+// TMA tensor store shared -> global (2-D box), tracked by the bulk async-group
+// of the issuing thread: commit, then wait until the smem has been read.
+__device__ __forceinline__ void tma_store_2d(const void* map, int c0, int c1, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// Contiguous global -> shared bulk copy (TMA, no tensor map): bytes % 16 == 0,
+// both addresses 16-byte aligned; completes `bytes` transactions on `bar`.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 // NHWC im2col box: coordinates {c, w, h, n} of the first output pixel's window
 // origin, filter-tap offsets {s, r}.
 __device__ __forceinline__ void tma_load_im2col(uint32_t dst, const void* map, int c, int w, int h, int n, int s,
@@ -205,6 +222,32 @@ __device__ __forceinline__ void mma_tf32_lh(uint32_t tmem_d, uint32_t alo, uint3
       " tcgen05.mma.cta_group::1.kind::tf32 [%0], ad, bd, %5, p;\n"
       "}\n" ::"r"(tmem_d),
       "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(accumulate));
+}
+// Whole-warp forms: every lane of the warp executes the call with the SAME
+// (warp-uniform) operands and elect.sync picks the one lane that issues.  Keeping
+// the issuing code in uniform control flow lets the compiler hold the
+// descriptors in uniform registers; a loop inside `if (lane == 0)` with
+// data-dependent control flow measured ~300 cycles per MMA instead of ~60-75
+// (tools/mma_layout_rate.cu).
+__device__ __forceinline__ void mma_tf32_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, p;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_warp(uint32_t bar) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(bar)
+      : "memory");
 }
 // Arrive on an mbarrier when all previously issued tcgen05 ops of this thread complete.
 __device__ __forceinline__ void mma_commit(uint32_t bar) {

@@ -325,9 +325,12 @@ def test_alg1_layer_by_layer_api_matches_train_one_batch():
         c.close()
 
 
-def test_relu_fusion_bit_exact():
-    net = configs.alexnet(hybrid=False)
-    b = 2
+@pytest.mark.parametrize("name,b", [("alexnet", 2), ("cifar10", 16)])
+def test_relu_fusion_bit_exact(name, b):
+    """Layer fusion (fused ReLU epilogues, pool [-> ReLU] -> LRN, ReLU backward in
+    the consumer, the first conv's weight gradient with the max pool's backward)
+    gives the same bits as the unfused layer-by-layer kernels."""
+    net = configs.alexnet(hybrid=False) if name == "alexnet" else configs.get(name)
     runs = [Run(net, b), Run(net, b)]
     runs[1].n.set_fusion(False)
     try:

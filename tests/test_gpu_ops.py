@@ -43,6 +43,8 @@ def test_gemm(M, N, K, ta, tb):
 CONV = [  # N, H, W, C, Co, R, stride, pad
     (4, 32, 32, 4, 32, 5, 1, 2),      # CIFAR conv1 (C padded to 4): direct CUDA-core path
     (3, 12, 10, 4, 8, 3, 1, 1),       # direct path, ragged Wo (10 = 2 x 4 + 2)
+    (150, 8, 8, 4, 32, 5, 1, 2),      # 4-channel resident-image weight gradient: 150 samples on 148 CTAs
+    (5, 7, 9, 4, 32, 3, 1, 1),        # ... ragged last 32-pixel stage (63 pixels)
     (4, 16, 16, 32, 32, 5, 1, 2),     # CIFAR conv2
     (8, 8, 8, 32, 64, 5, 1, 2),       # CIFAR conv3
     (3, 10, 7, 32, 32, 3, 1, 1),      # resident-image path, non-square, 3x3

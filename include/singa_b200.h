@@ -268,6 +268,27 @@ typedef struct {
 SG_API sg_status sg_plan_num_buckets(const sg_plan* p, int32_t* n, int64_t* padded_sizes /* cap n or NULL */);
 SG_API sg_status sg_plan_shard_map(const sg_plan* p, sg_shard_range* out, int32_t cap, int32_t* n);
 
+/* ---- Partitioning cost model (§5.4.1) ----
+ * Elements transferred per worker per iteration by one layer with p Params,
+ * per-sample visible / hidden feature lengths d_v / d_h, effective mini-batch
+ * b (summed over workers) and K workers: data parallelism p; model parallelism
+ * partitioned on hidden b*d_v, on visible b*d_h; no partitioning
+ * b*(K-1)*d_v/K (integer division); 0 for every strategy at K = 1.
+ * SG_ERR_INVALID_ARG for negative sizes, b < 1, K < 1 or an unknown strategy. */
+enum { SG_STRAT_DATA = 0, SG_STRAT_MODEL_HIDDEN = 1, SG_STRAT_MODEL_VISIBLE = 2, SG_STRAT_NONE = 3 };
+SG_API sg_status sg_layer_cost(int64_t p, int64_t d_v, int64_t d_h, int64_t b, int32_t K, int32_t strategy,
+                               int64_t* cost);
+/* Minimum-total-cost partition_dim per user layer for K workers at the
+ * config's global batch: exhaustive search over data / model parallelism of
+ * every conv / inner-product layer (model = the cheaper of the hidden /
+ * visible variants); pooling and LRN data parallel, element-wise layers inherit
+ * their source, a softmax loss is dim 0; ties toward data parallelism.
+ * dims[nlayers] receives 0 / 1 (directly usable as sg_layer_cfg.partition_dim),
+ * strategy[nlayers] / cost[nlayers] (may be NULL) the per-layer choice and
+ * cost, *total the plan's cost.  SG_ERR_CONFIG beyond 24 parameterised layers. */
+SG_API sg_status sg_recommend_plan(const sg_net_cfg* cfg, int32_t K, int32_t* dims, int32_t* strategy, int64_t* cost,
+                                   int64_t* total);
+
 /* ---- The net on the device ---- */
 typedef struct sg_net sg_net;
 /* COLLECTIVE (world > 1).  Plans (as sg_plan_create with the cluster's rank /

@@ -113,6 +113,8 @@ SIGS = {
     "sg_cluster_framework": [P, C.POINTER(C.c_char_p)],
     "sg_cluster_destroy": [P],
     "sg_plan_create": [C.POINTER(NetCfg), I32, I32, C.POINTER(P)],
+    "sg_layer_cost": [I64, I64, I64, I64, I32, I32, PI64],
+    "sg_recommend_plan": [C.POINTER(NetCfg), I32, PI32, PI32, PI64, PI64],
     "sg_plan_destroy": [P],
     "sg_plan_num_layers": [P, PI32],
     "sg_plan_layer_info": [P, I32, C.POINTER(LayerInfo)],

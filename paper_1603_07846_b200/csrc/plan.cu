@@ -469,6 +469,103 @@ using namespace sg;
 
 extern "C" {
 
+// ------------------------------------------------------------ cost model --
+// PAPER.md §5.4.1: elements transferred per worker per iteration.
+SG_API sg_status sg_layer_cost(int64_t p, int64_t d_v, int64_t d_h, int64_t b, int32_t K, int32_t strategy,
+                               int64_t* cost) {
+  SG_CHECK(cost, SG_ERR_INVALID_ARG, "sg_layer_cost: null output");
+  SG_CHECK(p >= 0 && d_v >= 0 && d_h >= 0 && b >= 1 && K >= 1, SG_ERR_INVALID_ARG,
+           "validation error: layer cost p=%lld d_v=%lld d_h=%lld b=%lld K=%d", (long long)p, (long long)d_v,
+           (long long)d_h, (long long)b, K);
+  SG_CHECK(strategy >= SG_STRAT_DATA && strategy <= SG_STRAT_NONE, SG_ERR_INVALID_ARG, "unknown strategy %d",
+           strategy);
+  if (K == 1) {
+    *cost = 0;
+  } else if (strategy == SG_STRAT_DATA) {
+    *cost = p;                                   // replicated Params exchanged
+  } else if (strategy == SG_STRAT_MODEL_HIDDEN) {
+    *cost = b * d_v;                             // whole visible features gathered
+  } else if (strategy == SG_STRAT_MODEL_VISIBLE) {
+    *cost = b * d_h;                             // partial hidden features combined
+  } else {
+    *cost = b * (K - 1) * d_v / K;               // no partitioning
+  }
+  return SG_OK;
+}
+
+// Exhaustive search over data / model parallelism of every parameterised layer
+// (S:564-571): pooling / LRN layers data parallel, element-wise layers
+// and the loss inherit their source's partitioning (a softmax loss: whole rows,
+// dim 0); ties toward data parallelism (lexicographically smallest dims).
+SG_API sg_status sg_recommend_plan(const sg_net_cfg* cfg, int32_t K, int32_t* dims, int32_t* strategy,
+                                   int64_t* cost, int64_t* total) {
+  SG_CHECK(cfg && dims && total && K >= 1, SG_ERR_INVALID_ARG, "sg_recommend_plan: bad argument");
+  Plan P;
+  SG_TRY(build_plan(cfg, 0, 1, &P));
+  const int nu = cfg->nlayers;
+  std::vector<int64_t> pz(nu, 0), dv(nu, 0), dh(nu, 0);
+  std::vector<int> kind(nu, 0), choose;
+  for (const LayerPlan& L : P.layers) {
+    if (L.user < 0) continue;
+    kind[L.user] = L.kind;
+    dv[L.user] = P.layers[L.src].feat;
+    dh[L.user] = L.feat;
+  }
+  for (const ParamPlan& q : P.params) pz[P.layers[q.layer].user] += q.rows * q.cols;
+  for (int i = 0; i < nu; ++i)
+    if (kind[i] == SG_CONV || kind[i] == SG_INNER_PRODUCT) choose.push_back(i);
+  SG_CHECK(choose.size() <= 24, SG_ERR_CONFIG, "config error: %zu parameterised layers (exhaustive search <= 24)",
+           choose.size());
+  const int64_t b = cfg->batch;
+  int64_t best = -1;
+  std::vector<int> bd(nu), bs(nu), cd(nu), cs(nu);
+  std::vector<int64_t> bc(nu), cc(nu);
+  const int64_t combos = 1LL << choose.size();
+  for (int64_t m = 0; m < combos; ++m) {
+    // bit (L-1-j) of m = strategy of the j-th parameterised layer: ascending m is lexicographic order
+    int cur = 0;
+    int64_t tot = 0;
+    size_t j = 0;
+    for (int i = 0; i < nu; ++i) {
+      int64_t c = 0;
+      int st = SG_STRAT_DATA;
+      if (j < choose.size() && choose[j] == i) {
+        cur = (int)((m >> (choose.size() - 1 - j)) & 1);
+        ++j;
+        if (cur == 0) {
+          SG_TRY(sg_layer_cost(pz[i], dv[i], dh[i], b, K, SG_STRAT_DATA, &c));
+        } else {
+          int64_t ch, cv;
+          SG_TRY(sg_layer_cost(pz[i], dv[i], dh[i], b, K, SG_STRAT_MODEL_HIDDEN, &ch));
+          SG_TRY(sg_layer_cost(pz[i], dv[i], dh[i], b, K, SG_STRAT_MODEL_VISIBLE, &cv));
+          c = ch <= cv ? ch : cv;
+          st = ch <= cv ? SG_STRAT_MODEL_HIDDEN : SG_STRAT_MODEL_VISIBLE;
+        }
+      } else {
+        if (kind[i] == SG_POOL_MAX || kind[i] == SG_POOL_AVG || kind[i] == SG_LRN || kind[i] == SG_SOFTMAX_CE) cur = 0;
+        st = cur == 0 ? SG_STRAT_DATA : SG_STRAT_MODEL_HIDDEN;
+      }
+      cd[i] = cur;
+      cs[i] = st;
+      cc[i] = c;
+      tot += c;
+    }
+    if (best < 0 || tot < best) {
+      best = tot;
+      bd = cd;
+      bs = cs;
+      bc = cc;
+    }
+  }
+  for (int i = 0; i < nu; ++i) {
+    dims[i] = bd[i];
+    if (strategy) strategy[i] = bs[i];
+    if (cost) cost[i] = bc[i];
+  }
+  *total = best;
+  return SG_OK;
+}
+
 SG_API sg_status sg_plan_create(const sg_net_cfg* cfg, int32_t rank, int32_t world, sg_plan** out) {
   SG_CHECK(out, SG_ERR_INVALID_ARG, "sg_plan_create: null output");
   sg_plan* p = new sg_plan();

@@ -148,6 +148,10 @@ SG_API sg_status sg_op_euclidean(const float* u_dev, const float* v_dev, int32_t
  * g' = s g + wd w ; v = mu v - lr g' ; w = w + v   (fp32, fixed FMA order). */
 SG_API sg_status sg_op_sgd_momentum(float* w_dev, const float* g_dev, float* v_dev, int64_t n, float lr, float mu,
                                     float wd, float s, void* stream);
+/* AdaGrad Updater ("such as AdaGrad"; reading A26):
+ * g' = s g + wd w ; h = h + g'^2 ; w = w - lr g' / (sqrt(h) + eps)  (fp32, fixed order). */
+SG_API sg_status sg_op_adagrad(float* w_dev, const float* g_dev, float* h_dev, int64_t n, float lr, float wd, float s,
+                               float eps, void* stream);
 
 /* ======================================================================
  * Cluster topology (AllReduce framework P:419-422).
@@ -319,7 +323,13 @@ typedef struct {
   int32_t lr_policy;  /* 0 fixed, 1 step: lr = base_lr * gamma^floor(step / step_size) */
   float gamma;
   int32_t step_size;
+  /* updating protocol: SG_UPD_SGD_MOMENTUM (default, uses momentum) or
+   * SG_UPD_ADAGRAD (the history buffer holds the squared-gradient accumulator h,
+   * momentum must be 0; eps <= 0 means 1e-8).  SG_ERR_CONFIG for other values. */
+  int32_t type;
+  float eps;
 } sg_updater_cfg;
+enum { SG_UPD_SGD_MOMENTUM = 0, SG_UPD_ADAGRAD = 1 };
 SG_API sg_status sg_updater_create(sg_net* n, const sg_updater_cfg* cfg, sg_updater** out);
 SG_API sg_status sg_updater_destroy(sg_updater* u);
 

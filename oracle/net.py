@@ -203,7 +203,7 @@ def train_one_batch(net, params, vel, x, labels, step, K, upd, return_blobs=Fals
     new_p, new_v = {}, {}
     for name, *_rest in pinfo:
         ls, ws = lscale[_rest[-1]]
-        new_p[name], new_v[name] = U.sgd_momentum(p64[name], vel[name], agg[name], upd, step, s, ls, ws)
+        new_p[name], new_v[name] = U.update(p64[name], vel[name], agg[name], upd, step, s, ls, ws)
     out = {"params": new_p, "vel": new_v, "loss": total / b, "grads": agg, "grad_scale": s}
     if return_blobs:
         out["workers"] = per_worker
@@ -332,9 +332,11 @@ def train_one_batch_partitioned(net, params, vel, x, labels, step, K, upd):
             dstate = new
     n_loc = inst[0][1]
     s = n_loc / b
+    lscale = {l["name"]: (l.get("lr_scale", 1.0), l.get("wd_scale", 1.0)) for l in net["layers"]}
     new_p, new_v = {}, {}
     for name, *_r in pinfo:
-        new_p[name], new_v[name] = U.sgd_momentum(p[name], vel[name], grads[name], upd, step, s)
+        ls, ws = lscale[_r[-1]]
+        new_p[name], new_v[name] = U.update(p[name], vel[name], grads[name], upd, step, s, ls, ws)
     return {"params": new_p, "vel": new_v, "loss": total / b, "grads": grads}
 
 

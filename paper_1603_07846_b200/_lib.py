@@ -81,7 +81,8 @@ class ShardRange(C.Structure):
 
 class UpdaterCfg(C.Structure):
     _fields_ = [("base_lr", C.c_float), ("momentum", C.c_float), ("weight_decay", C.c_float),
-                ("grad_scale", C.c_float), ("lr_policy", C.c_int32), ("gamma", C.c_float), ("step_size", C.c_int32)]
+                ("grad_scale", C.c_float), ("lr_policy", C.c_int32), ("gamma", C.c_float), ("step_size", C.c_int32),
+                ("type", C.c_int32), ("eps", C.c_float)]
 
 
 P = C.c_void_p
@@ -108,6 +109,7 @@ SIGS = {
     "sg_op_softmax_ce": [P, P, I32, I32, I32, P, P, P, P],
     "sg_op_euclidean": [P, P, I32, I32, I32, P, P, P],
     "sg_op_sgd_momentum": [P, P, P, I64, F32, F32, F32, F32, P],
+    "sg_op_adagrad": [P, P, P, I64, F32, F32, F32, F32, P],
     "sg_get_unique_id": [C.POINTER(C.c_uint8 * 128)],
     "sg_cluster_create": [C.POINTER(ClusterCfg), C.POINTER(P)],
     "sg_cluster_framework": [P, C.POINTER(C.c_char_p)],

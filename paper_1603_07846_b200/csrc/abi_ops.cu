@@ -308,4 +308,11 @@ SG_API sg_status sg_op_sgd_momentum(float* w, const float* g, float* v, int64_t 
   return SG_OK;
 }
 
+SG_API sg_status sg_op_adagrad(float* w, const float* g, float* h, int64_t n, float lr, float wd, float s, float eps,
+                               void* stream) {
+  SG_CHECK(w && g && h && n >= 0 && eps > 0.f, SG_ERR_INVALID_ARG, "adagrad: bad argument");
+  SG_LAUNCH(adagrad(w, g, h, n, lr, wd, s, eps, S(stream)));
+  return SG_OK;
+}
+
 }  // extern "C"

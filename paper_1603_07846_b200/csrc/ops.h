@@ -184,6 +184,12 @@ cudaError_t sgd_momentum(float* w, const float* g, float* v, long long n, float 
 cudaError_t sgd_momentum_dev(float* w, const float* g, float* v, long long n, const float* lr_dev, float lr_scale,
                              float mu, float wd, float s, cudaStream_t st, float* wk = nullptr, long long rn_end = 0);
 
+// ---- AdaGrad: g' = s g + wd w ; h += g'^2 ; w -= lr g' / (sqrt(h) + eps) ----
+cudaError_t adagrad(float* w, const float* g, float* h, long long n, float lr, float wd, float s, float eps,
+                    cudaStream_t st);
+cudaError_t adagrad_dev(float* w, const float* g, float* h, long long n, const float* lr_dev, float lr_scale, float wd,
+                        float s, float eps, cudaStream_t st, float* wk = nullptr, long long rn_end = 0);
+
 // ---- input layer: NHWC with C=3 (user layout) -> padded C=4 ----
 cudaError_t pad_channels(const float* x, float* y, long long pixels, int cin, int cout, cudaStream_t st, int rn = 0);
 // copy rows x cols fp32 (strided) — used for feature-blocked gathers on the host side of tests

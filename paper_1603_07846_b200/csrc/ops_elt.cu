@@ -641,6 +641,27 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, f
   }
 }
 
+// AdaGrad (reading A26), same working-copy convention as sgd_kernel.
+__device__ __forceinline__ void adagrad1(float& w, float g, float& h, float lr, float wd, float s, float eps) {
+  const float gp = __fmaf_rn(wd, w, __fmul_rn(s, g));
+  h = __fmaf_rn(gp, gp, h);
+  w = __fsub_rn(w, __fdiv_rn(__fmul_rn(lr, gp), __fadd_rn(__fsqrt_rn(h), eps)));
+}
+
+__global__ void adagrad_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ h,
+                               float* __restrict__ wk, long long rn_end, long long n, const float* lr_dev,
+                               float lr_scale, float lr_val, float wd, float s, float eps) {
+  pdl_entry();
+  const float lr = lr_dev ? lr_dev[0] * lr_scale : lr_val;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float ww = w[i], hh = h[i];
+    adagrad1(ww, g[i], hh, lr, wd, s, eps);
+    w[i] = ww;
+    h[i] = hh;
+    if (wk) wk[i] = i < rn_end ? tf32_rna(ww) : ww;
+  }
+}
+
 // ------------------------------------------------------------- input layer --
 __global__ void pad_channels_kernel(const float* __restrict__ x, float* __restrict__ y, long long pixels, int cin,
                                     int cout, int rn) {
@@ -807,6 +828,19 @@ cudaError_t sgd_momentum_dev(float* w, const float* g, float* v, long long n, co
   if (!aligned16(w) || !aligned16(g) || !aligned16(v) || (wk && !aligned16(wk))) return cudaErrorMisalignedAddress;
   return launch_k(sgd_kernel, blocks_for(n / 4 + 1, 256), 256, 0, st, w, g, v, wk, rn_end, n, lr_dev, lr_scale, 0.f,
                   mu, wd, s);
+}
+
+cudaError_t adagrad(float* w, const float* g, float* h, long long n, float lr, float wd, float s, float eps,
+                    cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  return launch_k(adagrad_kernel, blocks_for(n, 256), 256, 0, st, w, g, h, (float*)nullptr, 0LL, n,
+                  (const float*)nullptr, 1.f, lr, wd, s, eps);
+}
+cudaError_t adagrad_dev(float* w, const float* g, float* h, long long n, const float* lr_dev, float lr_scale, float wd,
+                        float s, float eps, cudaStream_t st, float* wk, long long rn_end) {
+  if (n <= 0) return cudaSuccess;
+  return launch_k(adagrad_kernel, blocks_for(n, 256), 256, 0, st, w, g, h, wk, rn_end, n, lr_dev, lr_scale, 0.f, wd,
+                  s, eps);
 }
 
 cudaError_t pad_channels(const float* x, float* y, long long pixels, int cin, int cout, cudaStream_t st, int rn) {

@@ -45,6 +45,7 @@ struct sg_cluster {
 struct sg_updater {
   sg_updater_cfg cfg;
   float s;
+  float eps;  // AdaGrad
 };
 
 struct sg_net {
@@ -87,7 +88,9 @@ struct sg_net {
   std::vector<char> pool_bwd_fused;  // max pool whose backward is done by its source conv's kernel
   std::vector<char> lrn_fused;  // LRN layer whose forward is done by the pool before it
   cudaGraphExec_t gexec = nullptr;
-  sg_updater* graph_upd = nullptr;
+  // the captured step bakes the Updater's hyper-parameters in by value: the
+  // graph is reused only for an updater with identical values
+  sg_updater graph_upd{};
   long long graph_launches = 0;
   long long last_launches = 0;
   // per-operation event timing (sg_net_profile)
@@ -387,9 +390,16 @@ sg_status update(sg_net* n, sg_updater* u, int i) {
     float* g = n->sgr[L.store];
     float* w = n->sw[L.store];
     SG_NCCL(ncclReduceScatter(g, g + P.rank * shard, (size_t)shard, ncclFloat, ncclSum, n->cl->comm_par, n->ps));
-    SG_LCH(sgd_momentum_dev(n->sm[L.store], g + P.rank * shard, n->sv[L.store], shard, n->lr_dev, L.lr_scale, mu, wd,
-                            u->s, n->ps, w + P.rank * shard, rn_end - P.rank * shard));
+    if (u->cfg.type == SG_UPD_ADAGRAD)
+      SG_LCH(adagrad_dev(n->sm[L.store], g + P.rank * shard, n->sv[L.store], shard, n->lr_dev, L.lr_scale, wd, u->s,
+                         u->eps, n->ps, w + P.rank * shard, rn_end - P.rank * shard));
+    else
+      SG_LCH(sgd_momentum_dev(n->sm[L.store], g + P.rank * shard, n->sv[L.store], shard, n->lr_dev, L.lr_scale, mu,
+                              wd, u->s, n->ps, w + P.rank * shard, rn_end - P.rank * shard));
     SG_NCCL(ncclAllGather(w + P.rank * shard, w, (size_t)shard, ncclFloat, n->cl->comm_par, n->ps));
+  } else if (u->cfg.type == SG_UPD_ADAGRAD) {
+    SG_LCH(adagrad_dev(n->sm[L.store], n->sgr[L.store], n->sv[L.store], S.padded, n->lr_dev, L.lr_scale, wd, u->s,
+                       u->eps, n->ps, n->sw[L.store], rn_end));
   } else {
     SG_LCH(sgd_momentum_dev(n->sm[L.store], n->sgr[L.store], n->sv[L.store], S.padded, n->lr_dev, L.lr_scale, mu, wd,
                             u->s, n->ps, n->sw[L.store], rn_end));
@@ -947,9 +957,13 @@ SG_API sg_status sg_updater_create(sg_net* n, const sg_updater_cfg* cfg, sg_upda
            (double)cfg->momentum, (double)cfg->weight_decay);
   SG_CHECK(cfg->lr_policy == 0 || (cfg->lr_policy == 1 && cfg->step_size > 0), SG_ERR_CONFIG,
            "updater: lr_policy=%d step_size=%d", cfg->lr_policy, cfg->step_size);
+  SG_CHECK(cfg->type == SG_UPD_SGD_MOMENTUM || (cfg->type == SG_UPD_ADAGRAD && cfg->momentum == 0.f), SG_ERR_CONFIG,
+           "updater: type=%d momentum=%g (AdaGrad takes no momentum)", cfg->type, (double)cfg->momentum);
   sg_updater* u = new sg_updater();
+  memset(u, 0, sizeof(*u));  // compared bytewise by the graph cache
   u->cfg = *cfg;
   u->s = cfg->grad_scale > 0.f ? cfg->grad_scale : PL(n).grad_scale;
+  u->eps = cfg->eps > 0.f ? cfg->eps : 1e-8f;
   *out = u;
   return SG_OK;
 }
@@ -1042,7 +1056,7 @@ SG_API sg_status sg_train_one_batch(sg_net* n, sg_updater* u, int64_t step, cons
   if (n->graph_on) {
     SG_TRY(set_input(n, x, labels));
     SG_TRY(forward(n, 0));  // input layer on the caller's buffer, then the captured rest of the step
-    if (!n->gexec || n->graph_upd != u) {
+    if (!n->gexec || memcmp(&n->graph_upd, u, sizeof(sg_updater)) != 0) {
       if (n->gexec) cudaGraphExecDestroy(n->gexec), n->gexec = nullptr;
       cudaGraph_t g;
       long long c0 = g_kernel_launches;
@@ -1057,7 +1071,7 @@ SG_API sg_status sg_train_one_batch(sg_net* n, sg_updater* u, int64_t step, cons
       cudaGraphDestroy(g);
       SG_CHECK(ce == cudaSuccess, SG_ERR_CUDA, "graph instantiation failed: %s", cudaGetErrorString(ce));
       n->graph_launches = g_kernel_launches - c0;
-      n->graph_upd = u;
+      n->graph_upd = *u;
     }
     SG_CUDA(cudaGraphLaunch(n->gexec, n->cs));
     n->last_launches = (g_kernel_launches - l0) + n->graph_launches;

@@ -55,6 +55,8 @@ def updater_cfg(upd, grad_scale=0.0):
     u.lr_policy = 1 if upd.get("lr_policy", "fixed") == "step" else 0
     u.gamma = upd.get("gamma", 1.0)
     u.step_size = upd.get("step_size", 1)
+    u.type = 1 if upd.get("type", "sgd_momentum") == "adagrad" else 0
+    u.eps = upd.get("eps", 0.0)
     return u
 
 

@@ -205,7 +205,7 @@ def check_layers(n, net, b, x, lab, p0, work0, grads, newp, work, upd, fused=Fal
     # Updater (layer-isolated): fp32 master from the GPU's own aggregated
     # gradient; working copy = TF32-RN(master) for weights, master for biases
     for name in p0:
-        w1, _ = OU.sgd_momentum(pm[name], np.zeros_like(pm[name]), f64(grads[name]), upd, 0, 1.0)
+        w1, _ = OU.update(pm[name], np.zeros_like(pm[name]), f64(grads[name]), upd, 0, 1.0)
         e = normwise(newp[name], w1)
         assert e < 1e-6, (name, e)
         want = newp[name] if name.endswith("/b") else rna_tf32(newp[name])
@@ -388,7 +388,7 @@ def check_layers_dist(n, net, b, x, lab, p0, work0, grads, newp, upd, rank, worl
     loss_dim = infos[-1]["partition_dim"]
     s = 1.0 / world if loss_dim == 0 else 1.0
     for name in p0:
-        w1, _ = OU.sgd_momentum(pm[name], np.zeros_like(pm[name]), f64(grads[name]), upd, 0, s)
+        w1, _ = OU.update(pm[name], np.zeros_like(pm[name]), f64(grads[name]), upd, 0, s)
         e = normwise(newp[name], w1)
         assert e < 1e-6, (name, e)
         rec(name, "update", e)

@@ -73,10 +73,11 @@ class Run:
         self.cl.close()
 
 
-def run_layer_isolated(net, b, cluster=None, fused=False, graph=False, sub=None):
+def run_layer_isolated(net, b, cluster=None, fused=False, graph=False, sub=None, upd=None):
     """One step, then every layer layer-isolated against the oracle
     (tests/layer_check.py).  Returns the set of layer kinds checked."""
-    run = Run(net, b, cluster=cluster, graph=graph)
+    upd = upd or configs.UPDATERS.get(net["name"]) or configs.UPDATERS[net["name"].split("_")[0]]
+    run = Run(net, b, upd=upd, cluster=cluster, graph=graph)
     run.n.set_fusion(fused)
     try:
         x, lab = generate.batch(net, b, 0)
@@ -84,7 +85,7 @@ def run_layer_isolated(net, b, cluster=None, fused=False, graph=False, sub=None)
         work0 = run.n.get_working(sh)
         run.step(0, x, lab)
         LC.check_layers(run.n, net, b, x, lab, run.p0, work0, run.n.get_grads(sh), run.n.get_params(sh),
-                        run.n.get_working(sh), configs.UPDATERS.get(net["name"]) or configs.UPDATERS[net["name"].split("_")[0]], fused=fused, sub=sub)
+                        run.n.get_working(sh), upd, fused=fused, sub=sub)
         return {li["kind"] for li in run.n.layer_info if li["kind"] != "input"}
     finally:
         run.close()
@@ -192,6 +193,47 @@ def test_diverged_is_reported():
         run.n.sync()                       # the flag is cleared once reported
     finally:
         run.close()
+
+
+ADAGRAD = {"base_lr": 0.01, "momentum": 0.0, "weight_decay": 5e-4, "lr_policy": "fixed", "type": "adagrad",
+           "eps": 1e-8}
+
+
+@pytest.mark.parametrize("name,b", [("mlp", 64), ("cifar10", 16)])
+def test_adagrad_layer_isolated_and_loss_curve(name, b):
+    """AdaGrad Updater (reading A26) in the training step: layer-isolated
+    Updater parity (master and TF32 working copy) and a 20-step free-running loss
+    within 1% of the oracle (A20)."""
+    net = configs.get(name)
+    run_layer_isolated(net, b, upd=ADAGRAD, fused=True, graph=True)
+    run = Run(net, b, upd=ADAGRAD, graph=True)
+    try:
+        p = {k: f64(v) for k, v in run.p0.items()}
+        h = {k: np.zeros_like(a) for k, a in p.items()}
+        for t in range(20):
+            x, lab = generate.batch(net, b, t)
+            gl = run.step(t, x, lab)
+            out = ON.train_one_batch(net, p, h, x, lab, t, 1, ADAGRAD)
+            assert abs(gl - out["loss"]) <= 0.01 * out["loss"], (t, gl, out["loss"])
+            p, h = out["params"], out["vel"]
+        hist = run.n.get_history(shapes_of(run.p0))
+        for k in hist:          # the accumulator is non-negative and tracks the oracle's
+            assert np.all(hist[k] >= 0) and normwise(hist[k], h[k]) < 5e-2, k
+    finally:
+        run.close()
+
+
+def test_adagrad_rejects_momentum():
+    net = configs.get("mlp")
+    cl = PN.Cluster(0, 1, 0)
+    n = PN.Net(cl, net, 64)
+    try:
+        with pytest.raises(L.SingaError) as e:
+            n.set_updater(dict(ADAGRAD, momentum=0.9))
+        assert e.value.name == "SG_ERR_CONFIG"
+    finally:
+        n.close()
+        cl.close()
 
 
 def test_mlp_whole_step_and_loss_curve():

@@ -259,6 +259,27 @@ def test_updater_vs_oracle_and_sharding():
     assert np.array_equal(host(w3), w)
 
 
+def test_adagrad_vs_oracle():
+    """AdaGrad Updater (reading A26) vs the float64 oracle
+    over 5 steps; S:418 first step -alpha*sign(g); zero gradient leaves w, h."""
+    n = (1 << 18) + 5
+    w, g = r32(n, scale=0.05), r32(n, scale=0.01)
+    cfg = {"base_lr": 0.01, "momentum": 0.0, "weight_decay": 5e-4, "lr_policy": "fixed", "type": "adagrad",
+           "eps": 1e-8}
+    wd_, gd, hd = dev(w), dev(g), dev(np.zeros(n, np.float32))
+    rw, rh = f64(w), np.zeros(n)
+    for t in range(5):
+        lib.sg_op_adagrad(ptr(wd_), ptr(gd), ptr(hd), n, 0.01, 5e-4, 0.5, 1e-8, None)
+        rw, rh = U.adagrad(rw, rh, f64(g), cfg, t, 0.5)
+    assert normwise(host(wd_), rw) < 1e-6 and normwise(host(hd), rh) < 1e-6
+    a, gg, hh = dev(np.zeros(4, np.float32)), dev(np.array([0.37, -2.5, 1e-3, 4.0], np.float32)), dev(np.zeros(4, np.float32))
+    lib.sg_op_adagrad(ptr(a), ptr(gg), ptr(hh), 4, 0.1, 0.0, 1.0, 1e-8, None)
+    assert np.allclose(host(a), -0.1 * np.sign([0.37, -2.5, 1e-3, 4.0]), atol=1e-6)
+    w0, h0 = dev(w), dev(np.abs(w))
+    lib.sg_op_adagrad(ptr(w0), ptr(dev(np.zeros(n, np.float32))), ptr(h0), n, 0.1, 0.0, 1.0, 1e-8, None)
+    assert np.array_equal(host(w0), w) and np.array_equal(host(h0), np.abs(w))
+
+
 def test_peer_sync_single_rank_vs_oracle_and_errors():
     """sg_peer_sync_* at K = 1 (no peers, no barriers): the fused exchange kernel
     is the Updater on the whole Param, s = grad_scale; bit-identical

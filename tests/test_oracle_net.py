@@ -171,3 +171,28 @@ def test_config_shapes():
     assert sum(int(np.prod(p[1])) for p in params) == 2823286
     _, params = N.setup(configs.AE_WIDE)
     assert sum(int(np.prod(p[1])) for p in params) == 92636800
+
+
+@pytest.mark.parametrize("updater", ["sgd_momentum", "adagrad"])
+def test_partition_transparency_with_multipliers_and_adagrad(updater):
+    """The partitioned data flow applies the per-layer lr / wd multipliers (reading
+    A23) and the configured Updater exactly like the unpartitioned step; a layer
+    with lr_scale 0 keeps its Params."""
+    net = copy.deepcopy(TINY_HYBRID)
+    net["layers"][0]["lr_scale"] = 0.0
+    for l in net["layers"]:
+        if l["kind"] == "ip":
+            l["lr_scale"], l["wd_scale"] = 2.0, 0.5
+            break
+    upd = dict(UPD, type=updater, eps=1e-8)
+    b, K = 8, 2
+    params, x, lab = make(net, b)
+    vel = {k: np.zeros_like(v, np.float64) for k, v in params.items()}
+    ref = N.train_one_batch(net, params, vel, x, lab, 0, K, upd)
+    part = N.train_one_batch_partitioned(net, params, vel, x, lab, 0, K, upd)
+    first = net["layers"][0]["name"]
+    for k in ref["params"]:
+        assert np.max(np.abs(ref["params"][k] - part["params"][k])) < 1e-12, k
+        assert np.max(np.abs(ref["vel"][k] - part["vel"][k])) < 1e-12, k
+        if k.startswith(first + "/"):
+            assert np.array_equal(ref["params"][k], np.asarray(params[k], np.float64)), k

@@ -64,6 +64,44 @@ def test_grad_scale():
     assert w[0] == -1.0
 
 
+def test_lr_wd_multipliers():
+    """Per-Param multipliers (reading A23): lr_scale = the base rate scaled, wd_scale =
+    the decay scaled, exactly (same arithmetic order)."""
+    rng = np.random.default_rng(3)
+    w0, g0 = rng.standard_normal(50), rng.standard_normal(50)
+    v0 = rng.standard_normal(50) * 0.1
+    a = U.sgd_momentum(w0, v0, g0, cfg(0.05, 0.9, 0.01), 0, 0.5, lr_scale=2.0, wd_scale=0.5)
+    b = U.sgd_momentum(w0, v0, g0, cfg(0.1, 0.9, 0.005), 0, 0.5)
+    assert np.allclose(a[0], b[0], rtol=0, atol=1e-15) and np.allclose(a[1], b[1], rtol=0, atol=1e-15)
+    w, v = U.sgd_momentum(w0, np.zeros(50), g0, cfg(0.05, 0.9, 0.01), 0, 1.0, lr_scale=0.0)
+    assert np.array_equal(w, w0)                       # lr_scale 0 freezes the Param
+
+
+def test_adagrad_first_step_is_sign():
+    """first update with gradient g, alpha 0.1, eps 1e-8 -> step -0.1 g / (|g| + eps) ~ -0.1 sign(g)."""
+    g = np.array([0.37, -2.5, 1e-3])
+    w, h = U.adagrad(np.zeros(3), np.zeros(3), g, cfg(0.1, eps=1e-8), 0, 1.0)
+    assert np.allclose(w, -0.1 * g / (np.abs(g) + 1e-8), rtol=0, atol=1e-17)
+    assert np.allclose(w, -0.1 * np.sign(g), atol=1e-6) and np.array_equal(h, g * g)
+
+
+def test_adagrad_constant_gradient_closed_form():
+    """constant gradient 1.0 -> cumulative displacement -alpha * sum_{i<=t} 1/(sqrt(i) + eps)."""
+    w, h = np.zeros(1), np.zeros(1)
+    alpha, eps = 0.05, 1e-8
+    for t in range(1, 60):
+        w, h = U.adagrad(w, h, np.ones(1), cfg(alpha, eps=eps), t, 1.0)
+        closed = -alpha * sum(1.0 / (np.sqrt(i) + eps) for i in range(1, t + 1))
+        assert abs(w[0] - closed) < 1e-13 and h[0] == t
+
+
+def test_adagrad_zero_gradient_unchanged():
+    """gradient 0 everywhere (no decay) -> value and accumulator unchanged."""
+    w0, h0 = np.random.default_rng(1).standard_normal(20), np.abs(np.random.default_rng(2).standard_normal(20))
+    w, h = U.adagrad(w0, h0, np.zeros(20), cfg(0.3, eps=1e-8), 0, 1.0)
+    assert np.array_equal(w, w0) and np.array_equal(h, h0)
+
+
 # ------------------------------------------------------------ partition -----
 @pytest.mark.parametrize("key", ["slice_rows", "slice_cols", "slice_remainder"])
 def test_partition_spec(key):

@@ -373,6 +373,16 @@ SG_API sg_status sg_net_enable_graph(sg_net* n, int32_t enable);
  *    the pool's backward (its dy) inside its weight-gradient kernel.
  * Every layer's data / grad blob is still written (sg_blob_get sees them). */
 SG_API sg_status sg_net_set_fusion(sg_net* n, int32_t enable);
+/* Gradient exchange of the sharded (dim-0) Param buckets (COLLECTIVE; call
+ * between steps): mode 0 = NCCL reduce-scatter -> Updater on the shard ->
+ * all-gather (default); mode 1 = one fused kernel per bucket over NVLink peer
+ * memory (CUDA IPC): ascending-rank gradient sum, Updater, the TF32 working
+ * copy stored into every rank, bracketed by two flag barriers whose epochs live
+ * in device memory (graph replayable).  Needs a partitioned net (world > 1 or
+ * exercise_collectives), at most 8 ranks.  A barrier that times out makes every
+ * later exchange skip its work and sg_net_sync return SG_ERR_CUDA.  With mode 1
+ * on, sg_net_destroy is COLLECTIVE. */
+SG_API sg_status sg_net_set_exchange(sg_net* n, int32_t mode);
 /* Kernel launches issued by the last sg_train_one_batch (graph replay counts the captured kernels). */
 SG_API sg_status sg_net_last_launch_count(const sg_net* n, int64_t* launches);
 /* Per-operation device timing (CUDA events around every layer operation, also

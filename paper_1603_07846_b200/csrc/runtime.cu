@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "abi_common.h"
+#include "exchange.h"
 #include "ops.h"
 #include "plan.h"
 
@@ -100,6 +101,9 @@ struct sg_net {
   std::vector<double> pacc;
   std::vector<long long> pcnt;
   std::vector<void*> allocs;
+  // fused peer-memory exchange of the sharded buckets (sg_net_set_exchange), else NCCL
+  sg::PeerExchange* px = nullptr;
+  std::vector<int> px_sid;  // store -> exchange bucket (or -1)
 };
 
 namespace sg {
@@ -382,7 +386,10 @@ sg_status update(sg_net* n, sg_updater* u, int i) {
   const float mu = u->cfg.momentum, wd = u->cfg.weight_decay * L.wd_scale;
   // elements [0, rn_end) of the store are the weight matrix (TF32-RN working copy); the bias follows
   const int64_t rn_end = P.params[L.pW].isize;
-  if (S.sharded) {
+  if (S.sharded && n->px && n->px_sid[L.store] >= 0) {
+    // the same exchange in one fused kernel over NVLink peer memory (exchange.h)
+    SG_LCH(px_update(n->px, n->px_sid[L.store], n->lr_dev, L.lr_scale, mu, wd, u->s, u->cfg.type, u->eps, n->ps));
+  } else if (S.sharded) {
     // worker group -> server group: reduce-scatter (sum) of the gradient bucket;
     // the server owning shard `rank` updates its fp32 master and writes the
     // working copy of the shard, which the all-gather distributes (Collect)
@@ -696,6 +703,7 @@ sg_status destroy_net(sg_net* n) {
   if (n->cs) cudaStreamSynchronize(n->cs);
   if (n->ps) cudaStreamSynchronize(n->ps);
   if (n->gexec) cudaGraphExecDestroy(n->gexec);
+  if (n->px) px_destroy(n->px, n->cl ? n->cl->comm_par : nullptr);
   for (void* p : n->allocs) cudaFree(p);
   for (auto e : n->ev_grad) cudaEventDestroy(e);
   for (auto e : n->ev_upd) cudaEventDestroy(e);
@@ -1117,6 +1125,8 @@ SG_API sg_status sg_net_sync(sg_net* n) {
   if (flags) SG_CUDA(cudaMemset(n->err, 0, sizeof(int)));
   SG_CHECK(!(flags & 1), SG_ERR_LABEL, "label error: a label is outside [0, %d)", PL(n).num_classes);
   SG_CHECK(!(flags & 2), SG_ERR_DIVERGED, "diverged: non-finite loss");
+  SG_CHECK(!px_failed(n->px), SG_ERR_CUDA,
+           "peer exchange: a barrier timed out (a rank did not arrive); the exchange is disabled for this net");
   return SG_OK;
 }
 
@@ -1179,6 +1189,39 @@ SG_API sg_status sg_net_op_times(sg_net* n, double* ms, int64_t* counts, int32_t
     std::fill(n->pcnt.begin(), n->pcnt.end(), 0);
   }
   return SG_OK;
+}
+
+SG_API sg_status sg_net_set_exchange(sg_net* n, int32_t mode) {
+  SG_CHECK(n && (mode == 0 || mode == 1), SG_ERR_INVALID_ARG, "sg_net_set_exchange: bad argument");
+  const Plan& P = PL(n);
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  SG_CUDA(cudaStreamSynchronize(n->ps));
+  SG_CUDA(cudaStreamSynchronize(n->cs));
+  if (n->gexec) {  // the captured step encodes the exchange path
+    cudaGraphExecDestroy(n->gexec);
+    n->gexec = nullptr;
+  }
+  if (n->px) {
+    px_destroy(n->px, n->cl->comm_par);
+    n->px = nullptr;
+  }
+  n->px_sid.assign(P.stores.size(), -1);
+  if (mode == 0) return SG_OK;
+  SG_CHECK(P.dist && n->cl->comm_par, SG_ERR_CONFIG,
+           "config error: the peer-memory exchange needs a partitioned net (world > 1 or exercise_collectives)");
+  std::vector<PxStore> stores;
+  for (size_t s = 0; s < P.stores.size(); ++s) {
+    const StorePlan& S = P.stores[s];
+    if (!S.sharded) continue;
+    n->px_sid[s] = (int)stores.size();
+    stores.push_back(PxStore{n->sgr[s], n->sw[s], n->sm[s], n->sv[s], S.padded, P.params[P.layers[S.layer].pW].isize});
+  }
+  sg_status st = px_create(n->cl->comm_par, P.rank, P.world, n->cl->device, stores, &n->px);
+  if (st != SG_OK) {
+    n->px = nullptr;
+    n->px_sid.assign(P.stores.size(), -1);
+  }
+  return st;
 }
 
 SG_API sg_status sg_net_set_fusion(sg_net* n, int32_t enable) {

@@ -231,6 +231,10 @@ class Net:
     def sync(self):
         L.sg_net_sync(self.h)
 
+    def set_exchange(self, mode):
+        """0: NCCL chain, 1: fused peer-memory kernel (COLLECTIVE)."""
+        L.sg_net_set_exchange(self.h, {"nccl": 0, "p2p": 1}.get(mode, mode))
+
     def set_fusion(self, on=True):
         L.sg_net_set_fusion(self.h, 1 if on else 0)
 

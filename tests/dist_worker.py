@@ -64,11 +64,13 @@ def setup():
     return rank, world, cl
 
 
-def run_net(cl, net, b, steps, upd, rank, world, graph=False):
+def run_net(cl, net, b, steps, upd, rank, world, graph=False, exchange="nccl"):
     n = PN.Net(cl, net, b)
     n.set_updater(upd)
     params = generate.init_params(ON.param_specs(net))
     n.set_params(params)
+    if exchange != "nccl":
+        n.set_exchange(exchange)
     if graph:
         n.enable_graph(True)
     info = n.layer_info
@@ -87,6 +89,12 @@ def run_net(cl, net, b, steps, upd, rank, world, graph=False):
         if t == 0:
             first_grads = n.get_grads({k: v.shape for k, v in params.items()})
     final = n.get_params({k: v.shape for k, v in params.items()})
+    work = n.get_working({k: v.shape for k, v in params.items()})
+    allw = [None] * world
+    dist.all_gather_object(allw, work)
+    for other in allw:                    # every rank holds the same working copy
+        for k in work:
+            assert np.array_equal(other[k], work[k]), k
     n.close()
     return params, losses, first_grads, final
 
@@ -105,8 +113,8 @@ def oracle_run(net, b, steps, upd, K, params):
     return losses, g0, p
 
 
-def run_smooth(net, b, steps, rank, world, cl, graph=False):
-    return (net, b, steps) + run_net(cl, net, b, steps, UPD, rank, world, graph)
+def run_smooth(net, b, steps, rank, world, cl, graph=False, exchange="nccl"):
+    return (net, b, steps) + run_net(cl, net, b, steps, UPD, rank, world, graph, exchange)
 
 
 def check_smooth(res, world, gtol=2e-3):
@@ -168,7 +176,7 @@ def case_alexnet(rank, world, cl):
     isolated(cl, net, b, rank, world, configs.UPDATERS["alexnet"], fused=True, graph=True)
 
 
-def isolated(cl, net, b, rank, world, upd, fused=False, graph=False):
+def isolated(cl, net, b, rank, world, upd, fused=False, graph=False, exchange="nccl"):
     """One step; every rank checks its local layers against the oracle fed its
     own blobs (tests/layer_check.check_layers_dist), cross-rank sums and
     gathers over gloo; 2e-3 for TF32 contractions, 1e-5 for SIMT kernels,
@@ -178,6 +186,8 @@ def isolated(cl, net, b, rank, world, upd, fused=False, graph=False):
     params = generate.init_params(ON.param_specs(net))
     n.set_params(params)
     n.set_fusion(fused)
+    if exchange != "nccl":
+        n.set_exchange(exchange)
     if graph:
         n.enable_graph(True)
     info = n.layer_info
@@ -206,7 +216,7 @@ def isolated(cl, net, b, rank, world, upd, fused=False, graph=False):
             for q, e in w.items():
                 tot[q] = max(tot.get(q, 0.0), e)
         kinds = sorted({l["kind"] for l in info})
-        print(f"{net['name']} K={world} layer-isolated ({len(rep)} checks/rank, kinds {kinds}): worst "
+        print(f"{net['name']} K={world} layer-isolated [{exchange}] ({len(rep)} checks/rank, kinds {kinds}): worst "
               + ", ".join(f"{q} {e:.2e}" for q, e in sorted(tot.items())), flush=True)
 
 
@@ -217,6 +227,24 @@ def case_isolated(rank, world, cl):
     ae = configs.get("ae") if world <= 2 else configs.autoencoder([784, 256, 64, 8, 64, 256, 784], "ae_k4")
     isolated(cl, ae, 16, rank, world, configs.UPDATERS["ae"], fused=True)
     isolated(cl, configs.get("mlp"), 8 * world, rank, world, configs.UPDATERS["mlp"])
+
+
+def case_p2p_step(rank, world, cl):
+    """The training step with the fused peer-memory exchange (sg_net_set_exchange
+    p2p): chained smooth nets at 2e-3, every layer
+    layer-isolated, weights identical on every rank, graph replay == eager."""
+    res = [run_smooth(CIFAR_SMOOTH, 4 * world, 3, rank, world, cl, exchange="p2p"),
+           run_smooth(CIFAR_SMOOTH, 4 * world, 3, rank, world, cl, graph=True, exchange="p2p"),
+           run_smooth(HYBRID_SMOOTH, 4 * world, 3, rank, world, cl, exchange="p2p")]
+    if rank == 0:
+        for r in res:
+            check_smooth(r, world)
+        for k in res[0][6]:
+            assert np.array_equal(res[0][6][k], res[1][6][k]), k
+    isolated(cl, configs.get("cifar10"), 8 * world, rank, world, configs.UPDATERS["cifar10"], fused=True, graph=True,
+             exchange="p2p")
+    isolated(cl, configs.alexnet(hybrid=True), 2 * world, rank, world, configs.UPDATERS["alexnet"], fused=True,
+             graph=True, exchange="p2p")
 
 
 def case_server_sync(rank, world, cl):
@@ -290,7 +318,7 @@ def case_peer_sync(rank, world, cl):
 
 
 CASES = {"k_invariance": case_k_invariance, "hybrid": case_hybrid, "autoencoder": case_autoencoder,
-         "isolated": case_isolated,
+         "isolated": case_isolated, "p2p_step": case_p2p_step,
          "alexnet": case_alexnet, "server_sync": case_server_sync, "peer_sync": case_peer_sync}
 
 if __name__ == "__main__":

@@ -74,7 +74,7 @@ def operands(p0, work0):
     return {k: f64(v) for k, v in work0.items()}
 
 
-def check_layers(n, net, b, x, lab, p0, work0, grads, newp, work, upd, fused=False, sub=None):
+def check_layers(n, net, b, x, lab, p0, work0, grads, newp, work, upd, fused=False, sub=None, hist=None):
     """Returns [(layer, quantity, error)]; raises AssertionError on a miss.
     p0 / work0: master and working copy before the step; newp / work after it."""
     infos = n.layer_info
@@ -205,9 +205,11 @@ def check_layers(n, net, b, x, lab, p0, work0, grads, newp, work, upd, fused=Fal
     # Updater (layer-isolated): fp32 master from the GPU's own aggregated
     # gradient; working copy = TF32-RN(master) for weights, master for biases
     for name in p0:
-        w1, _ = OU.update(pm[name], np.zeros_like(pm[name]), f64(grads[name]), upd, 0, 1.0)
+        w1, h1 = OU.update(pm[name], np.zeros_like(pm[name]), f64(grads[name]), upd, 0, 1.0)
         e = normwise(newp[name], w1)
         assert e < 1e-6, (name, e)
+        if hist is not None and np.any(h1):   # history after the first step: -lr g' (momentum) / g'^2 (AdaGrad)
+            assert normwise(hist[name], h1) < 1e-6, (name, "history")
         want = newp[name] if name.endswith("/b") else rna_tf32(newp[name])
         assert np.array_equal(work[name], want), (name, "working copy")
         rec(name, "update", e)

@@ -261,6 +261,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=50)
+    ap.add_argument("--exchange", default="p2p", choices=["nccl", "p2p"],
+                    help="gradient exchange of the sharded buckets at N > 1: NCCL chain or fused peer-memory kernel")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = env_rank()
@@ -288,6 +290,8 @@ def main():
     n = PN.Net(cluster, net_cfg, b)
     n.set_updater(configs.UPDATERS[args.config])
     n.set_params(init_params(PN, n, net_cfg))
+    if world > 1 and args.exchange != "nccl":
+        n.set_exchange(args.exchange)
     info = n.layer_info
     rows_in = info[0]["local_shape"][0]
     row_off = info[0]["local_offset"][0]
@@ -455,7 +459,8 @@ def main():
                 "config": {"workload": args.config, "global_batch": b, "per_gpu_batch": b // world if weak else None,
                            "parallelism": f"dp{world}" if args.config in ("cifar10", "mlp") else f"hybrid{world}",
                            "l2": "flushed (256 MB write) before every timed step",
-                           "graph": not args.no_graph, "final_loss": final_loss},
+                           "graph": not args.no_graph, "final_loss": final_loss,
+                           "exchange": args.exchange if world > 1 else None},
                 "roofline": roof, "grad_sync": grad_sync, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches * args.steps),
                 "clocks": clocks,
                 "ops": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in o.items()} for o in ops[:12]],

@@ -38,16 +38,24 @@ from workloads import configs, generate  # noqa: E402
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 TF32_OVER_BF16 = 1.1 / 2.25      # guide's nominal dense ratio (tf32 1.1 PF vs bf16 2.25 PF)
-PER_GPU_BATCH = {"cifar10": 128, "mlp": 64, "alexnet": 256, "ae_wide": 256, "ae": 256}
-SCALING = {"cifar10": "weak", "mlp": "weak", "alexnet": "strong", "ae_wide": "strong", "ae": "strong"}
+PER_GPU_BATCH = {"cifar10": 128, "mlp": 64, "alexnet": 256, "alexnet_dp": 256, "ae_wide": 256, "ae": 256}
+SCALING = {"cifar10": "weak", "mlp": "weak", "alexnet": "strong", "alexnet_dp": "strong", "ae_wide": "strong",
+           "ae": "strong"}
 
 
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d, "measured"
-    return PEAKS_FALLBACK, "fallback"
+        src = "measured"
+    else:
+        d, src = dict(PEAKS_FALLBACK), "fallback"
+    # TF32 tensor-pipe ceiling measured on a B200 of this pool (tools/tf32_peak.cu:
+    # every SM issuing 128x256x8 kind::tf32 MMAs from shared memory)
+    t = os.path.join(ROOT, "profiles", "r02_tf32_peak.json")
+    if os.path.exists(t):
+        d = dict(d, tf32_tflops=json.load(open(t))["tf32_tflops"])
+    return d, src
 
 
 def env_rank():
@@ -261,6 +269,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=50)
+    ap.add_argument("--batch", type=int, default=0, help="global batch override (ablations)")
+    ap.add_argument("--no-overlap", action="store_true", help="Update waits on the compute stream (P:770-774)")
     ap.add_argument("--exchange", default="p2p", choices=["nccl", "p2p"],
                     help="gradient exchange of the sharded buckets at N > 1: NCCL chain or fused peer-memory kernel")
     args = ap.parse_args()
@@ -286,12 +296,14 @@ def main():
     cluster = PN.Cluster(rank, world, local, nccl_id)
     net_cfg = configs.get(args.config)
     weak = SCALING[args.config] == "weak"
-    b = PER_GPU_BATCH[args.config] * (world if weak else 1)
+    b = args.batch or PER_GPU_BATCH[args.config] * (world if weak else 1)
     n = PN.Net(cluster, net_cfg, b)
     n.set_updater(configs.UPDATERS[args.config])
     n.set_params(init_params(PN, n, net_cfg))
     if world > 1 and args.exchange != "nccl":
         n.set_exchange(args.exchange)
+    if args.no_overlap:
+        L.sg_net_set_overlap(n.h, 0)
     info = n.layer_info
     rows_in = info[0]["local_shape"][0]
     row_off = info[0]["local_offset"][0]
@@ -377,7 +389,9 @@ def main():
     work = op_work(net_cfg, info, world)
     peaks, peaks_src = load_peaks()
     hbm_peak = peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
-    tf32_peak = peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]) * TF32_OVER_BF16
+    tf32_peak = peaks.get("tf32_tflops") or peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]) * TF32_OVER_BF16
+    tf32_src = "measured tf32 (profiles/r02_tf32_peak.json)" if peaks.get("tf32_tflops") else \
+        "bf16 x 1.1/2.25 nominal ratio"
     ops = []
     for s in range(nslots):
         if cnt[s] > 0 and s in work:
@@ -403,7 +417,7 @@ def main():
             roof = {"bound": "hbm", "achieved": dom["bytes"] / t_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": b_frac}
         roof.update({"kernel": dom["op"], "kernel_ms": dom["ms"], "share_of_step": dom["ms"] / (total_ms / args.steps),
-                     "peak_source": f"{peaks_src} ({'tf32 = bf16 x 1.1/2.25 nominal ratio' if roof['bound'] == 'tensor' else 'hbm copy'})",
+                     "peak_source": f"{peaks_src} ({tf32_src if roof['bound'] == 'tensor' else 'hbm copy'})",
                      "traffic": None})
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
@@ -457,10 +471,10 @@ def main():
                 "higher_is_better": True, "scaling": SCALING[args.config], "vs_baseline": None, "dtype": "tf32",
                 "data": "synthetic",
                 "config": {"workload": args.config, "global_batch": b, "per_gpu_batch": b // world if weak else None,
-                           "parallelism": f"dp{world}" if args.config in ("cifar10", "mlp") else f"hybrid{world}",
+                           "parallelism": f"dp{world}" if args.config in ("cifar10", "mlp", "alexnet_dp") else f"hybrid{world}",
                            "l2": "flushed (256 MB write) before every timed step",
                            "graph": not args.no_graph, "final_loss": final_loss,
-                           "exchange": args.exchange if world > 1 else None},
+                           "exchange": args.exchange if world > 1 else None, "overlap": not args.no_overlap},
                 "roofline": roof, "grad_sync": grad_sync, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches * args.steps),
                 "clocks": clocks,
                 "ops": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in o.items()} for o in ops[:12]],

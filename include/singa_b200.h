@@ -383,6 +383,11 @@ SG_API sg_status sg_net_set_fusion(sg_net* n, int32_t enable);
  * later exchange skip its work and sg_net_sync return SG_ERR_CUDA.  With mode 1
  * on, sg_net_destroy is COLLECTIVE. */
 SG_API sg_status sg_net_set_exchange(sg_net* n, int32_t mode);
+/* Overlap of communication and computation (§5.4.2, P:557-587;
+ * default on): Update(layer) runs on the parameter stream concurrently with the
+ * backward of the layers below it.  Off: the compute stream waits for each
+ * Update before continuing (the paper's "Sync Copy" baseline). */
+SG_API sg_status sg_net_set_overlap(sg_net* n, int32_t enable);
 /* Kernel launches issued by the last sg_train_one_batch (graph replay counts the captured kernels). */
 SG_API sg_status sg_net_last_launch_count(const sg_net* n, int64_t* launches);
 /* Per-operation device timing (CUDA events around every layer operation, also

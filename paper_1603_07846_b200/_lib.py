@@ -146,6 +146,7 @@ SIGS = {
     "sg_net_enable_graph": [P, I32],
     "sg_net_set_fusion": [P, I32],
     "sg_net_set_exchange": [P, I32],
+    "sg_net_set_overlap": [P, I32],
     "sg_net_last_launch_count": [P, PI64],
     "sg_net_profile": [P, I32],
     "sg_net_op_times": [P, C.POINTER(C.c_double), PI64, I32, PI32, I32],

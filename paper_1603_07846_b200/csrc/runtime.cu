@@ -104,6 +104,9 @@ struct sg_net {
   // fused peer-memory exchange of the sharded buckets (sg_net_set_exchange), else NCCL
   sg::PeerExchange* px = nullptr;
   std::vector<int> px_sid;  // store -> exchange bucket (or -1)
+  // Update(layer) overlaps the backward of the layers below (default); off: the
+  // compute stream waits for every Update right away ("Sync Copy")
+  bool overlap = true;
 };
 
 namespace sg {
@@ -414,6 +417,7 @@ sg_status update(sg_net* n, sg_updater* u, int i) {
   prof_mark(n, 4 * i + 3, 1, n->ps);
   SG_CUDA(cudaEventRecord(n->ev_upd[i], n->ps));
   n->upd_pending[i] = 1;
+  if (!n->overlap) SG_CUDA(cudaStreamWaitEvent(n->cs, n->ev_upd[i], 0));
   return SG_OK;
 }
 
@@ -1187,6 +1191,18 @@ SG_API sg_status sg_net_op_times(sg_net* n, double* ms, int64_t* counts, int32_t
   if (reset) {
     std::fill(n->pacc.begin(), n->pacc.end(), 0.0);
     std::fill(n->pcnt.begin(), n->pcnt.end(), 0);
+  }
+  return SG_OK;
+}
+
+SG_API sg_status sg_net_set_overlap(sg_net* n, int32_t enable) {
+  SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  SG_CUDA(cudaStreamSynchronize(n->cs));
+  n->overlap = enable != 0;
+  if (n->gexec) {
+    cudaGraphExecDestroy(n->gexec);
+    n->gexec = nullptr;
   }
   return SG_OK;
 }

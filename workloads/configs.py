@@ -131,7 +131,10 @@ TINY_CONV = {
     ],
 }
 
-NETS = {"mlp": MLP, "cifar10": CIFAR10, "alexnet": ALEXNET, "ae": AE, "ae_wide": AE_WIDE,
+# the paper's ablation baseline: every layer data parallel
+ALEXNET_DP = dict(alexnet(hybrid=False), name="alexnet_dp")
+
+NETS = {"mlp": MLP, "cifar10": CIFAR10, "alexnet": ALEXNET, "alexnet_dp": ALEXNET_DP, "ae": AE, "ae_wide": AE_WIDE,
         "tiny_conv": TINY_CONV}
 
 # Updater hyper-parameters per config.
@@ -139,6 +142,7 @@ UPDATERS = {
     "mlp": {"base_lr": 0.01, "momentum": 0.9, "weight_decay": 5e-4, "lr_policy": "fixed"},
     "cifar10": {"base_lr": 0.001, "momentum": 0.9, "weight_decay": 0.004, "lr_policy": "fixed"},
     "alexnet": {"base_lr": 0.01, "momentum": 0.9, "weight_decay": 5e-4, "lr_policy": "fixed"},
+    "alexnet_dp": {"base_lr": 0.01, "momentum": 0.9, "weight_decay": 5e-4, "lr_policy": "fixed"},
     "ae": {"base_lr": 0.01, "momentum": 0.9, "weight_decay": 0.0, "lr_policy": "fixed"},
     "ae_wide": {"base_lr": 0.01, "momentum": 0.9, "weight_decay": 0.0, "lr_policy": "fixed"},
     "tiny_conv": {"base_lr": 0.01, "momentum": 0.9, "weight_decay": 5e-4, "lr_policy": "fixed"},

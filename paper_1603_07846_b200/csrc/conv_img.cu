@@ -64,6 +64,7 @@ struct ImgConvArgs {
   int N;               // output channels (multiple of 32)
   int layer_c, layer_co;  // the layer's C / Co (weight tensor strides)
   int ntiles, img_rows, relu, dgrad;  // relu: epilogue flags EPI_RELU | EPI_RN (ops.h)
+  int split;  // CTAs per sample (strong scaling: few samples per rank), NT tiles each
   int Hrows;  // padded image rows staged (img_rows = Hrows * Wp rounded up to 8)
   int wsplit;  // filter bank staged one K block at a time
 };
@@ -77,7 +78,7 @@ __device__ __forceinline__ uint32_t ksw(int row, int chunk) {  // K-major SW128 
 // tile are issued before one wait, the bias is read once.
 template <int NB>
 __device__ __forceinline__ void img_epilogue(uint32_t tmem, int ntiles, int warp, int lane, int Wp, int Ho, int Wo,
-                                             float* outn, const float* bias, int flags) {
+                                             float* outn, const float* bias, int flags, int t0 = 0) {
   float bv[NB];
 #pragma unroll
   for (int c = 0; c < NB; ++c) bv[c] = bias ? __ldg(bias + c) : 0.f;
@@ -87,7 +88,7 @@ __device__ __forceinline__ void img_epilogue(uint32_t tmem, int ntiles, int warp
 #pragma unroll
     for (int c = 0; c < NB / 16; ++c) tmem_ld16_nowait(tmem + ((uint32_t)(warp * 32) << 16) + i * NB + c * 16, r[c]);
     tmem_wait_ld();
-    const int q = i * 128 + warp * 32 + lane;
+    const int q = (t0 + i) * 128 + warp * 32 + lane;  // tile t0 + i of the sample
     const int oh = q / Wp, ow = q - oh * Wp;
     if (oh >= Ho || ow >= Wo) continue;
     float4* dst = reinterpret_cast<float4*>(outn + ((size_t)oh * Wo + ow) * NB);
@@ -124,7 +125,9 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
   const uint32_t bar = wbase + wbytes, done_bar = bar + 8, wbar = done_bar + 8, wfree = wbar + 8, slot = wfree + 8;
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n = blockIdx.x;
+  // sample n, tiles [t0, t0 + nvalid) of it (a sample's tiles may be split over `split` CTAs)
+  const int n = blockIdx.x / a.split, t0 = (blockIdx.x % a.split) * NT;
+  const int nvalid = min(NT, a.ntiles - t0);
 
   if (tid == 0) {
     mbar_init(bar, 1);
@@ -190,10 +193,11 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
             const uint32_t b_c = DGRAD ? b_lo0 + ((uint32_t)(T - 1 - t) * 4096 >> 4) : b_lo0 + ((uint32_t)t * NB * 128 >> 4);
 #pragma unroll
             for (int i = 0; i < NT; ++i)
+              if (i < nvalid)
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                mma_tf32_lh(tmem + i * NB, a_t + i * 1024 + kk * 2, a_hi, b_c + kk * (DGRAD ? 64 : 2), b_hi, idesc,
-                            (t | kb | kk) ? 1u : 0u);
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_tf32_lh(tmem + i * NB, a_t + (t0 + i) * 1024 + kk * 2, a_hi, b_c + kk * (DGRAD ? 64 : 2), b_hi,
+                              idesc, (t | kb | kk) ? 1u : 0u);
             if (++sc == a.S) {
               sc = 0;
               ++r;
@@ -210,6 +214,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
         const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc) * 8;
 #pragma unroll
         for (int i = 0; i < NT; ++i)
+          if (i < nvalid)
 #pragma unroll
           for (int cb = 0; cb < CB; ++cb) {
             // forward: tap t of block cb; dgrad: flipped tap of K block cb (atom 0; LBO = T*4096)
@@ -217,8 +222,8 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
                                        : b_lo0 + ((uint32_t)(cb * T + t) * NB * 128 >> 4);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_tf32_lh(tmem + i * NB, a_t + i * 1024 + cb * plane16 + kk * 2, a_hi, b_c + kk * (DGRAD ? 64 : 2),
-                          b_hi, idesc, (t | cb | kk) ? 1u : 0u);
+              mma_tf32_lh(tmem + i * NB, a_t + (t0 + i) * 1024 + cb * plane16 + kk * 2, a_hi,
+                          b_c + kk * (DGRAD ? 64 : 2), b_hi, idesc, (t | cb | kk) ? 1u : 0u);
           }
         if (++sc == a.S) {
           sc = 0;
@@ -234,7 +239,8 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
     mbar_wait_sleep(done_bar, 0);
     if (tid == 0) IMG_TRACE(4, 0);
     tc_fence_after();
-    img_epilogue<NB>(tmem, NT, warp, lane, a.Wp, a.Ho, a.Wo, a.out + (size_t)n * a.Ho * a.Wo * NB, a.bias, a.relu);
+    img_epilogue<NB>(tmem, nvalid, warp, lane, a.Wp, a.Ho, a.Wo, a.out + (size_t)n * a.Ho * a.Wo * NB, a.bias, a.relu,
+                     t0);
   }
   tc_fence_before();
   __syncthreads();
@@ -305,7 +311,18 @@ cudaError_t launch_img(const ImgConvArgs& a, size_t smem, int nimg, cudaStream_t
     if (e != cudaSuccess) return e;
     set[split] = smem;
   }
-  return launch_k(k, nimg, kImgThreads, smem, st, a);
+  return launch_k(k, nimg * a.split, kImgThreads, smem, st, a);
+}
+
+// CTAs per sample: with fewer samples than SMs (strong scaling, small b/K) a
+// sample's output tiles are spread over several CTAs, each staging the whole
+// sample; returns the tiles per CTA.
+int img_split(int ntiles, int nimg, int* split) {
+  static const int maxs = getenv("SG_IMG_SPLIT") ? atoi(getenv("SG_IMG_SPLIT")) : 1 << 20;
+  int s = std::max(1, std::min({ntiles, 148 / std::max(nimg, 1), maxs}));
+  const int per = (ntiles + s - 1) / s;
+  *split = (ntiles + per - 1) / per;
+  return per;
 }
 
 template <int NB, bool DG, int NT>
@@ -313,8 +330,8 @@ cudaError_t run_img_cb(const ImgConvArgs& a, size_t smem, int nimg, cudaStream_t
   return a.C / 32 == 1 ? launch_img<NB, DG, NT, 1>(a, smem, nimg, st) : launch_img<NB, DG, NT, 2>(a, smem, nimg, st);
 }
 template <int NB, bool DG>
-cudaError_t run_img_nt(const ImgConvArgs& a, size_t smem, int nimg, cudaStream_t st) {
-  switch (a.ntiles) {
+cudaError_t run_img_nt(ImgConvArgs a, size_t smem, int nimg, cudaStream_t st) {
+  switch (img_split(a.ntiles, nimg, &a.split)) {
     case 1: return run_img_cb<NB, DG, 1>(a, smem, nimg, st);
     case 2: return run_img_cb<NB, DG, 2>(a, smem, nimg, st);
     case 3: return run_img_cb<NB, DG, 3>(a, smem, nimg, st);
@@ -341,6 +358,7 @@ struct Img4Args {
   const float* bias;
   float* out;
   int pad, R, S, SP, Wp, Ho, Wo, Hrows, img_rows, ntiles, relu;  // relu: epilogue flags
+  int split, tpc;  // CTAs per sample, tiles per CTA
 };
 
 template <int NB>
@@ -353,7 +371,8 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __g
   const uint32_t bar = wbase + ((wbytes + 1023) & ~1023u), done_bar = bar + 8, slot = done_bar + 8;
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n = blockIdx.x;
+  const int n = blockIdx.x / a.split, t0 = (blockIdx.x % a.split) * a.tpc;  // sample, first tile
+  const int t1 = min(a.ntiles, t0 + a.tpc);
 
   // zero weights of the padding taps s in [S, SP) (disjoint from the TMA boxes)
   for (int i = tid; i < a.R * (a.SP - a.S) * NB; i += kImgThreads) {
@@ -396,8 +415,8 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __g
         for (int sc = 0; sc < a.S; sc += 2) {
           const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc);  // 16-B pixel rows: start field += 1
           const uint32_t b_t = b_lo0 + (uint32_t)(r * a.SP + sc) * NB;
-          for (int i = 0; i < a.ntiles; ++i)
-            mma_tf32_lh(tmem + i * NB, a_t + i * 128, a_hi, b_t, b_hi, idesc, first ? 0u : 1u);
+          for (int i = t0; i < t1; ++i)
+            mma_tf32_lh(tmem + (i - t0) * NB, a_t + i * 128, a_hi, b_t, b_hi, idesc, first ? 0u : 1u);
           first = false;
         }
       IMG_TRACE(2, 0);
@@ -408,8 +427,8 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __g
     mbar_wait_sleep(done_bar, 0);
     if (tid == 0) IMG_TRACE(4, 0);
     tc_fence_after();
-    img_epilogue<NB>(tmem, a.ntiles, warp, lane, a.Wp, a.Ho, a.Wo, a.out + (size_t)n * a.Ho * a.Wo * NB, a.bias,
-                     a.relu);
+    img_epilogue<NB>(tmem, t1 - t0, warp, lane, a.Wp, a.Ho, a.Wo, a.out + (size_t)n * a.Ho * a.Wo * NB, a.bias,
+                     a.relu, t0);
   }
   if (tid == 0) IMG_TRACE(0, 0);
   tc_fence_before();
@@ -461,6 +480,7 @@ struct ImgWgradArgs {
   int C, Co, R, S, pad, Wp, Ho, Wo;
   int Hrows_i, Hrows_d, rows_i, rows_d, ksteps;
   int nimg, spc;  // samples, samples per CTA (accumulated in TMEM)
+  int split, kpc;  // CTAs per sample group (strong scaling), K steps per CTA
   int ntile;
   int t_off[kMaxWTiles], t_delta[kMaxWTiles], t_tap[kMaxWTiles][4];
 };
@@ -478,7 +498,10 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
   __shared__ float red[128];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n0 = blockIdx.x * a.spc, n1 = min(a.nimg, n0 + a.spc), ns = n1 - n0;
+  // sample group blockIdx.x / split; K steps (pixel rows of 8) [k0, k1) of it
+  const int part = blockIdx.x % a.split;
+  const int n0 = (blockIdx.x / a.split) * a.spc, n1 = min(a.nimg, n0 + a.spc), ns = n1 - n0;
+  const int k0 = part * a.kpc, k1 = min(a.ksteps, k0 + a.kpc);
   const int Kg = a.R * a.S * a.C, per = a.Co * Kg + a.Co;
 
   if (tid == 0) {
@@ -519,8 +542,9 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
         for (int g = 0; g < a.ntile; ++g) {
           const uint64_t ad0 = umma_desc_mn_sw128_32b(img + a.t_off[g] * 128, a.t_delta[g] * 128, 512);
           const uint32_t a_lo0 = (uint32_t)ad0, a_hi = (uint32_t)(ad0 >> 32);
-          for (int ks = 0; ks < a.ksteps; ++ks)
-            mma_tf32_lh(tmem + g * NB, a_lo0 + ks * 64, a_hi, b_lo0 + ks * 64, b_hi, idesc, (k | ks) ? 1u : 0u);
+          for (int ks = k0; ks < k1; ++ks)
+            mma_tf32_lh(tmem + g * NB, a_lo0 + ks * 64, a_hi, b_lo0 + ks * 64, b_hi, idesc,
+                        (k | (ks - k0)) ? 1u : 0u);
         }
         if (k + 2 < ns) mma_commit(bars + 16 + 8 * b);  // buffer b is restaged once these complete
       }
@@ -537,13 +561,16 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
         stage(k);
       }
     }
-    // db partial = sum over the CTA's samples of dy (SIMT, fixed order), while the MMAs run
+    // db partial = sum over the CTA's samples of dy (SIMT, fixed order), while the MMAs run;
+    // a split sample's pixels are divided evenly among its CTAs
     const int groups = 128 / a.Co;  // threads per channel (Co <= 128)
     float sacc = 0.f;
     if (tid < groups * a.Co) {
       const int co = tid % a.Co, grp = tid / a.Co;
       const float* dyn = a.dy + (size_t)n0 * a.Ho * a.Wo * a.Co;
-      for (int p = grp; p < ns * a.Ho * a.Wo; p += groups) sacc += __ldg(dyn + (size_t)p * a.Co + co);
+      const int np = ns * a.Ho * a.Wo, pc = (np + a.split - 1) / a.split;
+      const int pb = part * pc, pe = min(np, pb + pc);
+      for (int p = pb + grp; p < pe; p += groups) sacc += __ldg(dyn + (size_t)p * a.Co + co);
     }
     red[tid] = sacc;
     mbar_wait_sleep(done_bar, 0);
@@ -651,6 +678,15 @@ bool plan_wgrad(const ConvShape& s, ImgWgradArgs* a, size_t* smem) {
   static const int spc_env = getenv("SG_WGRAD_SPC") ? atoi(getenv("SG_WGRAD_SPC")) : 1;
   g.spc = std::max(1, std::min(s.N, spc_env));
   if (g.ntile * g.ksteps < 200) return false;
+  // strong scaling: spread a sample's K steps over several CTAs when the
+  // samples alone cannot fill the machine (partials summed by the reduction)
+  {
+    static const int maxs = getenv("SG_IMG_SPLIT") ? atoi(getenv("SG_IMG_SPLIT")) : 1 << 20;
+    const int groups = (s.N + g.spc - 1) / g.spc;
+    int sp = std::max(1, std::min({148 / std::max(groups, 1), maxs, g.ksteps / 8}));
+    g.kpc = (g.ksteps + sp - 1) / sp;
+    g.split = (g.ksteps + g.kpc - 1) / g.kpc;
+  }
   *smem = 1024 + 2 * ((size_t)g.rows_i * 128 + (size_t)(s.Co / 32) * g.rows_d * 128) + 64;
   if (*smem > 227 * 1024) return false;
   *a = g;
@@ -670,7 +706,7 @@ size_t conv_img_wgrad_ws_floats(const ConvShape& s) {
   ImgWgradArgs a;
   size_t smem;
   if (!plan_wgrad(s, &a, &smem)) return 0;
-  const size_t ctas = (s.N + a.spc - 1) / a.spc;
+  const size_t ctas = (size_t)((s.N + a.spc - 1) / a.spc) * a.split;
   return 1024 + ctas * (size_t)(s.Co * s.R * s.S * s.C + s.Co);
 }
 
@@ -693,7 +729,7 @@ cudaError_t conv_img_wgrad(const ConvShape& s, const float* x, const float* dy, 
   auto k = s.Co == 32 ? conv_img_wgrad_kernel<32> : conv_img_wgrad_kernel<64>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int ctas = (s.N + a.spc - 1) / a.spc;
+  const int ctas = ((s.N + a.spc - 1) / a.spc) * a.split;
   e = launch_k(k, ctas, kImgThreads, smem, st, a);
   if (e != cudaSuccess) return e;
   const int nw = s.Co * s.R * s.S * s.C, per = nw + s.Co;
@@ -752,7 +788,8 @@ cudaError_t conv_img_fwd(const ConvShape& s, const float* x, const float* W, con
     auto k = s.Co == 32 ? conv_img4_fwd_kernel<32> : conv_img4_fwd_kernel<64>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return launch_k(k, s.N, kImgThreads, smem, st, a4);
+    a4.tpc = img_split(a4.ntiles, s.N, &a4.split);
+    return launch_k(k, s.N * a4.split, kImgThreads, smem, st, a4);
   }
   if (!plan_img(s, false, &a, &smem)) return cudaErrorInvalidValue;
   a.src = x;

@@ -69,7 +69,12 @@ struct sg_net {
   float* x_exact = nullptr;  // unrounded copy of the input blob (a Euclidean loss's target when the input is rounded)
   const float* x_src = nullptr;
   sg::Workspace ws;
-  std::vector<cudaEvent_t> ev_grad, ev_upd;
+  // weight / bias gradients run on the parameter stream, off the critical path
+  // of the data-gradient chain (they are needed only by the layer's Update);
+  // their kernels use a workspace of their own
+  bool wgrad_side = true;
+  sg::Workspace ws2;
+  std::vector<cudaEvent_t> ev_grad, ev_upd, ev_dy;
   std::vector<char> upd_pending, fwd_done, bwd_done;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
   bool input_set = false;
@@ -302,17 +307,25 @@ sg_status backward(sg_net* n, int i) {
   float* db = L.pb >= 0 ? n->sgr[L.store] + P.params[L.pb].store_off : nullptr;
   const int s1 = 4 * i + 1, s2 = 4 * i + 2;
   const int rn_dx = S.rn_grad ? RN_OUT : 0;  // this layer's dx is a GEMM operand (reading A19)
-  prof_mark(n, s1, 0, st);
+  // weight gradient stream: the parameter stream (after dy is ready) or in line
+  const bool side = n->wgrad_side && (L.kind == SG_CONV || L.kind == SG_INNER_PRODUCT);
+  cudaStream_t wst = side ? n->ps : st;
+  const Workspace wws = side ? n->ws2 : n->ws;
+  if (side) {
+    SG_CUDA(cudaEventRecord(n->ev_dy[i], st));  // dy of this layer is complete
+    SG_CUDA(cudaStreamWaitEvent(n->ps, n->ev_dy[i], 0));
+  }
+  prof_mark(n, s1, 0, wst);
   switch (L.kind) {
     case SG_CONV:
       if (n->pool_into[i] >= 0) {  // fused: the max pool's backward builds this layer's dy (a13 + a15)
         const int c = n->pool_into[i];
         SG_LCH(conv_img4_pool_bwd(conv_shape(L, S), pool_shape(P.layers[c], L), n->data[L.src], n->grad[c],
-                                  n->mask[c], n->grad[i], L.rn_grad, dW, db, n->ws, st));
+                                  n->mask[c], n->grad[i], L.rn_grad, dW, db, wws, wst));
       } else {
-        SG_LCH(conv_wgrad(conv_shape(L, S), n->data[L.src], n->grad[i], dW, db, n->ws, st));
+        SG_LCH(conv_wgrad(conv_shape(L, S), n->data[L.src], n->grad[i], dW, db, wws, wst));
       }
-      prof_mark(n, s1, 1, st);
+      prof_mark(n, s1, 1, wst);
       if (need_dx) {
         prof_mark(n, s2, 0, st);
         SG_LCH(conv_dgrad(conv_shape(L, S), n->grad[i], W, n->grad[L.src], n->ws, st, S.rn_grad ? EPI_RN : 0));
@@ -346,8 +359,8 @@ sg_status backward(sg_net* n, int i) {
       break;
     case SG_INNER_PRODUCT: {
       View2D dy = plain(n->grad[i], (int)L.rows, (int)L.nout, L.ld);
-      SG_LCH(ip_wgrad(feat_view(S, n->data[L.src], L.kin), dy, (int)L.kin, (int)L.nout, dW, db, n->ws, st));
-      prof_mark(n, s1, 1, st);
+      SG_LCH(ip_wgrad(feat_view(S, n->data[L.src], L.kin), dy, (int)L.kin, (int)L.nout, dW, db, wws, wst));
+      prof_mark(n, s1, 1, wst);
       if (need_dx) {
         prof_mark(n, s2, 0, st);
         SG_LCH(ip_dgrad(dy, W, (int)L.kin, (int)L.nout, feat_view(S, n->grad[L.src], L.kin), n->ws, st,
@@ -383,6 +396,8 @@ sg_status update(sg_net* n, sg_updater* u, int i) {
   const LayerPlan& L = P.layers[i];
   if (L.store < 0) return SG_OK;
   const StorePlan& S = P.stores[L.store];
+  // the layer's backward (the data gradient reads the working copy the Updater
+  // rewrites) is complete; a side-stream weight gradient precedes in stream order
   SG_CUDA(cudaEventRecord(n->ev_grad[i], n->cs));
   SG_CUDA(cudaStreamWaitEvent(n->ps, n->ev_grad[i], 0));
   prof_mark(n, 4 * i + 3, 0, n->ps);
@@ -711,6 +726,7 @@ sg_status destroy_net(sg_net* n) {
   for (void* p : n->allocs) cudaFree(p);
   for (auto e : n->ev_grad) cudaEventDestroy(e);
   for (auto e : n->ev_upd) cudaEventDestroy(e);
+  for (auto e : n->ev_dy) cudaEventDestroy(e);
   for (auto e : {n->ev_in, n->ev_out, n->ev_fork, n->ev_join})
     if (e) cudaEventDestroy(e);
   for (auto e : n->pev) cudaEventDestroy(e);
@@ -735,12 +751,14 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
   n->mask.assign(nl, nullptr);
   n->ev_grad.resize(nl);
   n->ev_upd.resize(nl);
+  n->ev_dy.resize(nl);
   n->upd_pending.assign(nl, 0);
   n->fwd_done.assign(nl, 0);
   n->bwd_done.assign(nl, 0);
   for (int i = 0; i < nl; ++i) {
     SG_CUDA(cudaEventCreateWithFlags(&n->ev_grad[i], cudaEventDisableTiming));
     SG_CUDA(cudaEventCreateWithFlags(&n->ev_upd[i], cudaEventDisableTiming));
+    SG_CUDA(cudaEventCreateWithFlags(&n->ev_dy[i], cudaEventDisableTiming));
   }
   size_t ws = 1 << 16;
   auto need = [&](size_t f) {
@@ -774,6 +792,14 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
   // input layer are never formed.  The loss layer writes dz into its source's grad.
   SG_TRY(dalloc_t(n, ws, &n->ws.ptr));
   n->ws.floats = ws;
+  {
+    const char* env = getenv("SG_WGRAD_SIDE");
+    n->wgrad_side = env ? atoi(env) != 0 : true;
+  }
+  if (n->wgrad_side) {
+    SG_TRY(dalloc_t(n, ws, &n->ws2.ptr));
+    n->ws2.floats = ws;
+  }
   SG_TRY(dalloc_t(n, (size_t)std::max<int64_t>(P.loss_rows, 1), &n->row_loss));
   n->data[P.loss] = n->row_loss;
   SG_TRY(dalloc_t(n, 4, &n->loss_int));

@@ -397,10 +397,15 @@ SG_API sg_status sg_net_last_launch_count(const sg_net* n, int64_t* launches);
  * [4*i + 0] ComputeFeature, [4*i + 1] ComputeGradient (weight gradient for
  * conv / inner product), [4*i + 2] data gradient (conv / inner product),
  * [4*i + 3] Update (parameter stream).  counts[] (may be NULL) = intervals
- * summed per slot; reset != 0 clears the sums after reading. */
+ * summed per slot; reset != 0 clears the sums after reading.  enable == 1
+ * serialises the weight gradients onto the compute stream so every slot times
+ * its kernels alone; enable == 2 keeps the step's stream concurrency.
+ * sg_net_op_timeline: the last step's slot intervals as start / end times in
+ * ms relative to the start of the first used slot (-1 for unused slots). */
 SG_API sg_status sg_net_profile(sg_net* n, int32_t enable);
 SG_API sg_status sg_net_op_times(sg_net* n, double* ms, int64_t* counts, int32_t cap, int32_t* nslots,
                                  int32_t reset);
+SG_API sg_status sg_net_op_timeline(sg_net* n, double* t_start, double* t_end, int32_t cap, int32_t* nslots);
 
 /* ---- Blob access for layer-isolated parity (this rank's local blob) ----
  * which: 0 data (layer output), 1 grad (gradient w.r.t. the layer's SOURCE

@@ -150,6 +150,7 @@ SIGS = {
     "sg_net_last_launch_count": [P, PI64],
     "sg_net_profile": [P, I32],
     "sg_net_op_times": [P, C.POINTER(C.c_double), PI64, I32, PI32, I32],
+    "sg_net_op_timeline": [P, C.POINTER(C.c_double), C.POINTER(C.c_double), I32, PI32],
     "sg_blob_size": [P, I32, I32, C.POINTER(C.c_size_t)],
     "sg_blob_get": [P, I32, I32, P, C.c_size_t, P],
     "sg_blob_set": [P, I32, I32, P, C.c_size_t, P],

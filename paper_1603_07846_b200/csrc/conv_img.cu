@@ -124,7 +124,8 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
   const uint32_t wblk = (uint32_t)T * NB * 128, wbytes = (WSPLIT ? 1 : CB) * wblk;
   const uint32_t bar = wbase + wbytes, done_bar = bar + 8, wbar = done_bar + 8, wfree = wbar + 8, slot = wfree + 8;
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // warp index made warp-uniform (the MMA warp's loops then stay in uniform registers)
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   // sample n, tiles [t0, t0 + nvalid) of it (a sample's tiles may be split over `split` CTAs)
   const int n = blockIdx.x / a.split, t0 = (blockIdx.x % a.split) * NT;
   const int nvalid = min(NT, a.ntiles - t0);
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
     }
   }
   if (warp == 4) {
-    // ---- MMA issue: one lane, straight-line MMAs per tap ----
+    // ---- MMA issue: the whole warp, elected lane issues; straight-line MMAs per tap ----
     constexpr uint32_t idesc = idesc_tf32(128, NB, 0, DGRAD ? 1 : 0);
     const uint64_t ad0 = umma_desc_sw128(img, 16, 1024);
     const uint64_t bd0 =
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
           mbar_wait(wbar, (kb - 1) & 1);
           tc_fence_after();
         }
-        if (lane == 0) {
+        {
           int r = 0, sc = 0;
           for (int t = 0; t < T; ++t) {
             const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc) * 8 + kb * plane16;
@@ -196,19 +197,19 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
               if (i < nvalid)
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                  mma_tf32_lh(tmem + i * NB, a_t + (t0 + i) * 1024 + kk * 2, a_hi, b_c + kk * (DGRAD ? 64 : 2), b_hi,
+                  mma_tf32_lh_warp(tmem + i * NB, a_t + (t0 + i) * 1024 + kk * 2, a_hi, b_c + kk * (DGRAD ? 64 : 2), b_hi,
                               idesc, (t | kb | kk) ? 1u : 0u);
             if (++sc == a.S) {
               sc = 0;
               ++r;
             }
           }
-          mma_commit(kb + 1 < CB ? wfree : done_bar);
+          mma_commit_warp(kb + 1 < CB ? wfree : done_bar);
         }
         __syncwarp();
       }
     }
-    if (!WSPLIT && lane == 0) {
+    if (!WSPLIT) {
       int r = 0, sc = 0;
       for (int t = 0; t < T; ++t) {
         const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc) * 8;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
                                        : b_lo0 + ((uint32_t)(cb * T + t) * NB * 128 >> 4);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_tf32_lh(tmem + i * NB, a_t + (t0 + i) * 1024 + cb * plane16 + kk * 2, a_hi,
+              mma_tf32_lh_warp(tmem + i * NB, a_t + (t0 + i) * 1024 + cb * plane16 + kk * 2, a_hi,
                           b_c + kk * (DGRAD ? 64 : 2), b_hi, idesc, (t | cb | kk) ? 1u : 0u);
           }
         if (++sc == a.S) {
@@ -230,8 +231,8 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_kernel(const __grid_c
           ++r;
         }
       }
-      IMG_TRACE(2, 0);
-      mma_commit(done_bar);
+      if (lane == 0) IMG_TRACE(2, 0);
+      mma_commit_warp(done_bar);
     }
     __syncwarp();
   } else {
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __g
   const uint32_t wbytes = (uint32_t)a.R * a.SP * NB * 16;
   const uint32_t bar = wbase + ((wbytes + 1023) & ~1023u), done_bar = bar + 8, slot = done_bar + 8;
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   const int n = blockIdx.x / a.split, t0 = (blockIdx.x % a.split) * a.tpc;  // sample, first tile
   const int t1 = min(a.ntiles, t0 + a.tpc);
 
@@ -408,20 +409,17 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __g
     const uint32_t b_lo0 = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
     mbar_wait(bar, 0);
     tc_fence_after();
-    if (lane == 0) {
-      IMG_TRACE(3, 0);
-      bool first = true;
-      for (int r = 0; r < a.R; ++r)
-        for (int sc = 0; sc < a.S; sc += 2) {
-          const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc);  // 16-B pixel rows: start field += 1
-          const uint32_t b_t = b_lo0 + (uint32_t)(r * a.SP + sc) * NB;
-          for (int i = t0; i < t1; ++i)
-            mma_tf32_lh(tmem + (i - t0) * NB, a_t + i * 128, a_hi, b_t, b_hi, idesc, first ? 0u : 1u);
-          first = false;
-        }
-      IMG_TRACE(2, 0);
-      mma_commit(done_bar);
-    }
+    // whole warp, elected lane issues (uniform-register descriptors)
+    if (lane == 0) IMG_TRACE(3, 0);
+    for (int r = 0; r < a.R; ++r)
+      for (int sc = 0; sc < a.S; sc += 2) {
+        const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc);  // 16-B pixel rows: start field += 1
+        const uint32_t b_t = b_lo0 + (uint32_t)(r * a.SP + sc) * NB;
+        for (int i = t0; i < t1; ++i)
+          mma_tf32_lh_warp(tmem + (i - t0) * NB, a_t + i * 128, a_hi, b_t, b_hi, idesc, (r | sc) ? 1u : 0u);
+      }
+    if (lane == 0) IMG_TRACE(2, 0);
+    mma_commit_warp(done_bar);
     __syncwarp();
   } else {
     mbar_wait_sleep(done_bar, 0);
@@ -497,7 +495,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
   const uint32_t done_bar = bars + 32, slot = done_bar + 8;
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
   __shared__ float red[128];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   // sample group blockIdx.x / split; K steps (pixel rows of 8) [k0, k1) of it
   const int part = blockIdx.x % a.split;
   const int n0 = (blockIdx.x / a.split) * a.spc, n1 = min(a.nimg, n0 + a.spc), ns = n1 - n0;
@@ -529,8 +527,8 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
     for (int at = 0; at < NA; ++at) tma_load_4d(dyb + at * dy_plane, &a.dy_map, at * 32, 0, 0, n0 + k, bars + 8 * b);
   };
   if (warp == 4) {
-    if (lane == 0) {
-      // ---- MMA issue over the CTA's samples, accumulating in TMEM ----
+    {
+      // ---- MMA issue over the CTA's samples, accumulating in TMEM (whole warp, elected lane) ----
       constexpr uint32_t idesc = idesc_tf32(128, NB, 1, 1);
       for (int k = 0; k < ns; ++k) {
         const int b = k & 1;
@@ -543,12 +541,12 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
           const uint64_t ad0 = umma_desc_mn_sw128_32b(img + a.t_off[g] * 128, a.t_delta[g] * 128, 512);
           const uint32_t a_lo0 = (uint32_t)ad0, a_hi = (uint32_t)(ad0 >> 32);
           for (int ks = k0; ks < k1; ++ks)
-            mma_tf32_lh(tmem + g * NB, a_lo0 + ks * 64, a_hi, b_lo0 + ks * 64, b_hi, idesc,
+            mma_tf32_lh_warp(tmem + g * NB, a_lo0 + ks * 64, a_hi, b_lo0 + ks * 64, b_hi, idesc,
                         (k | (ks - k0)) ? 1u : 0u);
         }
-        if (k + 2 < ns) mma_commit(bars + 16 + 8 * b);  // buffer b is restaged once these complete
+        if (k + 2 < ns) mma_commit_warp(bars + 16 + 8 * b);  // buffer b is restaged once these complete
       }
-      mma_commit(done_bar);
+      mma_commit_warp(done_bar);
     }
     __syncwarp();
   } else {

@@ -945,7 +945,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   uint32_t* tmem_slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;  // warp-uniform role
   const int nkb_total = (args.K + GEMM_BK - 1) / GEMM_BK;
   const WorkDecode wd{(args.M + GEMM_BM - 1) / GEMM_BM, (args.N + BN - 1) / BN,
                       (nkb_total + args.kb_per_split - 1) / (args.kb_per_split > 0 ? args.kb_per_split : 1)};
@@ -1100,7 +1100,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
       }
     }
   } else if (warp == MMA_WARP) {
-    // --------------- MMA issuer: the whole warp waits, lane 0 issues ---------------
+    // ------- MMA issuer: the whole warp runs the loop, elect.sync picks the issuing lane -------
     constexpr uint32_t idesc = idesc_tf32(GEMM_BM, BN, LA::kMN & 1, LB::kMN & 1);
     int it = 0, local = 0;
     for (int w = blockIdx.x; w < nwork_it; w += gridDim.x, ++local) {
@@ -1125,20 +1125,20 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
           if (args.async_arrive) fence_proxy_async_smem();  // producers' generic-proxy writes -> tensor core
         }
         tc_fence_after();
-        if (lane == 0) {
+        {
           const uint32_t sa = sbase + s * STAGE_BYTES;
 #pragma unroll
           for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
             uint64_t ad = tile_desc<GEMM_BM, LA::kMN>(sa, kk);
             uint64_t bd = tile_desc<BN, LB::kMN>(sa + A_BYTES, kk);  // kMN also names the smem layout
-            mma_tf32(acc, ad, bd, idesc, (j | kk) ? 1u : 0u);
+            mma_tf32_warp(acc, ad, bd, idesc, (j | kk) ? 1u : 0u);
           }
-          mma_commit(bar_base + 8 * (STAGES + s));
-          SG_TRACE(3, it);
+          mma_commit_warp(bar_base + 8 * (STAGES + s));
+          if (lane == 0) SG_TRACE(3, it);
         }
         __syncwarp();
       }
-      if (lane == 0) mma_commit(tfull_bar + 8 * b);
+      mma_commit_warp(tfull_bar + 8 * b);
       __syncwarp();
     }
   } else {

@@ -100,7 +100,7 @@ struct sg_net {
   long long graph_launches = 0;
   long long last_launches = 0;
   // per-operation event timing (sg_net_profile)
-  bool prof = false, capturing = false;
+  bool prof = false, prof_concurrent = false, capturing = false;
   std::vector<cudaEvent_t> pev;  // 2 per slot, 4 slots per layer
   std::vector<char> pused;
   std::vector<double> pacc;
@@ -307,8 +307,9 @@ sg_status backward(sg_net* n, int i) {
   float* db = L.pb >= 0 ? n->sgr[L.store] + P.params[L.pb].store_off : nullptr;
   const int s1 = 4 * i + 1, s2 = 4 * i + 2;
   const int rn_dx = S.rn_grad ? RN_OUT : 0;  // this layer's dx is a GEMM operand (reading A19)
-  // weight gradient stream: the parameter stream (after dy is ready) or in line
-  const bool side = n->wgrad_side && (L.kind == SG_CONV || L.kind == SG_INNER_PRODUCT);
+  // weight gradient stream: the parameter stream (after dy is ready) or in line;
+  // in line while profiling, so every slot times its kernels alone
+  const bool side = n->wgrad_side && (!n->prof || n->prof_concurrent) && (L.kind == SG_CONV || L.kind == SG_INNER_PRODUCT);
   cudaStream_t wst = side ? n->ps : st;
   const Workspace wws = side ? n->ws2 : n->ws;
   if (side) {
@@ -1183,6 +1184,7 @@ SG_API sg_status sg_net_profile(sg_net* n, int32_t enable) {
     n->pcnt.assign(slots, 0);
   }
   n->prof = enable != 0;
+  n->prof_concurrent = enable == 2;
   if (n->gexec) {  // re-capture with / without the timing events
     SG_CUDA(cudaStreamSynchronize(n->cs));
     cudaGraphExecDestroy(n->gexec);
@@ -1217,6 +1219,32 @@ SG_API sg_status sg_net_op_times(sg_net* n, double* ms, int64_t* counts, int32_t
   if (reset) {
     std::fill(n->pacc.begin(), n->pacc.end(), 0.0);
     std::fill(n->pcnt.begin(), n->pcnt.end(), 0);
+  }
+  return SG_OK;
+}
+
+SG_API sg_status sg_net_op_timeline(sg_net* n, double* t_start, double* t_end, int32_t cap, int32_t* nslots) {
+  SG_CHECK(n && nslots && t_start && t_end, SG_ERR_INVALID_ARG, "null argument");
+  const int slots = 4 * (int)PL(n).layers.size();
+  *nslots = slots;
+  SG_CHECK(!n->pev.empty(), SG_ERR_INVALID_ARG, "profiling never enabled");
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  SG_CUDA(cudaStreamSynchronize(n->ps));
+  SG_CUDA(cudaStreamSynchronize(n->cs));
+  int first = -1;
+  for (int s = 0; s < slots && first < 0; ++s)
+    if (n->pused[s]) first = s;
+  for (int s = 0; s < slots && s < cap; ++s) {
+    t_start[s] = t_end[s] = -1.0;
+    float a = 0.f, b = 0.f;
+    if (first < 0 || !n->pused[s]) continue;
+    if (cudaEventElapsedTime(&a, n->pev[2 * first], n->pev[2 * s]) == cudaSuccess &&
+        cudaEventElapsedTime(&b, n->pev[2 * first], n->pev[2 * s + 1]) == cudaSuccess) {
+      t_start[s] = a;
+      t_end[s] = b;
+    } else {
+      cudaGetLastError();
+    }
   }
   return SG_OK;
 }

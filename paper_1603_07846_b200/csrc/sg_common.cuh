@@ -240,6 +240,21 @@ __device__ __forceinline__ void mma_tf32_warp(uint32_t tmem_d, uint64_t adesc, u
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// Whole-warp form with 32-bit descriptor halves (see mma_tf32_lh).
+__device__ __forceinline__ void mma_tf32_lh_warp(uint32_t tmem_d, uint32_t alo, uint32_t ahi, uint32_t blo,
+                                                 uint32_t bhi, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      " .reg .pred e, p;\n"
+      " .reg .b64 ad, bd;\n"
+      " mov.b64 ad, {%1, %2};\n"
+      " mov.b64 bd, {%3, %4};\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " setp.ne.b32 p, %6, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], ad, bd, %5, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void mma_commit_warp(uint32_t bar) {
   asm volatile(
       "{\n"

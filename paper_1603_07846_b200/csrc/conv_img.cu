@@ -354,13 +354,49 @@ cudaError_t run_img(ImgConvArgs a, size_t smem, int nimg, cudaStream_t st) {
 // with each filter row padded to an even number of taps (zero weights), so the
 // B operand of a tap pair is W[(r*SP + s) .. +1][co][4] with LBO = Co*16 B.
 struct Img4Args {
-  CUtensorMap img_map;  // x {4, W, H, N}, box {4, Wp, Hrows, 1}, no swizzle
-  CUtensorMap w_map;    // W {4, Co, T} (strides T*16, 16), box {4, Co, S}, no swizzle
+  CUtensorMap y_map;    // staged epilogue: y {Co, Ho*Wo, N}, box {32, kI4Box, 1}, SWIZZLE_128B
+  const float* x;       // [N][H][W][4]
+  const float* w;       // [Co][R][S][4]
+  int H, W;
   const float* bias;
   float* out;
   int pad, R, S, SP, Wp, Ho, Wo, Hrows, img_rows, ntiles, relu;  // relu: epilogue flags
   int split, tpc;  // CTAs per sample, tiles per CTA
+  int staged;      // 1: output tile staged in shared memory and written by TMA stores
+  uint32_t y_off;  // staged output: byte offset of the staging area from the aligned base
+  int y_rows;      // staged output rows per channel atom (Ho*Wo rounded up to kI4Box)
 };
+constexpr int kI4Box = 256;    // output pixels per TMA store box
+constexpr int kI4MaxTiles = 16;
+constexpr int kI4Group = 3;     // tiles per MMA commit group
+
+// The sample's output pixels p = oh*Wo + ow, staged as [atom][p][32 ch] rows of
+// 128 B in the TMA SWIZZLE_128B layout (16-B chunk c of row p at c ^ (p & 7)),
+// so a warp's 32 rows hit 8 distinct bank groups.
+template <int NB>
+__device__ __forceinline__ void img4_stage_tile(uint32_t tmem, int i, int t0, int warp, int lane, const Img4Args& a,
+                                                const float* bv, uint32_t ys) {
+  uint32_t r[NB / 16][16];
+#pragma unroll
+  for (int c = 0; c < NB / 16; ++c) tmem_ld16_nowait(tmem + ((uint32_t)(warp * 32) << 16) + i * NB + c * 16, r[c]);
+  tmem_wait_ld();
+  const int q = (t0 + i) * 128 + warp * 32 + lane;
+  const int oh = q / a.Wp, ow = q - oh * a.Wp;
+  if (oh >= a.Ho || ow >= a.Wo) return;
+  const uint32_t p = (uint32_t)(oh * a.Wo + ow);
+#pragma unroll
+  for (int j = 0; j < NB; j += 4) {
+    float4 o = make_float4(__uint_as_float(r[j / 16][j % 16]) + bv[j], __uint_as_float(r[j / 16][j % 16 + 1]) + bv[j + 1],
+                           __uint_as_float(r[j / 16][j % 16 + 2]) + bv[j + 2],
+                           __uint_as_float(r[j / 16][j % 16 + 3]) + bv[j + 3]);
+    if (a.relu & EPI_RELU) o = make_float4(fmaxf(o.x, 0.f), fmaxf(o.y, 0.f), fmaxf(o.z, 0.f), fmaxf(o.w, 0.f));
+    o = tf32_rna4_if(o, a.relu & EPI_RN);
+    const uint32_t at = (uint32_t)(j / 32), c = (uint32_t)((j % 32) / 4);
+    const uint32_t addr = ys + at * (uint32_t)a.y_rows * 128 + p * 128 + ((c ^ (p & 7)) << 4);
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w)
+                 : "memory");
+  }
+}
 
 template <int NB>
 __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __grid_constant__ Img4Args a) {
@@ -369,13 +405,18 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __g
   const uint32_t img = base;
   const uint32_t wbase = img + ((a.img_rows * 16 + 1023) & ~1023);
   const uint32_t wbytes = (uint32_t)a.R * a.SP * NB * 16;
-  const uint32_t bar = wbase + ((wbytes + 1023) & ~1023u), done_bar = bar + 8, slot = done_bar + 8;
+  // barriers: image+filter, then one per tile (its MMAs are done)
+  const uint32_t bar = wbase + ((wbytes + 1023) & ~1023u), tbar0 = bar + 8, slot = tbar0 + 8 * kI4MaxTiles;
+  const uint32_t ys = base + a.y_off;
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   const int n = blockIdx.x / a.split, t0 = (blockIdx.x % a.split) * a.tpc;  // sample, first tile
   const int t1 = min(a.ntiles, t0 + a.tpc);
 
-  // zero weights of the padding taps s in [S, SP) (disjoint from the TMA boxes)
+  // zero the padded image (the interior rows are then overwritten by bulk copies)
+  // and the weights of the padding taps s in [S, SP); both before the predecessor ends
+  for (int i = tid; i < a.img_rows; i += kImgThreads)
+    asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(img + i * 16), "f"(0.f) : "memory");
   for (int i = tid; i < a.R * (a.SP - a.S) * NB; i += kImgThreads) {
     const int r = i / ((a.SP - a.S) * NB), rem = i - r * (a.SP - a.S) * NB;
     const int sc = a.S + rem / NB, co = rem % NB;
@@ -385,10 +426,9 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __g
   fence_proxy_async_smem();
   if (tid == 0) {
     mbar_init(bar, 1);
-    mbar_init(done_bar, 1);
+    for (int i = 0; i < kI4MaxTiles; ++i) mbar_init(tbar0 + 8 * i, 1);
     fence_barrier_init();
-    prefetch_tmap(&a.img_map);
-    prefetch_tmap(&a.w_map);
+    if (a.staged) prefetch_tmap(&a.y_map);
   }
   if (warp == 4) tmem_alloc<512>(slot);
   tc_fence_before();
@@ -397,11 +437,34 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __g
   const uint32_t tmem = *slot_ptr;
   pdl_entry();
   if (tid == 0) {
+    // image rows: one contiguous bulk copy of W pixels x 16 B per row
     IMG_TRACE(5, 0);
-    mbar_arrive_expect_tx(bar, (uint32_t)a.Hrows * a.Wp * 16 + (uint32_t)a.R * a.S * NB * 16);
-    tma_load_4d(img, &a.img_map, 0, -a.pad, -a.pad, n, bar);
-    for (int r = 0; r < a.R; ++r) tma_load_3d(wbase + r * a.SP * NB * 16, &a.w_map, 0, 0, r * a.S, bar);
+    mbar_arrive_expect_tx(bar, (uint32_t)a.H * a.W * 16);
+    const float* xn = a.x + (size_t)n * a.H * a.W * 4;
+    for (int h = 0; h < a.H; ++h)
+      bulk_g2s(img + (uint32_t)((h + a.pad) * a.Wp + a.pad) * 16, xn + (size_t)h * a.W * 4, (uint32_t)a.W * 16, bar);
   }
+  // filter bank [co][r][s][4] -> shared [r][SP][co] 16-B rows (SIMT; all loads of a
+  // thread in flight before its stores)
+  for (int i0 = tid; i0 < NB * a.R * a.S; i0 += 8 * kImgThreads) {
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * kImgThreads;
+      if (i < NB * a.R * a.S) v[k] = __ldg(reinterpret_cast<const float4*>(a.w) + i);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = i0 + k * kImgThreads;
+      if (i >= NB * a.R * a.S) break;
+      const int co = i / (a.R * a.S), t = i - co * (a.R * a.S), r = t / a.S, sc = t - r * a.S;
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(wbase + ((r * a.SP + sc) * NB + co) * 16),
+                   "f"(v[k].x), "f"(v[k].y), "f"(v[k].z), "f"(v[k].w)
+                   : "memory");
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
   if (warp == 4) {
     constexpr uint32_t idesc = idesc_tf32(128, NB, 0, 0);
     const uint64_t ad0 = umma_desc_noswz(img, 16, 128), bd0 = umma_desc_noswz(wbase, NB * 16, 128);
@@ -409,24 +472,63 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img4_fwd_kernel(const __g
     const uint32_t b_lo0 = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
     mbar_wait(bar, 0);
     tc_fence_after();
-    // whole warp, elected lane issues (uniform-register descriptors)
+    // whole warp, elected lane issues (uniform-register descriptors); groups of
+    // kI4Group tiles, taps outer inside a group (consecutive MMAs go to
+    // independent accumulators), one commit per group, so the epilogue of a
+    // group overlaps the MMAs of the next
     if (lane == 0) IMG_TRACE(3, 0);
-    for (int r = 0; r < a.R; ++r)
-      for (int sc = 0; sc < a.S; sc += 2) {
-        const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc);  // 16-B pixel rows: start field += 1
-        const uint32_t b_t = b_lo0 + (uint32_t)(r * a.SP + sc) * NB;
-        for (int i = t0; i < t1; ++i)
-          mma_tf32_lh_warp(tmem + (i - t0) * NB, a_t + i * 128, a_hi, b_t, b_hi, idesc, (r | sc) ? 1u : 0u);
-      }
+    for (int g0 = t0; g0 < t1; g0 += kI4Group) {
+      const int g1 = min(t1, g0 + kI4Group);
+      for (int r = 0; r < a.R; ++r)
+        for (int sc = 0; sc < a.S; sc += 2) {
+          const uint32_t a_t = a_lo0 + (uint32_t)(r * a.Wp + sc);  // 16-B pixel rows: start field += 1
+          const uint32_t b_t = b_lo0 + (uint32_t)(r * a.SP + sc) * NB;
+          for (int i = g0; i < g1; ++i)
+            mma_tf32_lh_warp(tmem + (i - t0) * NB, a_t + i * 128, a_hi, b_t, b_hi, idesc, (r | sc) ? 1u : 0u);
+        }
+      mma_commit_warp(tbar0 + 8 * (g1 - 1 - t0));
+    }
     if (lane == 0) IMG_TRACE(2, 0);
-    mma_commit_warp(done_bar);
     __syncwarp();
   } else {
-    mbar_wait_sleep(done_bar, 0);
-    if (tid == 0) IMG_TRACE(4, 0);
-    tc_fence_after();
-    img_epilogue<NB>(tmem, t1 - t0, warp, lane, a.Wp, a.Ho, a.Wo, a.out + (size_t)n * a.Ho * a.Wo * NB, a.bias,
-                     a.relu, t0);
+    float bv[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) bv[c] = a.bias ? __ldg(a.bias + c) : 0.f;
+    if (a.staged) {
+      // TMEM -> swizzled shared staging -> TMA stores of whole 256-pixel boxes as soon as
+      // every tile covering them is staged (the last tile flushes the rest)
+      const int P = a.Ho * a.Wo;
+      int next_box = 0;
+      for (int i = 0; i < t1 - t0; ++i) {
+        mbar_wait_sleep(tbar0 + 8 * (min(t1 - t0, (i / kI4Group + 1) * kI4Group) - 1), 0);  // i's group
+        tc_fence_after();
+        if (i == 0 && tid == 0) IMG_TRACE(4, 0);
+        img4_stage_tile<NB>(tmem, i, t0, warp, lane, a, bv, ys);
+        fence_proxy_async_smem();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (tid == 0) {
+          // pixels staged so far: every q < (t0 + i + 1) * 128
+          const int qd = (t0 + i + 1) * 128;
+          const int pd = i + 1 == t1 - t0 ? P : min(P, (qd / a.Wp) * a.Wo + min(qd % a.Wp, a.Wo));
+          bool issued = false;
+          while (next_box * kI4Box < P && ((next_box + 1) * kI4Box <= pd || pd == P)) {
+            for (int at = 0; at < NB / 32; ++at)
+              tma_store_3d(&a.y_map, at * 32, next_box * kI4Box, n,
+                           ys + (uint32_t)at * a.y_rows * 128 + (uint32_t)next_box * kI4Box * 128);
+            ++next_box;
+            issued = true;
+          }
+          if (issued) bulk_commit();
+        }
+      }
+      if (tid == 0) bulk_wait_read0();  // the staging area is read; the writes complete with the grid
+    } else {
+      mbar_wait_sleep(tbar0 + 8 * (t1 - t0 - 1), 0);
+      if (tid == 0) IMG_TRACE(4, 0);
+      tc_fence_after();
+      img_epilogue<NB>(tmem, t1 - t0, warp, lane, a.Wp, a.Ho, a.Wo, a.out + (size_t)n * a.Ho * a.Wo * NB, a.bias,
+                       a.relu, t0);
+    }
   }
   if (tid == 0) IMG_TRACE(0, 0);
   tc_fence_before();
@@ -443,15 +545,25 @@ bool plan_img4(const ConvShape& s, Img4Args* a, size_t* smem) {
   g.pad = s.pad, g.R = s.R, g.S = s.S, g.SP = s.S + (s.S & 1);
   g.Wp = s.W + 2 * s.pad, g.Ho = s.Ho, g.Wo = s.Wo;
   g.ntiles = (g.Ho * g.Wp + 127) / 128;
-  if (g.ntiles * s.Co > 512) return false;
+  if (g.ntiles * s.Co > 512 || g.ntiles > kI4MaxTiles) return false;
   // rows read: tiles x 128 + the largest tap shift + the pair's second pixel
   const int need = g.ntiles * 128 + (s.R - 1) * g.Wp + g.SP - 1;
   g.Hrows = (need + g.Wp - 1) / g.Wp;
   g.img_rows = g.Hrows * g.Wp;
   if (g.Hrows > 256 || g.Wp > 256 || s.S > 256) return false;
-  *smem = 1024 + (((size_t)g.img_rows * 16 + 1023) & ~(size_t)1023) +
-          (((size_t)s.R * g.SP * s.Co * 16 + 1023) & ~(size_t)1023) + 64;
+  const size_t core = (((size_t)g.img_rows * 16 + 1023) & ~(size_t)1023) +
+                      (((size_t)s.R * g.SP * s.Co * 16 + 1023) & ~(size_t)1023) + 1024;  // + barriers / slot
+  *smem = 1024 + core;
   if (*smem > 227 * 1024) return false;
+  // staged epilogue when the sample's whole output fits next to the operands
+  g.y_rows = (g.Ho * g.Wo + kI4Box - 1) / kI4Box * kI4Box;
+  const size_t ybytes = (size_t)(s.Co / 32) * g.y_rows * 128;
+  static const int stage_env = getenv("SG_IMG4_STAGED") ? atoi(getenv("SG_IMG4_STAGED")) : 1;
+  if (stage_env && 1024 + core + ybytes <= 227 * 1024 && g.Ho * g.Wo <= 256 * kI4Box) {
+    g.staged = 1;
+    g.y_off = (uint32_t)core;
+    *smem = 1024 + core + ybytes;
+  }
   *a = g;
   return true;
 }
@@ -773,20 +885,23 @@ cudaError_t conv_img_fwd(const ConvShape& s, const float* x, const float* W, con
     a4.bias = b;
     a4.out = y;
     a4.relu = relu;
-    const int T = s.R * s.S;
-    const cuuint64_t xd[4] = {4, (cuuint64_t)s.W, (cuuint64_t)s.H, (cuuint64_t)s.N};
-    const cuuint64_t xs[3] = {16, (cuuint64_t)s.W * 16, (cuuint64_t)s.H * s.W * 16};
-    const cuuint32_t xb[4] = {4, (cuuint32_t)a4.Wp, (cuuint32_t)a4.Hrows, 1};
-    const cuuint64_t wd[3] = {4, (cuuint64_t)s.Co, (cuuint64_t)T};
-    const cuuint64_t ws[2] = {(cuuint64_t)T * 16, 16};
-    const cuuint32_t wb[3] = {4, (cuuint32_t)s.Co, (cuuint32_t)s.S};
-    if (!encode_tiled_f32(&a4.img_map, x, 4, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-        !encode_tiled_f32(&a4.w_map, W, 3, wd, ws, wb, CU_TENSOR_MAP_SWIZZLE_NONE))
-      return cudaErrorInvalidValue;
+    a4.x = x;
+    a4.w = W;
+    a4.H = s.H, a4.W = s.W;
+    a4.tpc = img_split(a4.ntiles, s.N, &a4.split);
+    if (a4.staged && a4.split > 1) {  // a split sample's CTAs own partial image rows: direct stores
+      a4.staged = 0;
+      smem = 1024 + a4.y_off;
+    }
+    if (a4.staged) {
+      const cuuint64_t yd[3] = {(cuuint64_t)s.Co, (cuuint64_t)s.Ho * s.Wo, (cuuint64_t)s.N};
+      const cuuint64_t ys[2] = {(cuuint64_t)s.Co * 4, (cuuint64_t)s.Ho * s.Wo * s.Co * 4};
+      const cuuint32_t yb[3] = {32, (cuuint32_t)kI4Box, 1};
+      if (!encode_tiled_f32(&a4.y_map, y, 3, yd, ys, yb, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+    }
     auto k = s.Co == 32 ? conv_img4_fwd_kernel<32> : conv_img4_fwd_kernel<64>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    a4.tpc = img_split(a4.ntiles, s.N, &a4.split);
     return launch_k(k, s.N * a4.split, kImgThreads, smem, st, a4);
   }
   if (!plan_img(s, false, &a, &smem)) return cudaErrorInvalidValue;

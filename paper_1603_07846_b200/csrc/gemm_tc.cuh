@@ -553,6 +553,17 @@ struct ScratchOf<T, std::void_t<decltype(T::kScratch)>> {
   static constexpr int value = T::kScratch;
 };
 
+// Producer warps issuing the A operand's TMA boxes (kIssueWarps parts, each part
+// issued by its own warp, the B operand by one more warp); 1 unless declared.
+template <class T, class = void>
+struct IssueWarpsOf {
+  static constexpr int value = 1;
+};
+template <class T>
+struct IssueWarpsOf<T, std::void_t<decltype(T::kIssueWarps)>> {
+  static constexpr int value = T::kIssueWarps;
+};
+
 // ------------------------------------------------------------ TMA loaders --
 // One elected producer thread issues cp.async.bulk.tensor per operand per stage
 // (tensor maps encoded on the host after the tile shape is chosen; layouts
@@ -703,6 +714,10 @@ struct TmaDgradB {
 struct TmaWgradA {
   static constexpr int kMN = 1;
   static constexpr bool kTMA = true;
+  // one 32-pixel im2col box per 32-channel atom: the issue of a box costs ~200
+  // cycles of the issuing thread (tools/gemm_trace.py), so the 4 atoms of a
+  // stage are issued by 4 producer warps side by side
+  static constexpr int kIssueWarps = 4;
   CUtensorMap map;
   int C, S, Ho, Wo, st, pad;
   int valid, ones_row;
@@ -725,6 +740,22 @@ struct TmaWgradA {
     mbar_expect_tx(bar, cnt * 32 * 128);
 #pragma unroll
     for (int a = 0; a < T / 32; ++a) {
+      const int kg = kg0 + 32 * a;
+      if (kg >= valid) continue;
+      const int rs = fC.div(kg), c0 = kg - rs * C;
+      const int r = fS.div(rs), s = rs - r * S;
+      tma_load_im2col(sm + a * (GEMM_BK * 128), &map, c0, ow * st - pad, oh * st - pad, n, s, r, bar);
+    }
+  }
+  // atoms a = part, part + kIssueWarps, ... of the stage (own expect_tx)
+  template <int T>
+  __device__ __forceinline__ void issue_part(uint32_t sm, int kg0, int k0, uint32_t bar, int part) const {
+    const int n = fHoWo.div(k0), rem = k0 - n * Ho * Wo;
+    const int oh = fWo.div(rem), ow = rem - oh * Wo;
+    int cnt = 0;
+    for (int a = part; a < T / 32; a += kIssueWarps) cnt += (kg0 + 32 * a < valid);
+    if (cnt) mbar_expect_tx(bar, cnt * 32 * 128);
+    for (int a = part; a < T / 32; a += kIssueWarps) {
       const int kg = kg0 + 32 * a;
       if (kg >= valid) continue;
       const int rs = fC.div(kg), c0 = kg - rs * C;
@@ -791,7 +822,7 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t sm, int kk) {
 template <int BN, int SCRATCH = 0>
 constexpr int gemm_stages() {
   // default depth; with a loader scratch as many stages as fit 225 KB
-  constexpr int d = BN <= 32 ? 8 : BN <= 64 ? 7 : BN <= 128 ? 6 : 4;
+  constexpr int d = BN <= 32 ? 8 : BN <= 64 ? 7 : BN <= 128 ? 6 : BN <= 192 ? 5 : 4;
   constexpr int fit = (225 * 1024 - SCRATCH) / ((GEMM_BM + BN) * GEMM_BK * 4);
   return d < fit ? d : fit;
 }
@@ -921,7 +952,8 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   constexpr int A_BYTES = GEMM_BM * GEMM_BK * 4;
   constexpr int B_BYTES = BN * GEMM_BK * 4;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  // two accumulator buffers, allocation rounded up to a power of two (BN = 192: 512)
+  constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   constexpr int LAG = STAGES > 2 ? STAGES - 2 : 1;
   constexpr int MMA_WARP = GEMM_PRODUCERS / 32;
   constexpr int EPI_WARP0 = MMA_WARP + 1;
@@ -932,6 +964,10 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
 
   constexpr int SCRATCH = ScratchOf<LA>::value;
   static_assert(ScratchOf<LB>::value == 0, "scratch is an A-operand feature");
+  // TMA producer warps: 1 (A and B by one thread) or A parts + 1 for B
+  constexpr int NA_ISSUE = IssueWarpsOf<LA>::value;
+  constexpr int NPW = NA_ISSUE > 1 ? NA_ISSUE + 1 : 1;
+  static_assert(NPW * 32 <= GEMM_PRODUCERS, "issue warps");
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -969,7 +1005,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(bar_base + 8 * s, TMA ? 1 : GEMM_PRODUCERS);  // TMA thread / every producer thread
+      mbar_init(bar_base + 8 * s, TMA ? NPW : GEMM_PRODUCERS);  // TMA issuing warps / every producer thread
       mbar_init(bar_base + 8 * (STAGES + s), 1);              // tcgen05.commit
     }
     for (int b = 0; b < 2; ++b) {
@@ -996,7 +1032,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   if (warp < MMA_WARP) {
     // ------------------------------- producers -------------------------------
     if constexpr (TMA) {
-      if (warp == 0) {
+      if (warp < NPW) {
         int it = 0;
         int tagA[STAGES], tagB[STAGES];  // row0 the stage's constant atoms were written for
 #pragma unroll
@@ -1011,13 +1047,13 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
             const int s = it % STAGES;
             const int round = it / STAGES;
             if (round > 0) mbar_wait(bar_base + 8 * (STAGES + s), (round - 1) & 1);
-            if (lane == 0) SG_TRACE(0, it);
+            if (lane == 0 && warp == 0) SG_TRACE(0, it);
             const uint32_t sa = sbase + s * STAGE_BYTES;
-            // constant operand atoms (zeros / the bias ones-row) are written by the warp
+            // constant operand atoms (zeros / the bias ones-row) are written by warp 0
             bool wrote = false;
 #pragma unroll
             for (int q = 0; q < STAGES; ++q) {
-              if (q != s) continue;
+              if (q != s || warp != 0) continue;
               // (a tag names the row0 whose constant atoms the stage holds; a tile
               // without constant atoms lets TMA overwrite them, clearing the tag)
               if (!args.a.template needs_prefill<GEMM_BM>(m0)) {
@@ -1042,10 +1078,17 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
             if (lane == 0) {
               const uint32_t full = bar_base + 8 * s;
               const int k0 = (kb0 + j) * GEMM_BK;
-              args.a.template issue<GEMM_BM>(sa, m0, k0, full);
-              args.b.template issue<BN>(sa + A_BYTES, n0, k0, full);
-              mbar_arrive(full);
-              SG_TRACE(1, it);
+              if constexpr (NPW == 1) {
+                args.a.template issue<GEMM_BM>(sa, m0, k0, full);
+                args.b.template issue<BN>(sa + A_BYTES, n0, k0, full);
+              } else {
+                if (warp < NA_ISSUE)
+                  args.a.template issue_part<GEMM_BM>(sa, m0, k0, full, warp);
+                else
+                  args.b.template issue<BN>(sa + A_BYTES, n0, k0, full);
+              }
+              mbar_arrive(full);  // after this warp's expect_tx (the phase needs all NPW arrivals)
+              if (warp == 0) SG_TRACE(1, it);
             }
             __syncwarp();
           }

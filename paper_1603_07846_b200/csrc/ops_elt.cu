@@ -105,36 +105,103 @@ PoolK pool_k(const PoolShape& s) {
                make_fastdiv(s.H), make_fastdiv(s.s)};
 }
 
+// Window scans of the pooling forward.  KS > 0: the k x k window is a compile-time
+// size, its loads are all issued before the compares (out-of-range taps
+// predicated off); KS == 0: runtime k.  Same (h, w) scan order either way, so
+// the same bits and argmax (first maximum, strict >; reading A5).
+template <int KS>
+__device__ __forceinline__ float4 maxpool_at(const PoolK& P, const float* __restrict__ x, int i, uchar4& arg) {
+  const PoolShape& s = P.s;
+  const int C4 = s.C >> 2;
+  const int t = P.fC4.div(i), c4 = i - t * C4;
+  const int t2 = P.fWo.div(t), ow = t - t2 * s.Wo;
+  const int n = P.fHo.div(t2), oh = t2 - n * s.Ho;
+  const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
+  const int hs = max(h0, 0), he = min(h0 + s.k, s.H), ws = max(w0, 0), we = min(w0 + s.k, s.W);
+  float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  int a[4] = {0, 0, 0, 0};
+  const float* xn = x + (size_t)n * s.H * s.W * s.C + c4 * 4;
+  auto take = [&](const float4& v, int off) {
+    if (v.x > m[0]) { m[0] = v.x; a[0] = off; }
+    if (v.y > m[1]) { m[1] = v.y; a[1] = off; }
+    if (v.z > m[2]) { m[2] = v.z; a[2] = off; }
+    if (v.w > m[3]) { m[3] = v.w; a[3] = off; }
+  };
+  if constexpr (KS > 0) {
+    float4 v[KS * KS];
+#pragma unroll
+    for (int dh = 0; dh < KS; ++dh)
+#pragma unroll
+      for (int dw = 0; dw < KS; ++dw) {
+        const int h = h0 + dh, w = w0 + dw;
+        const bool ok = h >= hs && h < he && w >= ws && w < we;
+        v[dh * KS + dw] = ok ? __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C))
+                             : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+#pragma unroll
+    for (int j = 0; j < KS * KS; ++j) take(v[j], j);  // -inf never beats the running maximum
+  } else {
+    for (int h = hs; h < he; ++h)
+      for (int w = ws; w < we; ++w)
+        take(__ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C)), (h - h0) * s.k + (w - w0));
+  }
+  arg = make_uchar4(a[0], a[1], a[2], a[3]);
+  return make_float4(m[0], m[1], m[2], m[3]);
+}
+template <int KS>
+__device__ __forceinline__ float4 avgpool_at(const PoolK& P, const float* __restrict__ x, int i) {
+  const PoolShape& s = P.s;
+  const int C4 = s.C >> 2;
+  const int t = P.fC4.div(i), c4 = i - t * C4;
+  const int t2 = P.fWo.div(t), ow = t - t2 * s.Wo;
+  const int n = P.fHo.div(t2), oh = t2 - n * s.Ho;
+  const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
+  const int he_u = min(h0 + s.k, s.H + s.p), we_u = min(w0 + s.k, s.W + s.p);
+  const float inv = 1.f / (float)((he_u - h0) * (we_u - w0));
+  const int hs = max(h0, 0), he = min(he_u, s.H), ws = max(w0, 0), we = min(we_u, s.W);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* xn = x + (size_t)n * s.H * s.W * s.C + c4 * 4;
+  if constexpr (KS > 0) {
+    float4 v[KS * KS];
+    bool ok[KS * KS];
+#pragma unroll
+    for (int dh = 0; dh < KS; ++dh)
+#pragma unroll
+      for (int dw = 0; dw < KS; ++dw) {
+        const int h = h0 + dh, w = w0 + dw;
+        ok[dh * KS + dw] = h >= hs && h < he && w >= ws && w < we;
+        v[dh * KS + dw] = ok[dh * KS + dw] ? __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C))
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+    for (int j = 0; j < KS * KS; ++j)
+      if (ok[j]) {  // the in-range taps in scan order, as the runtime loop adds them
+        acc.x += v[j].x; acc.y += v[j].y; acc.z += v[j].z; acc.w += v[j].w;
+      }
+  } else {
+    for (int h = hs; h < he; ++h)
+      for (int w = ws; w < we; ++w) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C));
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+  }
+  return make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+}
+
 // Thread per (n, oh, ow, 4 channels).  Window origin (oh*s - p, ow*s - p);
 // the argmax is stored as the uint8 offset (h - h0)*k + (w - w0); first maximum
 // in (h, w) scan order (strict >), reading A5.
+template <int KS>
 __global__ void maxpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* __restrict__ y,
                                    uint8_t* __restrict__ arg, float* __restrict__ relu_out, int rn) {
   pdl_entry();
   const PoolShape& s = P.s;
-  const int C4 = s.C >> 2;
-  const int total = s.N * s.Ho * s.Wo * C4;
+  const int total = s.N * s.Ho * s.Wo * (s.C >> 2);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int t = P.fC4.div(i), c4 = i - t * C4;
-    const int t2 = P.fWo.div(t), ow = t - t2 * s.Wo;
-    const int n = P.fHo.div(t2), oh = t2 - n * s.Ho;
-    const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
-    const int hs = max(h0, 0), he = min(h0 + s.k, s.H), ws = max(w0, 0), we = min(w0 + s.k, s.W);
-    float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    int a[4] = {0, 0, 0, 0};
-    const float* xn = x + (size_t)n * s.H * s.W * s.C + c4 * 4;
-    for (int h = hs; h < he; ++h)
-      for (int w = ws; w < we; ++w) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C));
-        const int off = (h - h0) * s.k + (w - w0);
-        if (v.x > m[0]) { m[0] = v.x; a[0] = off; }
-        if (v.y > m[1]) { m[1] = v.y; a[1] = off; }
-        if (v.z > m[2]) { m[2] = v.z; a[2] = off; }
-        if (v.w > m[3]) { m[3] = v.w; a[3] = off; }
-      }
-    const float4 o = make_float4(m[0], m[1], m[2], m[3]);
+    uchar4 a4;
+    const float4 o = maxpool_at<KS>(P, x, i, a4);
     *reinterpret_cast<float4*>(y + (size_t)i * 4) = tf32_rna4_if(o, rn & RN_OUT);
-    *reinterpret_cast<uchar4*>(arg + (size_t)i * 4) = make_uchar4(a[0], a[1], a[2], a[3]);
+    *reinterpret_cast<uchar4*>(arg + (size_t)i * 4) = a4;
     if (relu_out) *reinterpret_cast<float4*>(relu_out + (size_t)i * 4) = tf32_rna4_if(relu4(o), rn & RN_AUX);
   }
 }
@@ -207,28 +274,14 @@ __global__ void maxpool_bwd_kernel(PoolK P, const float* __restrict__ dy, const 
   }
 }
 
+template <int KS>
 __global__ void avgpool_fwd_kernel(PoolK P, const float* __restrict__ x, float* __restrict__ y,
                                    float* __restrict__ relu_out, int rn) {
   pdl_entry();
   const PoolShape& s = P.s;
-  const int C4 = s.C >> 2;
-  const int total = s.N * s.Ho * s.Wo * C4;
+  const int total = s.N * s.Ho * s.Wo * (s.C >> 2);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int t = P.fC4.div(i), c4 = i - t * C4;
-    const int t2 = P.fWo.div(t), ow = t - t2 * s.Wo;
-    const int n = P.fHo.div(t2), oh = t2 - n * s.Ho;
-    const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
-    const int he_u = min(h0 + s.k, s.H + s.p), we_u = min(w0 + s.k, s.W + s.p);
-    const float inv = 1.f / (float)((he_u - h0) * (we_u - w0));
-    const int hs = max(h0, 0), he = min(he_u, s.H), ws = max(w0, 0), we = min(we_u, s.W);
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float* xn = x + (size_t)n * s.H * s.W * s.C + c4 * 4;
-    for (int h = hs; h < he; ++h)
-      for (int w = ws; w < we; ++w) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C));
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
-    const float4 o = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    const float4 o = avgpool_at<KS>(P, x, i);
     *reinterpret_cast<float4*>(y + (size_t)i * 4) = tf32_rna4_if(o, rn & RN_OUT);
     if (relu_out) *reinterpret_cast<float4*>(relu_out + (size_t)i * 4) = tf32_rna4_if(relu4(o), rn & RN_AUX);
   }
@@ -357,50 +410,7 @@ __global__ void lrn_fwd_kernel(LrnK K, const float* __restrict__ x, float* __res
 // 4 channels), the LRN channel window by warp shuffles; writes the pooling
 // output (+ argmax), the ReLU output and the LRN output + scale, each computed
 // exactly as by the separate kernels.
-__device__ __forceinline__ float4 maxpool_at(const PoolK& P, const float* __restrict__ x, int i, uchar4& arg) {
-  const PoolShape& s = P.s;
-  const int C4 = s.C >> 2;
-  const int t = P.fC4.div(i), c4 = i - t * C4;
-  const int t2 = P.fWo.div(t), ow = t - t2 * s.Wo;
-  const int n = P.fHo.div(t2), oh = t2 - n * s.Ho;
-  const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
-  const int hs = max(h0, 0), he = min(h0 + s.k, s.H), ws = max(w0, 0), we = min(w0 + s.k, s.W);
-  float m[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-  int a[4] = {0, 0, 0, 0};
-  const float* xn = x + (size_t)n * s.H * s.W * s.C + c4 * 4;
-  for (int h = hs; h < he; ++h)
-    for (int w = ws; w < we; ++w) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C));
-      const int off = (h - h0) * s.k + (w - w0);
-      if (v.x > m[0]) { m[0] = v.x; a[0] = off; }
-      if (v.y > m[1]) { m[1] = v.y; a[1] = off; }
-      if (v.z > m[2]) { m[2] = v.z; a[2] = off; }
-      if (v.w > m[3]) { m[3] = v.w; a[3] = off; }
-    }
-  arg = make_uchar4(a[0], a[1], a[2], a[3]);
-  return make_float4(m[0], m[1], m[2], m[3]);
-}
-__device__ __forceinline__ float4 avgpool_at(const PoolK& P, const float* __restrict__ x, int i) {
-  const PoolShape& s = P.s;
-  const int C4 = s.C >> 2;
-  const int t = P.fC4.div(i), c4 = i - t * C4;
-  const int t2 = P.fWo.div(t), ow = t - t2 * s.Wo;
-  const int n = P.fHo.div(t2), oh = t2 - n * s.Ho;
-  const int h0 = oh * s.s - s.p, w0 = ow * s.s - s.p;
-  const int he_u = min(h0 + s.k, s.H + s.p), we_u = min(w0 + s.k, s.W + s.p);
-  const float inv = 1.f / (float)((he_u - h0) * (we_u - w0));
-  const int hs = max(h0, 0), he = min(he_u, s.H), ws = max(w0, 0), we = min(we_u, s.W);
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float* xn = x + (size_t)n * s.H * s.W * s.C + c4 * 4;
-  for (int h = hs; h < he; ++h)
-    for (int w = ws; w < we; ++w) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(xn + (h * s.W + w) * s.C));
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-    }
-  return make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-}
-
-template <bool MAX>
+template <bool MAX, int KS>
 __global__ void pool_lrn_fwd_kernel(PoolK P, LrnK K, const float* __restrict__ x, float* __restrict__ py,
                                     uint8_t* __restrict__ arg, float* __restrict__ relu_out, float* __restrict__ ly,
                                     float* __restrict__ scale, int rn) {
@@ -412,7 +422,7 @@ __global__ void pool_lrn_fwd_kernel(PoolK P, LrnK K, const float* __restrict__ x
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (in) {
       uchar4 a4;
-      v = MAX ? maxpool_at(P, x, i, a4) : avgpool_at(P, x, i);
+      v = MAX ? maxpool_at<KS>(P, x, i, a4) : avgpool_at<KS>(P, x, i);
       reinterpret_cast<float4*>(py)[i] = v;
       if (MAX) reinterpret_cast<uchar4*>(arg)[i] = a4;
       if (relu_out) {
@@ -730,7 +740,8 @@ cudaError_t maxpool_fwd(const PoolShape& s, const float* x, float* y, uint8_t* a
   const long long n = (long long)s.N * s.Ho * s.Wo * s.C / 4;
   if (s.C % 4 || s.k * s.k > 256 || !fits32(n * 4) || !fits32((long long)s.N * s.H * s.W * s.C))
     return cudaErrorInvalidValue;
-  return launch_k(maxpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y, arg, relu_out, rn);
+  return launch_k(s.k == 3 ? maxpool_fwd_kernel<3> : maxpool_fwd_kernel<0>, blocks_for(n, 256), 256, 0, st, pool_k(s), x,
+                  y, arg, relu_out, rn);
 }
 cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg, float* dx, cudaStream_t st,
                         const float* relu_y, float* dx_relu, int rn) {
@@ -741,7 +752,8 @@ cudaError_t maxpool_bwd(const PoolShape& s, const float* dy, const uint8_t* arg,
 cudaError_t avgpool_fwd(const PoolShape& s, const float* x, float* y, cudaStream_t st, float* relu_out, int rn) {
   const long long n = (long long)s.N * s.Ho * s.Wo * s.C / 4;
   if (s.C % 4 || !fits32(n * 4) || !fits32((long long)s.N * s.H * s.W * s.C)) return cudaErrorInvalidValue;
-  return launch_k(avgpool_fwd_kernel, blocks_for(n, 256), 256, 0, st, pool_k(s), x, y, relu_out, rn);
+  return launch_k(s.k == 3 ? avgpool_fwd_kernel<3> : avgpool_fwd_kernel<0>, blocks_for(n, 256), 256, 0, st, pool_k(s), x,
+                  y, relu_out, rn);
 }
 cudaError_t avgpool_bwd(const PoolShape& s, const float* dy, float* dx, cudaStream_t st, const float* relu_y,
                         float* dx_relu, int rn) {
@@ -789,11 +801,9 @@ cudaError_t pool_lrn_fwd(const PoolShape& ps, bool max_pool, const float* x, flo
       !fits32((long long)ps.N * ps.H * ps.W * ps.C) || (max_pool && ps.k * ps.k > 256) ||
       !lrn_fast(ls, {py, ly, scale, relu_out ? relu_out : py}, &k))
     return cudaErrorInvalidValue;
-  if (max_pool)
-    return launch_k(pool_lrn_fwd_kernel<true>, blocks_for(k.total, 256), 256, 0, st, pool_k(ps), k, x, py, arg,
-                    relu_out, ly, scale, rn);
-  return launch_k(pool_lrn_fwd_kernel<false>, blocks_for(k.total, 256), 256, 0, st, pool_k(ps), k, x, py, arg,
-                  relu_out, ly, scale, rn);
+  auto kern = max_pool ? (ps.k == 3 ? pool_lrn_fwd_kernel<true, 3> : pool_lrn_fwd_kernel<true, 0>)
+                      : (ps.k == 3 ? pool_lrn_fwd_kernel<false, 3> : pool_lrn_fwd_kernel<false, 0>);
+  return launch_k(kern, blocks_for(k.total, 256), 256, 0, st, pool_k(ps), k, x, py, arg, relu_out, ly, scale, rn);
 }
 bool pool_lrn_fusable(const PoolShape& ps, const LrnShape& ls) {
   LrnK k;

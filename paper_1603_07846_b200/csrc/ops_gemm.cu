@@ -62,15 +62,20 @@ struct Plan {
 
 inline long long pad4(int n) { return (n + 3) & ~3; }
 
-Plan plan_gemm(int M, int N, int K, size_t ws_floats_avail) {
+Plan plan_gemm(int M, int N, int K, size_t ws_floats_avail, bool wide192 = true) {
   Plan p;
   static const int big_bn = getenv("SG_BN_BIG") ? atoi(getenv("SG_BN_BIG")) : 1;
+  static const int bn192 = getenv("SG_BN192") ? atoi(getenv("SG_BN192")) : 1;
   p.bn = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  // N a multiple of 192 (AlexNet conv2 192, conv3 384 channels): 192-wide tiles
+  // waste no accumulator columns (256-wide: 75% used); not for the TMA weight
+  // gradient, whose long-K split plan measured slower with them (AlexNet conv2 325 -> 343 us)
+  if (bn192 && wide192 && N > 128 && N % 192 == 0) p.bn = 192;
   p.mt = (M + GEMM_BM - 1) / GEMM_BM;
   const int nkb0 = (K + GEMM_BK - 1) / GEMM_BK;
   // wide tiles halve the operand bytes per MMA; keep them when split-K can fill the machine
   const bool can_split = nkb0 >= 2 * kMinKbPerSplit * ((kNumSMs + p.mt - 1) / p.mt);
-  if (p.bn == 256 && p.mt * ((N + 255) / 256) < kNumSMs && !(big_bn && can_split)) p.bn = 128;
+  if (p.bn >= 192 && p.mt * ((N + p.bn - 1) / p.bn) < kNumSMs && !(big_bn && can_split)) p.bn = 128;
   p.nt = (N + p.bn - 1) / p.bn;
   const int nkb = (K + GEMM_BK - 1) / GEMM_BK;
   const int tiles = p.mt * p.nt;
@@ -204,6 +209,7 @@ cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int
     case 32: e = launch_bn<32>(args, p, st); break;
     case 64: e = launch_bn<64>(args, p, st); break;
     case 128: e = launch_bn<128>(args, p, st); break;
+    case 192: e = launch_bn<192>(args, p, st); break;
     default: e = launch_bn<256>(args, p, st); break;
   }
   if (e != cudaSuccess || p.splits == 1 || fixup) return e;
@@ -697,7 +703,7 @@ cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, floa
     a.fS = make_fastdiv(s.S);
     a.fHoWo = make_fastdiv(s.Ho * s.Wo);
     a.fWo = make_fastdiv(s.Wo);
-    const Plan p = plan_gemm(M, s.Co, Mtot, ws.floats);
+    const Plan p = plan_gemm(M, s.Co, Mtot, ws.floats, false);
     TmaMN bd = tma_mn(vplain(dy, Mtot, s.Co, s.Co), s.Co, -1, p.bn, &ok);
     if (ok) return run_gemm_planned(a, bd, p, M, s.Co, Mtot, e, ws, st);
   }

@@ -678,17 +678,21 @@ struct TmaIm2col {
     }
     const int n = fHW.div(m0), rem = m0 - n * gH * gW;
     const int y = fW.div(rem), x = rem - y * gW;
-    mbar_expect_tx(bar, 128 * 128);
+    mbar_expect_tx(bar, T * 128);  // one box of T pixels (encoded for the tile height)
     tma_load_im2col(sm, &map, c0, x * st + lo, y * st + lo, n, s, r, bar);
   }
 };
 
-// Data-gradient B(c, k = (rs, co)) = W[co][rs][c]: 3-D map {C, RS, Co}, box {32, 1, 32}.
+// Data-gradient B(c, k = (rs, co)) = W[co][rs][c]: 3-D map {C, RS, Co}, box
+// {32, 1, 32} per 32-channel atom, or (atoms4) the whole tile as ONE box of the
+// 4-D view {32, RS, Co, C/32}, box {32, 1, 32, BN/32} (atom-consecutive in shared
+// memory, channels past C zero-filled): one TMA issue per stage instead of BN/32.
 struct TmaDgradB {
   static constexpr int kMN = 1;
   static constexpr bool kTMA = true;
   CUtensorMap map;
   int C, Co;
+  int atoms4;
   FastDiv fCo;
   template <int T>
   __device__ __forceinline__ bool needs_prefill(int) const {
@@ -699,6 +703,11 @@ struct TmaDgradB {
   template <int T>
   __device__ __forceinline__ void issue(uint32_t sm, int c0, int k0, uint32_t bar) const {
     const int rs = fCo.div(k0), co0 = k0 - rs * Co;
+    if (atoms4) {
+      mbar_expect_tx(bar, T * 128);
+      tma_load_4d(sm, &map, 0, rs, co0, c0 >> 5, bar);
+      return;
+    }
     int n = 0;
 #pragma unroll
     for (int a = 0; a < T / 32; ++a) n += (c0 + 32 * a < C);
@@ -819,17 +828,19 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t sm, int kk) {
   }
 }
 
-template <int BN, int SCRATCH = 0>
+// MT = M tiles of 128 rows per CTA work item (2: a 256-row tile, both halves
+// sharing the B stage: twice the MMA work per B box for narrow N).
+template <int BN, int SCRATCH = 0, int MT = 1>
 constexpr int gemm_stages() {
   // default depth; with a loader scratch as many stages as fit 225 KB
-  constexpr int d = BN <= 32 ? 8 : BN <= 64 ? 7 : BN <= 128 ? 6 : BN <= 192 ? 5 : 4;
-  constexpr int fit = (225 * 1024 - SCRATCH) / ((GEMM_BM + BN) * GEMM_BK * 4);
+  constexpr int d = MT == 2 ? 5 : BN <= 32 ? 8 : BN <= 64 ? 7 : BN <= 128 ? 6 : BN <= 192 ? 5 : 4;
+  constexpr int fit = (225 * 1024 - SCRATCH) / ((MT * GEMM_BM + BN) * GEMM_BK * 4);
   return d < fit ? d : fit;
 }
 
-template <int BN, int STAGES, int SCRATCH = 0>
+template <int BN, int STAGES, int SCRATCH = 0, int MT = 1>
 constexpr int gemm_smem_bytes() {
-  return STAGES * (GEMM_BM * GEMM_BK * 4 + BN * GEMM_BK * 4) + SCRATCH + 1024 /*align*/ + 256 /*barriers*/;
+  return STAGES * (MT * GEMM_BM * GEMM_BK * 4 + BN * GEMM_BK * 4) + SCRATCH + 1024 /*align*/ + 256 /*barriers*/;
 }
 
 // Second counter block of the split-K workspace head (re-arm counters).
@@ -947,13 +958,18 @@ struct WorkDecode {
   }
 };
 
-template <int BN, int STAGES, class LA, class LB>
+template <int BN, int STAGES, class LA, class LB, int MT = 1>
 __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmArgs<LA, LB> args) {
-  constexpr int A_BYTES = GEMM_BM * GEMM_BK * 4;
+  constexpr int TM = MT * GEMM_BM;  // rows of a work item
+  constexpr int A_HALF = GEMM_BM * GEMM_BK * 4;
+  constexpr int A_BYTES = MT * A_HALF;
   constexpr int B_BYTES = BN * GEMM_BK * 4;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // two accumulator buffers, allocation rounded up to a power of two (BN = 192: 512)
-  constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  constexpr int ACC = MT * BN;  // accumulator columns of one work item
+  constexpr int TMEM_COLS = 2 * ACC <= 32 ? 32 : 2 * ACC <= 64 ? 64 : 2 * ACC <= 128 ? 128 : 2 * ACC <= 256 ? 256 : 512;
+  static_assert(2 * ACC <= 512, "TMEM");
+  static_assert(MT == 1 || (LA::kTMA && ScratchOf<LA>::value == 0), "256-row tiles: TMA operands only");
   constexpr int LAG = STAGES > 2 ? STAGES - 2 : 1;
   constexpr int MMA_WARP = GEMM_PRODUCERS / 32;
   constexpr int EPI_WARP0 = MMA_WARP + 1;
@@ -964,9 +980,10 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
 
   constexpr int SCRATCH = ScratchOf<LA>::value;
   static_assert(ScratchOf<LB>::value == 0, "scratch is an A-operand feature");
-  // TMA producer warps: 1 (A and B by one thread) or A parts + 1 for B
+  // TMA producer warps: the A operand's parts, then one warp for B (box issues of
+  // the two operands overlap)
   constexpr int NA_ISSUE = IssueWarpsOf<LA>::value;
-  constexpr int NPW = NA_ISSUE > 1 ? NA_ISSUE + 1 : 1;
+  constexpr int NPW = NA_ISSUE + 1;
   static_assert(NPW * 32 <= GEMM_PRODUCERS, "issue warps");
 
   extern __shared__ uint8_t smem_raw[];
@@ -983,7 +1000,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;  // warp-uniform role
   const int nkb_total = (args.K + GEMM_BK - 1) / GEMM_BK;
-  const WorkDecode wd{(args.M + GEMM_BM - 1) / GEMM_BM, (args.N + BN - 1) / BN,
+  const WorkDecode wd{(args.M + TM - 1) / TM, (args.N + BN - 1) / BN,
                       (nkb_total + args.kb_per_split - 1) / (args.kb_per_split > 0 ? args.kb_per_split : 1)};
   const int nwork = wd.mt * wd.nt * (wd.splits > 0 ? wd.splits : 1);
   // work items of this CTA: strided (neighbouring CTAs share operand tiles in
@@ -1042,7 +1059,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
           int mi, ni, si, kb0, nkb;
           wd.get(work_of(w), mi, ni, si);
           kb_range(si, kb0, nkb);
-          const int m0 = mi * GEMM_BM, n0 = ni * BN;
+          const int m0 = mi * TM, n0 = ni * BN;
           for (int j = 0; j < nkb; ++j, ++it) {
             const int s = it % STAGES;
             const int round = it / STAGES;
@@ -1056,10 +1073,10 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
               if (q != s || warp != 0) continue;
               // (a tag names the row0 whose constant atoms the stage holds; a tile
               // without constant atoms lets TMA overwrite them, clearing the tag)
-              if (!args.a.template needs_prefill<GEMM_BM>(m0)) {
+              if (!args.a.template needs_prefill<TM>(m0)) {
                 tagA[q] = -1;
               } else if (tagA[q] != m0) {
-                args.a.template prefill<GEMM_BM>(sa, m0, lane, 32);
+                args.a.template prefill<TM>(sa, m0, lane, 32);
                 tagA[q] = m0;
                 wrote = true;
               }
@@ -1078,14 +1095,13 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
             if (lane == 0) {
               const uint32_t full = bar_base + 8 * s;
               const int k0 = (kb0 + j) * GEMM_BK;
-              if constexpr (NPW == 1) {
-                args.a.template issue<GEMM_BM>(sa, m0, k0, full);
-                args.b.template issue<BN>(sa + A_BYTES, n0, k0, full);
-              } else {
-                if (warp < NA_ISSUE)
-                  args.a.template issue_part<GEMM_BM>(sa, m0, k0, full, warp);
+              if (warp < NA_ISSUE) {
+                if constexpr (NA_ISSUE == 1)
+                  args.a.template issue<TM>(sa, m0, k0, full);
                 else
-                  args.b.template issue<BN>(sa + A_BYTES, n0, k0, full);
+                  args.a.template issue_part<TM>(sa, m0, k0, full, warp);
+              } else {
+                args.b.template issue<BN>(sa + A_BYTES, n0, k0, full);
               }
               mbar_arrive(full);  // after this warp's expect_tx (the phase needs all NPW arrivals)
               if (warp == 0) SG_TRACE(1, it);
@@ -1155,7 +1171,7 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
       const int use = local >> 1;  // how many times buffer b was used before
       if (use > 0) mbar_wait(tempty_bar + 8 * b, (use - 1) & 1);
       tc_fence_after();
-      const uint32_t acc = tmem + b * BN;
+      const uint32_t acc = tmem + b * ACC;
       for (int j = 0; j < nkb; ++j, ++it) {
         const int s = it % STAGES;
 #ifdef SG_MMA_BACKOFF
@@ -1172,9 +1188,12 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
           const uint32_t sa = sbase + s * STAGE_BYTES;
 #pragma unroll
           for (int kk = 0; kk < GEMM_BK / 8; ++kk) {
-            uint64_t ad = tile_desc<GEMM_BM, LA::kMN>(sa, kk);
-            uint64_t bd = tile_desc<BN, LB::kMN>(sa + A_BYTES, kk);  // kMN also names the smem layout
-            mma_tf32_warp(acc, ad, bd, idesc, (j | kk) ? 1u : 0u);
+            const uint64_t bd = tile_desc<BN, LB::kMN>(sa + A_BYTES, kk);  // kMN also names the smem layout
+#pragma unroll
+            for (int h = 0; h < MT; ++h) {  // 128-row halves of the A stage, one accumulator each
+              const uint64_t ad = tile_desc<GEMM_BM, LA::kMN>(sa + h * A_HALF, kk);
+              mma_tf32_warp(acc + h * BN, ad, bd, idesc, (j | kk) ? 1u : 0u);
+            }
           }
           mma_commit_warp(bar_base + 8 * (STAGES + s));
           if (lane == 0) SG_TRACE(3, it);
@@ -1187,8 +1206,12 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
   } else {
     // ---------------------------------- epilogue ----------------------------------
     const int lg = warp & 3;  // TMEM lane group this warp may access
-    constexpr int HALF = BN / 2;
-    const int cbeg = ((warp - EPI_WARP0) >> 2) * HALF;
+    // MT = 1: the two warp quads take the column halves; MT = 2: quad g takes
+    // all columns of the 128-row half g
+    constexpr int HALF = MT == 1 ? BN / 2 : BN;
+    const int quad = (warp - EPI_WARP0) >> 2;
+    const int cbeg = MT == 1 ? quad * HALF : 0;
+    const int rhalf = MT == 1 ? 0 : quad;
     const EpiArgs& e = args.epi;
     const bool plain_vec = !e.trans && e.cb >= args.N && (e.ld & 3) == 0 && !e.bias_on_m;
     int local = 0;
@@ -1205,9 +1228,9 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
 #endif
       if (warp == EPI_WARP0 && lane == 0) SG_TRACE(4, local);
       tc_fence_after();
-      const int m0 = mi * GEMM_BM, n0 = ni * BN;
-      const int row = m0 + lg * 32 + lane;
-      const uint32_t tb = tmem + b * BN + ((uint32_t)(lg * 32) << 16);
+      const int m0 = mi * TM, n0 = ni * BN;
+      const int row = m0 + rhalf * GEMM_BM + lg * 32 + lane;
+      const uint32_t tb = tmem + b * ACC + rhalf * BN + ((uint32_t)(lg * 32) << 16);
 #pragma unroll 1
       for (int c0 = cbeg; c0 < cbeg + HALF; c0 += 16) {
         if (n0 + c0 >= args.N) break;
@@ -1253,8 +1276,8 @@ __global__ void __launch_bounds__(GEMM_ALL_THREADS, 1) gemm_tc_kernel(const __gr
         }
         epi_bar_sync();
         __threadfence();
-        const int r_b = m0 + si * GEMM_BM / S;
-        const int r_e = min(m0 + (si + 1) * GEMM_BM / S, args.M);
+        const int r_b = m0 + si * TM / S;
+        const int r_e = min(m0 + (si + 1) * TM / S, args.M);
         constexpr int C4 = BN / 4;
         const int et = (warp - EPI_WARP0) * 32 + lane;
         for (int idx = et; idx < (r_e - r_b) * C4; idx += GEMM_EPI_WARPS * 32) {

@@ -109,6 +109,25 @@ cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* W, floa
 cudaError_t conv_wgrad(const ConvShape& s, const float* x, const float* dy, float* dW, float* db, Workspace ws,
                        cudaStream_t st);
 
+// ---- strided convolution by space-to-depth (conv_s2d.cu) ----
+// A stride-st convolution equals a stride-1, unpadded one with ceil(R/st) x
+// ceil(S/st) taps over the st x st space-to-depth image (st*st*C channels).
+bool conv_s2d_ok(const ConvShape& s);
+ConvShape conv_s2d_shape(const ConvShape& s);
+size_t conv_s2d_x_floats(const ConvShape& s);
+size_t conv_s2d_w_floats(const ConvShape& s);
+cudaError_t conv_s2d_input(const ConvShape& s, const float* x, float* xs, cudaStream_t st);
+// input layer: channel padding cin -> 4 into y and the space-to-depth image xs of
+// the first convolution (shape s, C = 4) in one pass; xs borders must be zero
+cudaError_t pad_channels_s2d(const float* x, int cin, float* y, float* xs, const ConvShape& s, cudaStream_t st,
+                             int rn);
+// Wt: scratch for the rearranged filter (conv_s2d_w_floats)
+cudaError_t conv_fwd_s2d(const ConvShape& s, const float* xs, const float* W, float* Wt, const float* b, float* y,
+                         int flags, Workspace ws, cudaStream_t st);
+// dWt: scratch for the space-to-depth filter gradient (conv_s2d_w_floats)
+cudaError_t conv_wgrad_s2d(const ConvShape& s, const float* xs, const float* dy, float* dWt, float* dW, float* db,
+                           Workspace ws, cudaStream_t st);
+
 // ---- inner product:  y = x W + b ; W [d_v][d_h] ----
 cudaError_t ip_fwd(View2D x, const float* W, int dv, int dh, const float* b, View2D y, int flags, Workspace ws,
                    cudaStream_t st);

@@ -58,6 +58,7 @@ bool splitk_fixup() {
 
 struct Plan {
   int bn, mt, nt, splits, kb_per_split;
+  int mt2 = 0;  // 256-row work items (mt counts 128-row tiles; see tile256())
 };
 
 inline long long pad4(int n) { return (n + 3) & ~3; }
@@ -170,19 +171,27 @@ __global__ void __launch_bounds__(1024) splitk_reduce_kernel(const float* __rest
     if (n + i < N) reduce_store(e, m, n + i, N, r[i]);
 }
 
-template <int BN, class LA, class LB>
+template <int BN, class LA, class LB, int MT = 1>
 cudaError_t launch_bn(const GemmArgs<LA, LB>& args, const Plan& p, cudaStream_t st) {
-  constexpr int STAGES = gemm_stages<BN, ScratchOf<LA>::value>();
-  constexpr int SMEM = gemm_smem_bytes<BN, STAGES, ScratchOf<LA>::value>();
-  auto kern = gemm_tc_kernel<BN, STAGES, LA, LB>;
+  constexpr int STAGES = gemm_stages<BN, ScratchOf<LA>::value, MT>();
+  constexpr int SMEM = gemm_smem_bytes<BN, STAGES, ScratchOf<LA>::value, MT>();
+  auto kern = gemm_tc_kernel<BN, STAGES, LA, LB, MT>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int nwork = p.mt * p.nt * p.splits;
+  const int nwork = (MT == 1 ? p.mt : (p.mt + 1) / 2) * p.nt * p.splits;
   return launch_k(kern, std::min(nwork, kNumSMs), GEMM_ALL_THREADS, SMEM, st, args);
+}
+
+// 256-row work items (two accumulators sharing each B stage) for narrow N:
+// TMA A operands whose box can be encoded 256 rows tall (TmaIm2col), no split-K,
+// and at least one full wave of 256-row items.
+inline bool tile256(const Plan& p) {
+  static const int on = getenv("SG_TILE256") ? atoi(getenv("SG_TILE256")) : 1;
+  return on && p.bn <= 64 && p.splits == 1 && ((p.mt + 1) / 2) * p.nt >= kNumSMs;
 }
 
 template <class LA, class LB>
@@ -205,6 +214,16 @@ cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int
     args.epi.ws = nullptr;
   }
   cudaError_t e;
+  if constexpr (LA::kTMA && ScratchOf<LA>::value == 0) {
+    if (p.mt2) {
+      switch (p.bn) {
+        case 32: return launch_bn<32, LA, LB, 2>(args, p, st);
+        case 64: return launch_bn<64, LA, LB, 2>(args, p, st);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+  }
+  if (p.mt2) return cudaErrorInvalidValue;
   switch (p.bn) {
     case 32: e = launch_bn<32>(args, p, st); break;
     case 64: e = launch_bn<64>(args, p, st); break;
@@ -221,7 +240,8 @@ cudaError_t run_gemm_planned(const LA& a, const LB& b, const Plan& p, int M, int
 
 template <class LA, class LB>
 cudaError_t run_gemm(const LA& a, const LB& b, int M, int N, int K, EpiArgs epi, Workspace ws, cudaStream_t st) {
-  return run_gemm_planned(a, b, plan_gemm(M, N, K, ws.floats), M, N, K, epi, ws, st);
+  // 192-wide tiles only for TMA operands (the cp.async loaders' thread maps assume power-of-two widths)
+  return run_gemm_planned(a, b, plan_gemm(M, N, K, ws.floats, LA::kTMA), M, N, K, epi, ws, st);
 }
 
 // TMA operands: the tensor maps' boxes depend on the tile chosen by the plan.
@@ -601,8 +621,10 @@ cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const f
   if (tma_on(0) && s.C % 32 == 0 && aligned16p(x)) {
     bool ok = true;
     TmaIm2col a{};
-    a.map = enc_im2col(x, s.N, s.H, s.W, s.C, -s.pad, -s.pad, s.pad - (s.S - 1), s.pad - (s.R - 1), 32, GEMM_BM,
-                       s.st, CU_TENSOR_MAP_SWIZZLE_128B, &ok);
+    Plan p = plan_gemm(M, N, K, ws.floats);
+    p.mt2 = tile256(p);
+    a.map = enc_im2col(x, s.N, s.H, s.W, s.C, -s.pad, -s.pad, s.pad - (s.S - 1), s.pad - (s.R - 1), 32,
+                       GEMM_BM * (p.mt2 ? 2 : 1), s.st, CU_TENSOR_MAP_SWIZZLE_128B, &ok);
     a.C = s.C;
     a.R = s.R;
     a.S = s.S;
@@ -615,7 +637,6 @@ cudaError_t conv_fwd(const ConvShape& s, const float* x, const float* W, const f
     a.fS = make_fastdiv(s.S);
     a.fHW = make_fastdiv(s.Ho * s.Wo);
     a.fW = make_fastdiv(s.Wo);
-    const Plan p = plan_gemm(M, N, K, ws.floats);
     TmaK bw = tma_k(vplain(W, s.Co, K, K), p.bn, &ok);
     if (ok) return run_gemm_planned(a, bw, p, M, N, K, e, ws, st);
   }
@@ -639,8 +660,10 @@ cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* W, floa
     bool ok = true;
     const int lo = s.pad - (s.R - 1);
     TmaIm2col a{};
-    a.map = enc_im2col(dy, s.N, s.Ho, s.Wo, s.Co, lo, lo, lo + (s.W - s.Wo), lo + (s.H - s.Ho), 32, GEMM_BM, 1,
-                       CU_TENSOR_MAP_SWIZZLE_128B, &ok);
+    Plan p = plan_gemm(M, N, K, ws.floats);
+    p.mt2 = tile256(p);
+    a.map = enc_im2col(dy, s.N, s.Ho, s.Wo, s.Co, lo, lo, lo + (s.W - s.Wo), lo + (s.H - s.Ho), 32,
+                       GEMM_BM * (p.mt2 ? 2 : 1), 1, CU_TENSOR_MAP_SWIZZLE_128B, &ok);
     a.C = s.Co;
     a.R = s.R;
     a.S = s.S;
@@ -654,14 +677,16 @@ cudaError_t conv_dgrad(const ConvShape& s, const float* dy, const float* W, floa
     a.fHW = make_fastdiv(s.H * s.W);
     a.fW = make_fastdiv(s.W);
     TmaDgradB bw{};
-    cuuint64_t dims[3] = {(cuuint64_t)s.C, (cuuint64_t)(s.R * s.S), (cuuint64_t)s.Co};
-    cuuint64_t strides[2] = {(cuuint64_t)s.C * 4, (cuuint64_t)s.R * s.S * s.C * 4};
-    cuuint32_t box[3] = {32, 1, 32};
-    bw.map = enc_tiled(W, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, &ok);
+    // whole B tile in one 4-D box (atoms of 32 channels consecutive)
+    cuuint64_t dims[4] = {32, (cuuint64_t)(s.R * s.S), (cuuint64_t)s.Co, (cuuint64_t)(s.C / 32)};
+    cuuint64_t strides[3] = {(cuuint64_t)s.C * 4, (cuuint64_t)s.R * s.S * s.C * 4, 128};
+    cuuint32_t box[4] = {32, 1, 32, (cuuint32_t)(p.bn / 32)};
+    bw.map = enc_tiled(W, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, &ok);
+    bw.atoms4 = 1;
     bw.C = s.C;
     bw.Co = s.Co;
     bw.fCo = make_fastdiv(s.Co);
-    if (ok) return run_gemm(a, bw, M, N, K, e, ws, st);
+    if (ok) return run_gemm_planned(a, bw, p, M, N, K, e, ws, st);
   }
   LdConvDgradA a{dy, geom(s)};
   LdConvDgradB bw{W, geom(s)};

@@ -54,6 +54,10 @@ struct sg_net {
   sg_plan plan;
   cudaStream_t cs = nullptr, ps = nullptr;
   std::vector<float*> data, grad, scale;
+  // strided first-layer conv by space-to-depth (conv_s2d.cu): image, filter, filter gradient
+  std::vector<float*> s2d_x, s2d_w, s2d_dw;
+  bool s2d_wgrad = true;
+  int s2d_of_input = -1;  // conv whose space-to-depth image the input layer writes (or -1)
   std::vector<uint8_t*> mask;
   // per store: working copy of the weights (full; what the GEMMs read: TF32-RN
   // weights, fp32 biases), gradients (full), fp32 master weights and history
@@ -222,14 +226,24 @@ sg_status forward_impl(sg_net* n, int i) {
   switch (L.kind) {
     case SG_INPUT:
       SG_CHECK(n->x_src, SG_ERR_SEQUENCE, "sequence error: no input set (sg_net_set_input)");
-      if (L.image)
+      if (L.image && n->s2d_of_input >= 0) {
+        const int c = n->s2d_of_input;
+        SG_LCH(pad_channels_s2d(n->x_src, L.c_real, n->data[i], n->s2d_x[c], conv_shape(P.layers[c], L), st,
+                                L.rn_data));
+      } else if (L.image) {
         SG_LCH(pad_channels(n->x_src, n->data[i], L.rows * L.h * L.w, L.c_real, L.c, st, L.rn_data));
+      }
       else
         SG_LCH(copy2d(n->x_src, L.feat, n->data[i], L.ld, (int)L.rows, (int)L.feat, st, L.rn_data));
       if (n->x_exact) SG_LCH(copy2d(n->x_src, L.feat, n->x_exact, L.ld, (int)L.rows, (int)L.feat, st, 0));
       break;
     case SG_CONV:
-      SG_LCH(conv_fwd(conv_shape(L, *S), n->data[L.src], W, b, n->data[i], epi_flags(n, i), n->ws, st));
+      if (n->s2d_x[i]) {  // stride-st first layer as a stride-1 conv of the space-to-depth image
+        if (n->s2d_of_input != i) SG_LCH(conv_s2d_input(conv_shape(L, *S), n->data[L.src], n->s2d_x[i], st));
+        SG_LCH(conv_fwd_s2d(conv_shape(L, *S), n->s2d_x[i], W, n->s2d_w[i], b, n->data[i], epi_flags(n, i), n->ws, st));
+      } else {
+        SG_LCH(conv_fwd(conv_shape(L, *S), n->data[L.src], W, b, n->data[i], epi_flags(n, i), n->ws, st));
+      }
       break;
     case SG_POOL_MAX:
     case SG_POOL_AVG: {
@@ -323,6 +337,8 @@ sg_status backward(sg_net* n, int i) {
         const int c = n->pool_into[i];
         SG_LCH(conv_img4_pool_bwd(conv_shape(L, S), pool_shape(P.layers[c], L), n->data[L.src], n->grad[c],
                                   n->mask[c], n->grad[i], L.rn_grad, dW, db, wws, wst));
+      } else if (n->s2d_x[i] && n->s2d_wgrad) {
+        SG_LCH(conv_wgrad_s2d(conv_shape(L, S), n->s2d_x[i], n->grad[i], n->s2d_dw[i], dW, db, wws, wst));
       } else {
         SG_LCH(conv_wgrad(conv_shape(L, S), n->data[L.src], n->grad[i], dW, db, wws, wst));
       }
@@ -749,6 +765,9 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
   n->data.assign(nl, nullptr);
   n->grad.assign(nl, nullptr);
   n->scale.assign(nl, nullptr);
+  n->s2d_x.assign(nl, nullptr);
+  n->s2d_w.assign(nl, nullptr);
+  n->s2d_dw.assign(nl, nullptr);
   n->mask.assign(nl, nullptr);
   n->ev_grad.resize(nl);
   n->ev_upd.resize(nl);
@@ -781,6 +800,22 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
       need(colsum_ws_floats((int)(L.rows * L.h * L.w), L.c));
       need(conv_img_wgrad_ws_floats(conv_shape(L, S)));
       need(conv_img4_wgrad_ws_floats(conv_shape(L, S)));
+      const ConvShape cs = conv_shape(L, S);
+      if (conv_s2d_ok(cs) && !conv_img_fwd_ok(cs)) {
+        const ConvShape t = conv_s2d_shape(cs);
+        const int Kt = t.R * t.S * t.C;
+        SG_TRY(dalloc_t(n, conv_s2d_x_floats(cs), &n->s2d_x[i]));
+        SG_TRY(dalloc_t(n, conv_s2d_w_floats(cs), &n->s2d_w[i]));
+        SG_TRY(dalloc_t(n, conv_s2d_w_floats(cs), &n->s2d_dw[i]));
+        // the input layer writes the image directly (channel padding to 4 and one consumer)
+        if (S.kind == SG_INPUT && S.image && S.c == 4 && S.c_real <= 4 && n->s2d_of_input < 0) {
+          int consumers = 0;
+          for (int j = 0; j < nl; ++j) consumers += P.layers[j].src == L.src;
+          if (consumers == 1) n->s2d_of_input = i;
+        }
+        need(gemm_ws_floats((int)(L.rows * L.h * L.w), L.c, Kt));
+        need(gemm_ws_floats(Kt + 1, L.c, (int)(L.rows * L.h * L.w)));
+      }
     }
     if (L.kind == SG_INNER_PRODUCT) {
       need(gemm_ws_floats((int)L.rows, (int)L.nout, (int)L.kin));
@@ -793,6 +828,10 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
   // input layer are never formed.  The loss layer writes dz into its source's grad.
   SG_TRY(dalloc_t(n, ws, &n->ws.ptr));
   n->ws.floats = ws;
+  {
+    const char* env = getenv("SG_S2D_WGRAD");
+    n->s2d_wgrad = env ? atoi(env) != 0 : false;  // measured slower (TMA-box bound, 291 -> 421 us)
+  }
   {
     const char* env = getenv("SG_WGRAD_SIDE");
     n->wgrad_side = env ? atoi(env) != 0 : true;

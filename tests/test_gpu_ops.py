@@ -56,6 +56,7 @@ CONV = [  # N, H, W, C, Co, R, stride, pad
     (2, 13, 13, 192, 384, 3, 1, 1),   # AlexNet conv3
     (27, 27, 27, 64, 192, 5, 1, 2),   # 192-wide tiles (>= 148 M tiles): im2col forward, TMA weight gradient
     (26, 27, 27, 192, 32, 3, 1, 1),   # 192-wide tiles: TMA data gradient (N = C = 192)
+    (52, 27, 27, 64, 64, 3, 1, 1),    # 256-row work items (N = 64, >= 148 of them): forward and data gradient
     (3, 9, 7, 8, 12, 3, 2, 1),        # ragged, strided dgrad
 ]
 

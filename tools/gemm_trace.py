@@ -1,6 +1,6 @@
 """CTA-0 timeline of one GEMM-engine launch (needs the trace variant:
 python -m paper_1603_07846_b200.build --variant trace -D SG_GEMM_TRACE; run with
-SG_LIB=build/trace/libsinga_b200.so).  Usage: gemm_trace.py conv N H C Co R st p [fwd|wgrad]
+SG_LIB=build/trace/libsinga_b200.so).  Usage: gemm_trace.py conv N H C Co R st p [fwd|wgrad|dgrad]
                                       or gemm_trace.py gemm M N K"""
 import ctypes as C
 import os
@@ -49,6 +49,10 @@ def main():
     dW, db = torch.empty_like(Wt), torch.empty_like(b)
     if which == "fwd":
         run(lambda: L.sg_op_conv_forward(C.byref(d), x.data_ptr(), Wt.data_ptr(), b.data_ptr(), y.data_ptr(), None))
+    elif which == "dgrad":  # the data gradient is the last GEMM launched
+        dx = torch.empty_like(x)
+        run(lambda: L.sg_op_conv_backward(C.byref(d), x.data_ptr(), Wt.data_ptr(), dy.data_ptr(), dx.data_ptr(),
+                                          dW.data_ptr(), db.data_ptr(), None))
     else:
         run(lambda: L.sg_op_conv_backward(C.byref(d), x.data_ptr(), Wt.data_ptr(), dy.data_ptr(), None, dW.data_ptr(),
                                           db.data_ptr(), None))

@@ -589,10 +589,14 @@ struct ImgWgradArgs {
   float* part;          // [CTA][Co*Kg + Co]
   int C, Co, R, S, pad, Wp, Ho, Wo;
   int Hrows_i, Hrows_d, rows_i, rows_d, ksteps;
-  int nimg, spc;  // samples, samples per CTA (accumulated in TMEM)
+  int nimg, spc;  // staged units (samples, or bands of samples), units per CTA (accumulated in TMEM)
   int split, kpc;  // CTAs per sample group (strong scaling), K steps per CTA
   int ntile;
   int t_off[kMaxWTiles], t_delta[kMaxWTiles], t_tap[kMaxWTiles][4];
+  int t_cb[kMaxWTiles];  // 32-channel block of the tile's atoms (t_off includes its plane)
+  int cpl;               // channel planes C / 32 of the staged image
+  int nb, BR;            // bands per sample (1: whole image) and output rows per band
+  int dyrows;            // dy rows per TMA box (Hrows_d; BR for bands: the k-lines past BR*Wp are zeroed once)
 };
 
 template <int NB>
@@ -602,7 +606,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t dy_plane = a.rows_d * 128;
-  const uint32_t buf_bytes = a.rows_i * 128 + NA * dy_plane;  // one sample: image, then dy atoms
+  const uint32_t buf_bytes = a.cpl * a.rows_i * 128 + NA * dy_plane;  // one unit: image planes, then dy atoms
   const uint32_t bars = base + 2 * buf_bytes;                // full[2], empty[2], done
   const uint32_t done_bar = bars + 32, slot = done_bar + 8;
   uint32_t* slot_ptr = reinterpret_cast<uint32_t*>(smem_raw + (slot - smem_u32(smem_raw)));
@@ -613,6 +617,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
   const int n0 = (blockIdx.x / a.split) * a.spc, n1 = min(a.nimg, n0 + a.spc), ns = n1 - n0;
   const int k0 = part * a.kpc, k1 = min(a.ksteps, k0 + a.kpc);
   const int Kg = a.R * a.S * a.C, per = a.Co * Kg + a.Co;
+  // unit q = band q % nb of sample q / nb: output rows [b*BR, b*BR + BR)
 
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
@@ -624,19 +629,32 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
     prefetch_tmap(&a.img_map);
     prefetch_tmap(&a.dy_map);
   }
+  {
+    // band units: the dy k-lines [dyrows*Wp, ksteps*8) belong to no box (the next
+    // band's rows must not enter): zero them once in both buffers
+    const int z0 = a.dyrows * a.Wp, z1 = a.ksteps * 8;
+    for (int i = tid; i < 2 * NA * (z1 - z0) * 8; i += kImgThreads) {
+      const int c16 = i & 7, r = i >> 3, line = z0 + r % (z1 - z0), pl = r / (z1 - z0);
+      const uint32_t addr = base + (pl / NA) * buf_bytes + a.cpl * a.rows_i * 128 + (pl % NA) * dy_plane + line * 128 +
+                            c16 * 16;
+      asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "f"(0.f) : "memory");
+    }
+    fence_proxy_async_smem();
+  }
   if (warp == 4) tmem_alloc<TCOLS>(slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot_ptr;
   pdl_entry();
-  const uint32_t tx = (uint32_t)(a.Hrows_i * a.Wp + NA * a.Hrows_d * a.Wp) * 128;
-  auto stage = [&](int k) {  // TMA staging of sample n0 + k into buffer k & 1
-    const int b = k & 1;
-    const uint32_t img = base + b * buf_bytes, dyb = img + a.rows_i * 128;
+  const uint32_t tx = (uint32_t)(a.cpl * a.Hrows_i * a.Wp + NA * a.dyrows * a.Wp) * 128;
+  auto stage = [&](int k) {  // TMA staging of unit n0 + k into buffer k & 1
+    const int b = k & 1, q = n0 + k, sn = q / a.nb, y0 = (q % a.nb) * a.BR;
+    const uint32_t img = base + b * buf_bytes, dyb = img + a.cpl * a.rows_i * 128;
     mbar_arrive_expect_tx(bars + 8 * b, tx);
-    tma_load_4d(img, &a.img_map, 0, -a.pad, -a.pad, n0 + k, bars + 8 * b);
-    for (int at = 0; at < NA; ++at) tma_load_4d(dyb + at * dy_plane, &a.dy_map, at * 32, 0, 0, n0 + k, bars + 8 * b);
+    for (int cb = 0; cb < a.cpl; ++cb)
+      tma_load_4d(img + cb * a.rows_i * 128, &a.img_map, cb * 32, -a.pad, y0 - a.pad, sn, bars + 8 * b);
+    for (int at = 0; at < NA; ++at) tma_load_4d(dyb + at * dy_plane, &a.dy_map, at * 32, 0, y0, sn, bars + 8 * b);
   };
   if (warp == 4) {
     {
@@ -646,7 +664,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
         const int b = k & 1;
         mbar_wait(bars + 8 * b, (k >> 1) & 1);
         tc_fence_after();
-        const uint32_t img = base + b * buf_bytes, dyb = img + a.rows_i * 128;
+        const uint32_t img = base + b * buf_bytes, dyb = img + a.cpl * a.rows_i * 128;
         const uint64_t bd0 = umma_desc_mn_sw128_32b(dyb, dy_plane, 512);
         const uint32_t b_lo0 = (uint32_t)bd0, b_hi = (uint32_t)(bd0 >> 32);
         for (int g = 0; g < a.ntile; ++g) {
@@ -662,26 +680,36 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
     }
     __syncwarp();
   } else {
+    // ---- TMA staging, double-buffered over the CTA's units; db = the sum of the
+    // staged dy tiles (thread per output channel, k-lines of this CTA's K range in
+    // order, units in order), read from shared memory before a buffer is restaged ----
     if (tid == 0) {
-      // ---- TMA staging, double-buffered over the CTA's samples ----
       stage(0);
       if (ns > 1) stage(1);
-      for (int k = 2; k < ns; ++k) {
-        mbar_wait(bars + 16 + 8 * (k & 1), ((k - 2) >> 1) & 1);
-        stage(k);
+    }
+    float sacc = 0.f;
+    const int kl0 = k0 * 8, kl1 = min(k1 * 8, a.dyrows * a.Wp);
+    for (int k = 0; k < ns; ++k) {
+      const int b = k & 1;
+      mbar_wait(bars + 8 * b, (k >> 1) & 1);
+      if (tid < a.Co) {
+        const uint32_t dyb = base + b * buf_bytes + a.cpl * a.rows_i * 128 + (tid >> 5) * dy_plane;
+        const uint32_t co = tid & 31;
+        for (int q = kl0; q < kl1; ++q) {
+          float v;
+          asm volatile("ld.shared.f32 %0, [%1];"
+                       : "=f"(v)
+                       : "r"(dyb + q * 128 + (((co >> 3) ^ ((uint32_t)q & 3)) << 5) + (co & 7) * 4));
+          sacc += v;
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // every dy read of buffer b done
+      if (tid == 0 && k + 2 < ns) {
+        mbar_wait(bars + 16 + 8 * b, (k >> 1) & 1);  // its MMAs done
+        stage(k + 2);
       }
     }
-    // db partial = sum over the CTA's samples of dy (SIMT, fixed order), while the MMAs run;
-    // a split sample's pixels are divided evenly among its CTAs
-    const int groups = 128 / a.Co;  // threads per channel (Co <= 128)
-    float sacc = 0.f;
-    if (tid < groups * a.Co) {
-      const int co = tid % a.Co, grp = tid / a.Co;
-      const float* dyn = a.dy + (size_t)n0 * a.Ho * a.Wo * a.Co;
-      const int np = ns * a.Ho * a.Wo, pc = (np + a.split - 1) / a.split;
-      const int pb = part * pc, pe = min(np, pb + pc);
-      for (int p = pb + grp; p < pe; p += groups) sacc += __ldg(dyn + (size_t)p * a.Co + co);
-    }
+    const int groups = 1;
     red[tid] = sacc;
     mbar_wait_sleep(done_bar, 0);
     tc_fence_after();
@@ -689,7 +717,7 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
     float* out = a.part + (size_t)blockIdx.x * per;
     for (int g = 0; g < a.ntile; ++g) {
       const int tap = a.t_tap[g][warp];
-      const int kg = tap * a.C + lane;
+      const int kg = tap * a.C + a.t_cb[g] * 32 + lane;
 #pragma unroll 1
       for (int c0 = 0; c0 < NB; c0 += 16) {
         float v[16];
@@ -741,64 +769,98 @@ __global__ void __launch_bounds__(512) conv_wgrad_sum_kernel(const float* __rest
 // leftover columns s of all rows in runs of 4 (stride Wp rows); at most
 // kMaxWTiles tiles, unused atoms marked -1.
 bool plan_wgrad(const ConvShape& s, ImgWgradArgs* a, size_t* smem) {
-  if (!img_conv_enabled() || s.st != 1 || s.C != 32 || (s.Co != 32 && s.Co != 64)) return false;
+  if (!img_conv_enabled() || s.st != 1 || (s.C != 32 && s.C != 64) || (s.Co != 32 && s.Co != 64)) return false;
   ImgWgradArgs g{};
   g.C = s.C, g.Co = s.Co, g.R = s.R, g.S = s.S, g.pad = s.pad;
   g.Wp = s.W + 2 * s.pad, g.Ho = s.Ho, g.Wo = s.Wo;
+  g.cpl = s.C / 32;
+  // tap tiles per 32-channel plane (t_off in k-lines of the plane; the plane
+  // offset is added once the plane height is known)
+  int off_in[kMaxWTiles], used[kMaxWTiles];
   g.ntile = 0;
-  auto add = [&](int off, int delta, const int* taps, int cnt) {
+  auto add = [&](int cb, int off, int delta, const int* taps, int cnt) {
     if (g.ntile >= kMaxWTiles) return false;
-    g.t_off[g.ntile] = off;
+    off_in[g.ntile] = off;
+    used[g.ntile] = cnt;
+    g.t_cb[g.ntile] = cb;
     g.t_delta[g.ntile] = delta;
     for (int k = 0; k < 4; ++k) g.t_tap[g.ntile][k] = k < cnt ? taps[k] : -1;
     ++g.ntile;
     return true;
   };
   const int full = s.S / 4;
-  for (int r = 0; r < s.R; ++r)
-    for (int b = 0; b < full; ++b) {
-      int taps[4];
-      for (int k = 0; k < 4; ++k) taps[k] = r * s.S + b * 4 + k;
-      if (!add(r * g.Wp + b * 4, 1, taps, 4)) return false;
-    }
-  for (int sc = full * 4; sc < s.S; ++sc)
-    for (int r0 = 0; r0 < s.R; r0 += 4) {
-      int taps[4], cnt = 0;
-      for (int k = 0; k < 4 && r0 + k < s.R; ++k) taps[cnt++] = (r0 + k) * s.S + sc;
-      if (!add(r0 * g.Wp + sc, g.Wp, taps, cnt)) return false;
-    }
-  const int K = g.Ho * g.Wp;
-  g.ksteps = (K + 7) / 8;
-  int need_rows = 0;
-  for (int t = 0; t < g.ntile; ++t) need_rows = std::max(need_rows, g.t_off[t] + 3 * g.t_delta[t] + g.ksteps * 8);
-  g.Hrows_i = (need_rows + g.Wp - 1) / g.Wp;
-  g.Hrows_d = (g.ksteps * 8 + g.Wp - 1) / g.Wp;
-  if (g.Hrows_i > 256 || g.Hrows_d > 256 || g.Wp > 256) return false;
-  g.rows_i = (g.Hrows_i * g.Wp + 7) / 8 * 8;
-  g.rows_d = (g.Hrows_d * g.Wp + 7) / 8 * 8;
+  for (int cb = 0; cb < g.cpl; ++cb) {
+    for (int r = 0; r < s.R; ++r)
+      for (int b = 0; b < full; ++b) {
+        int taps[4];
+        for (int k = 0; k < 4; ++k) taps[k] = r * s.S + b * 4 + k;
+        if (!add(cb, r * g.Wp + b * 4, 1, taps, 4)) return false;
+      }
+    for (int sc = full * 4; sc < s.S; ++sc)
+      for (int r0 = 0; r0 < s.R; r0 += 4) {
+        int taps[4], cnt = 0;
+        for (int k = 0; k < 4 && r0 + k < s.R; ++k) taps[cnt++] = (r0 + k) * s.S + sc;
+        if (!add(cb, r0 * g.Wp + sc, g.Wp, taps, cnt)) return false;
+      }
+  }
   if (g.ntile * s.Co > 512) return false;
-  // samples per CTA: enough MMAs per CTA to amortise the per-CTA partial
-  // (Co*Kg floats written and re-read by the reduction)
-  g.nimg = s.N;
-  // Samples per CTA (SG_WGRAD_SPC, default 1): accumulating several samples per
-  // CTA measured slower (CIFAR conv2: 26 -> 36 us at 2, 87 us at 3).  A sample's
-  // partial (Co*Kg floats, written and re-read by the reduction) must be
-  // amortised by its MMAs: below ~200 MMAs per sample the implicit GEMM wins
-  // (CIFAR conv3: 24 vs 20 us), so such shapes are declined.
-  static const int spc_env = getenv("SG_WGRAD_SPC") ? atoi(getenv("SG_WGRAD_SPC")) : 1;
-  g.spc = std::max(1, std::min(s.N, spc_env));
-  if (g.ntile * g.ksteps < 200) return false;
-  // strong scaling: spread a sample's K steps over several CTAs when the
-  // samples alone cannot fill the machine (partials summed by the reduction)
-  {
+  // staging unit: the whole sample, or (image too large for two buffers) a band
+  // of BR output rows with its R - 1 halo rows (TMA boxes at row offsets, zero
+  // fill past the image)
+  auto size_for = [&](int BR, size_t* sm) {
+    g.BR = BR;
+    g.nb = (g.Ho + BR - 1) / BR;
+    const int K = BR * g.Wp;
+    g.ksteps = (K + 7) / 8;
+    // image rows the used atoms read; an unused 4th atom of a 3-tap tile reads
+    // past them (discarded accumulator rows) but must stay inside the unit's buffer
+    int need_rows = 0;
+    for (int t = 0; t < g.ntile; ++t)
+      need_rows = std::max(need_rows, off_in[t] + (used[t] - 1) * g.t_delta[t] + g.ksteps * 8);
+    g.Hrows_i = (need_rows + g.Wp - 1) / g.Wp;
+    g.Hrows_d = (g.ksteps * 8 + g.Wp - 1) / g.Wp;
+    if (g.Hrows_i > 256 || g.Hrows_d > 256 || g.Wp > 256) return false;
+    g.rows_i = (g.Hrows_i * g.Wp + 7) / 8 * 8;
+    // a band's dy box is BR rows and the rest of its k-lines is zeroed: no halo rows
+    g.rows_d = BR < g.Ho ? (g.ksteps * 8 + 7) / 8 * 8 : (g.Hrows_d * g.Wp + 7) / 8 * 8;
+    const int unit_lines = g.cpl * g.rows_i + (s.Co / 32) * g.rows_d;
+    for (int t = 0; t < g.ntile; ++t)
+      if (off_in[t] + g.t_cb[t] * g.rows_i + 3 * g.t_delta[t] + g.ksteps * 8 > unit_lines) return false;
+    *sm = 1024 + 2 * ((size_t)g.cpl * g.rows_i * 128 + (size_t)(s.Co / 32) * g.rows_d * 128) + 64;
+    return *sm <= 227 * 1024;
+  };
+  if (!size_for(g.Ho, smem)) {
+    static const int band_env = getenv("SG_WGRAD_BANDS") ? atoi(getenv("SG_WGRAD_BANDS")) : 1;
+    if (!band_env) return false;
+    int BR = g.Ho - 1;
+    while (BR >= 1 && !size_for(BR, smem)) --BR;
+    if (BR < 1) return false;
+  }
+  for (int t = 0; t < g.ntile; ++t) g.t_off[t] = g.t_cb[t] * g.rows_i + off_in[t];
+  g.nimg = s.N * g.nb;
+  g.dyrows = g.nb == 1 ? g.Hrows_d : g.BR;
+  if (g.nb == 1) {
+    // Samples per CTA (SG_WGRAD_SPC, default 1): accumulating several samples per
+    // CTA measured slower (CIFAR conv2: 26 -> 36 us at 2, 87 us at 3).  A sample's
+    // partial (Co*Kg floats, written and re-read by the reduction) must be
+    // amortised by its MMAs: below ~200 MMAs per sample the implicit GEMM wins
+    // (CIFAR conv3: 24 vs 20 us), so such shapes are declined.
+    static const int spc_env = getenv("SG_WGRAD_SPC") ? atoi(getenv("SG_WGRAD_SPC")) : 1;
+    g.spc = std::max(1, std::min(s.N, spc_env));
+    if (g.ntile * g.ksteps < 200) return false;
+    // strong scaling: spread a sample's K steps over several CTAs when the
+    // samples alone cannot fill the machine (partials summed by the reduction)
     static const int maxs = getenv("SG_IMG_SPLIT") ? atoi(getenv("SG_IMG_SPLIT")) : 1 << 20;
     const int groups = (s.N + g.spc - 1) / g.spc;
     int sp = std::max(1, std::min({148 / std::max(groups, 1), maxs, g.ksteps / 8}));
     g.kpc = (g.ksteps + sp - 1) / sp;
     g.split = (g.ksteps + g.kpc - 1) / g.kpc;
+  } else {
+    // bands: one wave of CTAs, each accumulating a contiguous run of bands in TMEM
+    g.spc = (g.nimg + 147) / 148;
+    g.kpc = g.ksteps;
+    g.split = 1;
   }
-  *smem = 1024 + 2 * ((size_t)g.rows_i * 128 + (size_t)(s.Co / 32) * g.rows_d * 128) + 64;
-  if (*smem > 227 * 1024) return false;
   *a = g;
   return true;
 }
@@ -816,7 +878,7 @@ size_t conv_img_wgrad_ws_floats(const ConvShape& s) {
   ImgWgradArgs a;
   size_t smem;
   if (!plan_wgrad(s, &a, &smem)) return 0;
-  const size_t ctas = (size_t)((s.N + a.spc - 1) / a.spc) * a.split;
+  const size_t ctas = (size_t)((a.nimg + a.spc - 1) / a.spc) * a.split;
   return 1024 + ctas * (size_t)(s.Co * s.R * s.S * s.C + s.Co);
 }
 
@@ -832,14 +894,14 @@ cudaError_t conv_img_wgrad(const ConvShape& s, const float* x, const float* dy, 
   const cuuint32_t xb[4] = {32, (cuuint32_t)a.Wp, (cuuint32_t)a.Hrows_i, 1};
   const cuuint64_t dd[4] = {(cuuint64_t)s.Co, (cuuint64_t)s.Wo, (cuuint64_t)s.Ho, (cuuint64_t)s.N};
   const cuuint64_t ds[3] = {(cuuint64_t)s.Co * 4, (cuuint64_t)s.Wo * s.Co * 4, (cuuint64_t)s.Ho * s.Wo * s.Co * 4};
-  const cuuint32_t db4[4] = {32, (cuuint32_t)a.Wp, (cuuint32_t)a.Hrows_d, 1};
+  const cuuint32_t db4[4] = {32, (cuuint32_t)a.Wp, (cuuint32_t)a.dyrows, 1};
   if (!encode_tiled_f32(&a.img_map, x, 4, xd, xs, xb, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
       !encode_tiled_f32(&a.dy_map, dy, 4, dd, ds, db4, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
     return cudaErrorInvalidValue;
   auto k = s.Co == 32 ? conv_img_wgrad_kernel<32> : conv_img_wgrad_kernel<64>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int ctas = ((s.N + a.spc - 1) / a.spc) * a.split;
+  const int ctas = ((a.nimg + a.spc - 1) / a.spc) * a.split;
   e = launch_k(k, ctas, kImgThreads, smem, st, a);
   if (e != cudaSuccess) return e;
   const int nw = s.Co * s.R * s.S * s.C, per = nw + s.Co;

@@ -815,6 +815,7 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
         }
         need(gemm_ws_floats((int)(L.rows * L.h * L.w), L.c, Kt));
         need(gemm_ws_floats(Kt + 1, L.c, (int)(L.rows * L.h * L.w)));
+        need(conv_img_wgrad_ws_floats(t));
       }
     }
     if (L.kind == SG_INNER_PRODUCT) {
@@ -830,7 +831,7 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
   n->ws.floats = ws;
   {
     const char* env = getenv("SG_S2D_WGRAD");
-    n->s2d_wgrad = env ? atoi(env) != 0 : false;  // measured slower (TMA-box bound, 291 -> 421 us)
+    n->s2d_wgrad = env ? atoi(env) != 0 : true;
   }
   {
     const char* env = getenv("SG_WGRAD_SIDE");

@@ -63,4 +63,13 @@ __device__ __forceinline__ void lrn_apply(const LrnShape& s, int C4, float4 v, i
 }
 
 
+// LRN backward of one channel (reading A6; a12): t = g*y/s of the window's
+// channels, o = g*s^-beta - coef*x*sum(t), coef = 2*alpha*beta/n.  Explicit
+// round-to-nearest intrinsics (no FMA contraction), so the separate kernel and
+// the convolution epilogue that fuses it produce identical bits.
+__device__ __forceinline__ float lrn_bwd_t(float g, float y, float s) { return __fdiv_rn(__fmul_rn(g, y), s); }
+__device__ __forceinline__ float lrn_bwd_out(float g, float s, float x, float acc, float beta, float coef) {
+  return __fsub_rn(__fmul_rn(g, pow_neg(s, beta)), __fmul_rn(__fmul_rn(coef, x), acc));
+}
+
 }  // namespace sg

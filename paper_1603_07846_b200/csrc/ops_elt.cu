@@ -407,8 +407,9 @@ __global__ void lrn_bwd_kernel(LrnK K, const float* __restrict__ x, const float*
     const float4 sv = in ? __ldg(reinterpret_cast<const float4*>(scale) + i) : make_float4(1.f, 1.f, 1.f, 1.f);
     const float4 xv = in ? __ldg(reinterpret_cast<const float4*>(x) + i) : z;
     float e[12];
-    lrn_neighbours(make_float4(g.x * yv.x / sv.x, g.y * yv.y / sv.y, g.z * yv.z / sv.z, g.w * yv.w / sv.w), c4, K.C4,
-                   e);
+    lrn_neighbours(make_float4(lrn_bwd_t(g.x, yv.x, sv.x), lrn_bwd_t(g.y, yv.y, sv.y), lrn_bwd_t(g.z, yv.z, sv.z),
+                               lrn_bwd_t(g.w, yv.w, sv.w)),
+                   c4, K.C4, e);
     const float gs[4] = {g.x, g.y, g.z, g.w}, ss[4] = {sv.x, sv.y, sv.z, sv.w}, xs[4] = {xv.x, xv.y, xv.z, xv.w};
     float o[4];
 #pragma unroll
@@ -416,9 +417,9 @@ __global__ void lrn_bwd_kernel(LrnK K, const float* __restrict__ x, const float*
       float acc = 0.f;
       // ascending d over the window (half <= 4): compile-time indices keep e[] in registers
 #pragma unroll
-    for (int d = -4; d <= 4; ++d)
-      if (d >= -half && d <= half) acc += e[4 + j + d];
-      o[j] = gs[j] * pow_neg(ss[j], s.beta) - coef * xs[j] * acc;
+      for (int d = -4; d <= 4; ++d)
+        if (d >= -half && d <= half) acc = __fadd_rn(acc, e[4 + j + d]);
+      o[j] = lrn_bwd_out(gs[j], ss[j], xs[j], acc, s.beta, coef);
     }
     if (in) {
       const float4 d = make_float4(o[0], o[1], o[2], o[3]);

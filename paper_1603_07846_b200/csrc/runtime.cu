@@ -78,7 +78,14 @@ struct sg_net {
   // their kernels use a workspace of their own
   bool wgrad_side = true;
   sg::Workspace ws2;
-  std::vector<cudaEvent_t> ev_grad, ev_upd, ev_dy;
+  std::vector<cudaEvent_t> ev_grad, ev_upd, ev_dy, ev_wg;
+  // Updates (and their collectives / peer exchange) run on a stream of their own
+  // when the weight gradients use the parameter stream, so an exchange waiting
+  // for the peers never holds up the next layer's weight gradient
+  cudaStream_t us = nullptr;
+  cudaEvent_t ev_join_u = nullptr;
+  std::vector<char> wg_on_ps;      // layer i's weight gradient of this step ran on the parameter stream
+  bool ps_used = false, us_used = false;  // streams forked in this step (joined at its end)
   std::vector<char> upd_pending, fwd_done, bwd_done;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
   bool input_set = false;
@@ -326,7 +333,9 @@ sg_status backward(sg_net* n, int i) {
   const bool side = n->wgrad_side && (!n->prof || n->prof_concurrent) && (L.kind == SG_CONV || L.kind == SG_INNER_PRODUCT);
   cudaStream_t wst = side ? n->ps : st;
   const Workspace wws = side ? n->ws2 : n->ws;
+  n->wg_on_ps[i] = side;
   if (side) {
+    n->ps_used = true;
     SG_CUDA(cudaEventRecord(n->ev_dy[i], st));  // dy of this layer is complete
     SG_CUDA(cudaStreamWaitEvent(n->ps, n->ev_dy[i], 0));
   }
@@ -416,14 +425,20 @@ sg_status update(sg_net* n, sg_updater* u, int i) {
   // the layer's backward (the data gradient reads the working copy the Updater
   // rewrites) is complete; a side-stream weight gradient precedes in stream order
   SG_CUDA(cudaEventRecord(n->ev_grad[i], n->cs));
-  SG_CUDA(cudaStreamWaitEvent(n->ps, n->ev_grad[i], 0));
-  prof_mark(n, 4 * i + 3, 0, n->ps);
+  cudaStream_t us = n->us ? n->us : n->ps;
+  (n->us ? n->us_used : n->ps_used) = true;
+  SG_CUDA(cudaStreamWaitEvent(us, n->ev_grad[i], 0));
+  if (n->us && n->wg_on_ps[i]) {  // the layer's weight gradient (parameter stream) is complete
+    SG_CUDA(cudaEventRecord(n->ev_wg[i], n->ps));
+    SG_CUDA(cudaStreamWaitEvent(us, n->ev_wg[i], 0));
+  }
+  prof_mark(n, 4 * i + 3, 0, us);
   const float mu = u->cfg.momentum, wd = u->cfg.weight_decay * L.wd_scale;
   // elements [0, rn_end) of the store are the weight matrix (TF32-RN working copy); the bias follows
   const int64_t rn_end = P.params[L.pW].isize;
   if (S.sharded && n->px && n->px_sid[L.store] >= 0) {
     // the same exchange in one fused kernel over NVLink peer memory (exchange.h)
-    SG_LCH(px_update(n->px, n->px_sid[L.store], n->lr_dev, L.lr_scale, mu, wd, u->s, u->cfg.type, u->eps, n->ps));
+    SG_LCH(px_update(n->px, n->px_sid[L.store], n->lr_dev, L.lr_scale, mu, wd, u->s, u->cfg.type, u->eps, us));
   } else if (S.sharded) {
     // worker group -> server group: reduce-scatter (sum) of the gradient bucket;
     // the server owning shard `rank` updates its fp32 master and writes the
@@ -431,23 +446,23 @@ sg_status update(sg_net* n, sg_updater* u, int i) {
     const int64_t shard = S.padded / P.world;
     float* g = n->sgr[L.store];
     float* w = n->sw[L.store];
-    SG_NCCL(ncclReduceScatter(g, g + P.rank * shard, (size_t)shard, ncclFloat, ncclSum, n->cl->comm_par, n->ps));
+    SG_NCCL(ncclReduceScatter(g, g + P.rank * shard, (size_t)shard, ncclFloat, ncclSum, n->cl->comm_par, us));
     if (u->cfg.type == SG_UPD_ADAGRAD)
       SG_LCH(adagrad_dev(n->sm[L.store], g + P.rank * shard, n->sv[L.store], shard, n->lr_dev, L.lr_scale, wd, u->s,
-                         u->eps, n->ps, w + P.rank * shard, rn_end - P.rank * shard));
+                         u->eps, us, w + P.rank * shard, rn_end - P.rank * shard));
     else
       SG_LCH(sgd_momentum_dev(n->sm[L.store], g + P.rank * shard, n->sv[L.store], shard, n->lr_dev, L.lr_scale, mu,
-                              wd, u->s, n->ps, w + P.rank * shard, rn_end - P.rank * shard));
-    SG_NCCL(ncclAllGather(w + P.rank * shard, w, (size_t)shard, ncclFloat, n->cl->comm_par, n->ps));
+                              wd, u->s, us, w + P.rank * shard, rn_end - P.rank * shard));
+    SG_NCCL(ncclAllGather(w + P.rank * shard, w, (size_t)shard, ncclFloat, n->cl->comm_par, us));
   } else if (u->cfg.type == SG_UPD_ADAGRAD) {
     SG_LCH(adagrad_dev(n->sm[L.store], n->sgr[L.store], n->sv[L.store], S.padded, n->lr_dev, L.lr_scale, wd, u->s,
-                       u->eps, n->ps, n->sw[L.store], rn_end));
+                       u->eps, us, n->sw[L.store], rn_end));
   } else {
     SG_LCH(sgd_momentum_dev(n->sm[L.store], n->sgr[L.store], n->sv[L.store], S.padded, n->lr_dev, L.lr_scale, mu, wd,
-                            u->s, n->ps, n->sw[L.store], rn_end));
+                            u->s, us, n->sw[L.store], rn_end));
   }
-  prof_mark(n, 4 * i + 3, 1, n->ps);
-  SG_CUDA(cudaEventRecord(n->ev_upd[i], n->ps));
+  prof_mark(n, 4 * i + 3, 1, us);
+  SG_CUDA(cudaEventRecord(n->ev_upd[i], us));
   n->upd_pending[i] = 1;
   if (!n->overlap) SG_CUDA(cudaStreamWaitEvent(n->cs, n->ev_upd[i], 0));
   return SG_OK;
@@ -487,6 +502,7 @@ sg_status set_input(sg_net* n, const float* x, const int32_t* labels) {
 sg_status step_body(sg_net* n, sg_updater* u) {
   const Plan& P = PL(n);
   const int nl = (int)P.layers.size();
+  n->ps_used = n->us_used = false;  // set by the backward / Update calls below
   for (int i = 0; i < nl; ++i) {
     SG_TRY(collect(n, i));
     // the input layer reads the caller's x pointer, which changes per call: the
@@ -499,9 +515,17 @@ sg_status step_body(sg_net* n, sg_updater* u) {
     SG_TRY(update(n, u, i));
   }
   SG_TRY(loss_reduce(n));
-  // join the parameter stream (all Updates of this step) back into the compute stream
-  SG_CUDA(cudaEventRecord(n->ev_join, n->ps));
-  SG_CUDA(cudaStreamWaitEvent(n->cs, n->ev_join, 0));
+  // join the parameter / update streams (weight gradients, all Updates of this
+  // step) back into the compute stream
+  if (n->ps_used) {
+    SG_CUDA(cudaEventRecord(n->ev_join, n->ps));
+    SG_CUDA(cudaStreamWaitEvent(n->cs, n->ev_join, 0));
+  }
+  if (n->us_used) {
+    SG_CUDA(cudaEventRecord(n->ev_join_u, n->us));
+    SG_CUDA(cudaStreamWaitEvent(n->cs, n->ev_join_u, 0));
+  }
+  n->ps_used = n->us_used = false;
   std::fill(n->upd_pending.begin(), n->upd_pending.end(), 0);
   return SG_OK;
 }
@@ -596,6 +620,7 @@ sg_status param_export(sg_net* n, int p, int which, float* user) {
   const StorePlan& S = P.stores[q.store];
   SG_CUDA(cudaSetDevice(n->cl->device));
   SG_CUDA(cudaStreamSynchronize(n->ps));
+  if (n->us) SG_CUDA(cudaStreamSynchronize(n->us));
   SG_CUDA(cudaStreamSynchronize(n->cs));
   const int K = P.world;
   if (which == 3) {  // working copy: full on every rank (dim-0) or the rank's columns (dim-1)
@@ -738,17 +763,20 @@ sg_status destroy_net(sg_net* n) {
   cudaSetDevice(n->cl ? n->cl->device : 0);
   if (n->cs) cudaStreamSynchronize(n->cs);
   if (n->ps) cudaStreamSynchronize(n->ps);
+  if (n->us) cudaStreamSynchronize(n->us);
   if (n->gexec) cudaGraphExecDestroy(n->gexec);
   if (n->px) px_destroy(n->px, n->cl ? n->cl->comm_par : nullptr);
   for (void* p : n->allocs) cudaFree(p);
   for (auto e : n->ev_grad) cudaEventDestroy(e);
   for (auto e : n->ev_upd) cudaEventDestroy(e);
   for (auto e : n->ev_dy) cudaEventDestroy(e);
-  for (auto e : {n->ev_in, n->ev_out, n->ev_fork, n->ev_join})
+  for (auto e : n->ev_wg) cudaEventDestroy(e);
+  for (auto e : {n->ev_in, n->ev_out, n->ev_fork, n->ev_join, n->ev_join_u})
     if (e) cudaEventDestroy(e);
   for (auto e : n->pev) cudaEventDestroy(e);
   if (n->cs) cudaStreamDestroy(n->cs);
   if (n->ps) cudaStreamDestroy(n->ps);
+  if (n->us) cudaStreamDestroy(n->us);
   delete n;
   return SG_OK;
 }
@@ -772,6 +800,8 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
   n->ev_grad.resize(nl);
   n->ev_upd.resize(nl);
   n->ev_dy.resize(nl);
+  n->ev_wg.resize(nl);
+  n->wg_on_ps.assign(nl, 0);
   n->upd_pending.assign(nl, 0);
   n->fwd_done.assign(nl, 0);
   n->bwd_done.assign(nl, 0);
@@ -779,6 +809,7 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
     SG_CUDA(cudaEventCreateWithFlags(&n->ev_grad[i], cudaEventDisableTiming));
     SG_CUDA(cudaEventCreateWithFlags(&n->ev_upd[i], cudaEventDisableTiming));
     SG_CUDA(cudaEventCreateWithFlags(&n->ev_dy[i], cudaEventDisableTiming));
+    SG_CUDA(cudaEventCreateWithFlags(&n->ev_wg[i], cudaEventDisableTiming));
   }
   size_t ws = 1 << 16;
   auto need = [&](size_t f) {
@@ -840,6 +871,11 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
   if (n->wgrad_side) {
     SG_TRY(dalloc_t(n, ws, &n->ws2.ptr));
     n->ws2.floats = ws;
+    const char* env = getenv("SG_UPDATE_STREAM");
+    if (!env || atoi(env) != 0) {
+      SG_CUDA(cudaStreamCreateWithFlags(&n->us, cudaStreamNonBlocking));
+      SG_CUDA(cudaEventCreateWithFlags(&n->ev_join_u, cudaEventDisableTiming));
+    }
   }
   SG_TRY(dalloc_t(n, (size_t)std::max<int64_t>(P.loss_rows, 1), &n->row_loss));
   n->data[P.loss] = n->row_loss;
@@ -998,6 +1034,7 @@ SG_API sg_status sg_param_set_value(sg_net* n, int32_t p, const float* user) {
   to_internal(P, q, user, h);
   SG_CUDA(cudaSetDevice(n->cl->device));
   SG_CUDA(cudaStreamSynchronize(n->ps));
+  if (n->us) SG_CUDA(cudaStreamSynchronize(n->us));
   SG_CUDA(cudaStreamSynchronize(n->cs));
   // fp32 master: the whole Param, or its part inside this rank's shard
   const int64_t shard = S.sharded ? S.padded / P.world : S.padded;
@@ -1190,6 +1227,7 @@ SG_API sg_status sg_net_sync(sg_net* n) {
   SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
   SG_CUDA(cudaSetDevice(n->cl->device));
   SG_CUDA(cudaStreamSynchronize(n->ps));
+  if (n->us) SG_CUDA(cudaStreamSynchronize(n->us));
   SG_CUDA(cudaStreamSynchronize(n->cs));
   int flags = 0;
   SG_CUDA(cudaMemcpy(&flags, n->err, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1241,6 +1279,7 @@ SG_API sg_status sg_net_op_times(sg_net* n, double* ms, int64_t* counts, int32_t
   if (n->pev.empty()) return SG_OK;
   SG_CUDA(cudaSetDevice(n->cl->device));
   SG_CUDA(cudaStreamSynchronize(n->ps));
+  if (n->us) SG_CUDA(cudaStreamSynchronize(n->us));
   SG_CUDA(cudaStreamSynchronize(n->cs));
   for (int s = 0; s < slots; ++s) {
     if (!n->pused[s]) continue;
@@ -1270,6 +1309,7 @@ SG_API sg_status sg_net_op_timeline(sg_net* n, double* t_start, double* t_end, i
   SG_CHECK(!n->pev.empty(), SG_ERR_INVALID_ARG, "profiling never enabled");
   SG_CUDA(cudaSetDevice(n->cl->device));
   SG_CUDA(cudaStreamSynchronize(n->ps));
+  if (n->us) SG_CUDA(cudaStreamSynchronize(n->us));
   SG_CUDA(cudaStreamSynchronize(n->cs));
   int first = -1;
   for (int s = 0; s < slots && first < 0; ++s)
@@ -1306,6 +1346,7 @@ SG_API sg_status sg_net_set_exchange(sg_net* n, int32_t mode) {
   const Plan& P = PL(n);
   SG_CUDA(cudaSetDevice(n->cl->device));
   SG_CUDA(cudaStreamSynchronize(n->ps));
+  if (n->us) SG_CUDA(cudaStreamSynchronize(n->us));
   SG_CUDA(cudaStreamSynchronize(n->cs));
   if (n->gexec) {  // the captured step encodes the exchange path
     cudaGraphExecDestroy(n->gexec);

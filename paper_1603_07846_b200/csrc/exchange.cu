@@ -29,22 +29,21 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   return v;
 }
 
-// One warp: lane j < world signals rank j (slot [sid][phase][rank] of rank j's
-// flags) and waits for slot [sid][phase][j] of its own flags to reach the
-// target epoch; phase 1 (trailing) advances the bucket's device epoch by 2.
-__global__ void px_barrier_kernel(PxFlags fl, int sid, int phase, int rank, int world, unsigned* epoch,
-                                  int* err, int* err_host) {
-  pdl_entry();
-  const int j = threadIdx.x;
-  if (*(volatile int*)err) return;  // an earlier exchange failed: no waiting, no work
-  const unsigned target = epoch[sid] + 1 + phase;
-  const int slot = (sid * 2 + phase) * kPxMaxPeers;
-  __threadfence_system();  // this rank's gradient (phase 0) / peer stores (phase 1) before the signal
-  if (j < world) st_release_sys(fl.f[j] + slot + rank, target);
+// Cross-rank flag barrier of bucket sid, phase ph: lane j < world of the calling
+// warp signals rank j (slot [sid][ph][rank] of rank j's flags; only when
+// `signal`) and waits for slot [sid][ph][j] of its own flags to reach `target`.
+// Bounded spin: a peer that never arrives sets the error flag (device and
+// mapped host memory) and the wait gives up.
+__device__ __forceinline__ void px_warp_barrier(const PxFlags& fl, int sid, int ph, int rank, int world,
+                                                unsigned target, bool signal, int* err, int* err_host) {
+  const int j = threadIdx.x & 31;
+  const int slot = (sid * 2 + ph) * kPxMaxPeers;
+  if (signal && j < world) st_release_sys(fl.f[j] + slot + rank, target);
   if (j < world) {
     const unsigned* mine = fl.f[rank] + slot + j;
     long long spins = 0;
     while (ld_acquire_sys(mine) < target) {
+      if (*(volatile int*)err) break;
       if (++spins > (1LL << 26)) {
         atomicExch(err, 1);
         *(volatile int*)err_host = 1;  // mapped host memory: visible to sg_net_sync without a copy
@@ -54,66 +53,93 @@ __global__ void px_barrier_kernel(PxFlags fl, int sid, int phase, int rank, int 
     }
   }
   __syncwarp();
-  __threadfence_system();
-  if (phase == 1 && j == 0) epoch[sid] = target;
 }
 
-// Rank r's shard [r*shard, (r+1)*shard) of the bucket: ascending-rank sum of the
-// K gradients, Updater on the master shard, working copy to every rank.
+// The whole exchange of bucket sid in ONE kernel (rank r owns shard r):
+//   entry barrier (every rank's gradient of the bucket complete: CTA 0 signals,
+//   every CTA waits) -> ascending-rank sum of the K gradients of the shard,
+//   Updater on the fp32 master shard, TF32 working copy stored into every rank
+//   -> each CTA fences its stores system-wide and arrives on a counter; the last
+//   CTA runs the trailing barrier (every rank's stores into this rank landed, no
+//   peer reads this rank's gradient any more) and advances the bucket's epoch.
+// The epoch lives in device memory, so the launch is CUDA-graph replayable.
 template <int TYPE>
-__global__ void __launch_bounds__(256) px_update_kernel(PxPeers p, float* __restrict__ m, float* __restrict__ v,
-                                                        long long shard, long long rn_end, int rank, int world,
-                                                        const float* lr_dev, float lr_scale, float mu, float wd,
-                                                        float s, float eps, const int* err) {
+__global__ void __launch_bounds__(256) px_exchange_kernel(PxPeers p, PxFlags fl, float* __restrict__ m,
+                                                          float* __restrict__ v, long long shard, long long rn_end,
+                                                          int sid, int rank, int world, const float* lr_dev,
+                                                          float lr_scale, float mu, float wd, float s, float eps,
+                                                          unsigned* epoch, unsigned* counter, int* err, int* err_host) {
   pdl_entry();
-  if (*(volatile const int*)err) return;
-  const float lr = lr_dev[0] * lr_scale;
-  const long long base = (long long)rank * shard;
-  const long long n4 = shard >> 2;
-  float4* m4 = reinterpret_cast<float4*>(m);
-  float4* v4 = reinterpret_cast<float4*>(v);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
-    float4 gk[kPxMaxPeers];
+  __shared__ int last;
+  if (*(volatile const int*)err) return;  // an earlier exchange failed: no waiting, no work
+  const unsigned e0 = epoch[sid];
+  if (threadIdx.x < 32) {
+    if (blockIdx.x == 0) __threadfence_system();  // this rank's gradient before the signal
+    px_warp_barrier(fl, sid, 0, rank, world, e0 + 1, blockIdx.x == 0, err, err_host);
+  }
+  __syncthreads();
+  if (!*(volatile const int*)err) {
+    const float lr = lr_dev[0] * lr_scale;
+    const long long base = (long long)rank * shard;
+    const long long n4 = shard >> 2;
+    float4* m4 = reinterpret_cast<float4*>(m);
+    float4* v4 = reinterpret_cast<float4*>(v);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+         i += (long long)gridDim.x * blockDim.x) {
+      float4 gk[kPxMaxPeers];
 #pragma unroll
-    for (int k = 0; k < kPxMaxPeers; ++k)  // every peer load in flight before the sum
-      if (k < world) gk[k] = reinterpret_cast<const float4*>(p.g[k] + base)[i];
-    float4 g = gk[0];
+      for (int k = 0; k < kPxMaxPeers; ++k)  // every peer load in flight before the sum
+        if (k < world) gk[k] = reinterpret_cast<const float4*>(p.g[k] + base)[i];
+      float4 g = gk[0];
 #pragma unroll
-    for (int k = 1; k < kPxMaxPeers; ++k)
-      if (k < world) {
-        g.x = __fadd_rn(g.x, gk[k].x);
-        g.y = __fadd_rn(g.y, gk[k].y);
-        g.z = __fadd_rn(g.z, gk[k].z);
-        g.w = __fadd_rn(g.w, gk[k].w);
+      for (int k = 1; k < kPxMaxPeers; ++k)
+        if (k < world) {
+          g.x = __fadd_rn(g.x, gk[k].x);
+          g.y = __fadd_rn(g.y, gk[k].y);
+          g.z = __fadd_rn(g.z, gk[k].z);
+          g.w = __fadd_rn(g.w, gk[k].w);
+        }
+      float4 ww = m4[i], vv = v4[i];
+      float* wp = &ww.x;
+      float* vp = &vv.x;
+      const float* gp = &g.x;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float gq = __fmaf_rn(wd, wp[e], __fmul_rn(s, gp[e]));
+        if (TYPE == 0) {
+          vp[e] = __fmaf_rn(mu, vp[e], -__fmul_rn(lr, gq));
+          wp[e] = __fadd_rn(wp[e], vp[e]);
+        } else {
+          vp[e] = __fmaf_rn(gq, gq, vp[e]);
+          wp[e] = __fsub_rn(wp[e], __fdiv_rn(__fmul_rn(lr, gq), __fadd_rn(__fsqrt_rn(vp[e]), eps)));
+        }
       }
-    float4 ww = m4[i], vv = v4[i];
-    float* wp = &ww.x;
-    float* vp = &vv.x;
-    const float* gp = &g.x;
+      m4[i] = ww;
+      v4[i] = vv;
+      const long long el = base + 4 * i;
+      float4 wk = ww;
+      if (el < rn_end) wk.x = tf32_rna(wk.x);
+      if (el + 1 < rn_end) wk.y = tf32_rna(wk.y);
+      if (el + 2 < rn_end) wk.z = tf32_rna(wk.z);
+      if (el + 3 < rn_end) wk.w = tf32_rna(wk.w);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float gq = __fmaf_rn(wd, wp[e], __fmul_rn(s, gp[e]));
-      if (TYPE == 0) {
-        vp[e] = __fmaf_rn(mu, vp[e], -__fmul_rn(lr, gq));
-        wp[e] = __fadd_rn(wp[e], vp[e]);
-      } else {
-        vp[e] = __fmaf_rn(gq, gq, vp[e]);
-        wp[e] = __fsub_rn(wp[e], __fdiv_rn(__fmul_rn(lr, gq), __fadd_rn(__fsqrt_rn(vp[e]), eps)));
-      }
+      for (int k = 0; k < kPxMaxPeers; ++k)
+        if (k < world) reinterpret_cast<float4*>(p.w[k] + base)[i] = wk;
+      // the aggregated gradient of this shard (only this rank reads this region of its own bucket)
+      reinterpret_cast<float4*>(const_cast<float*>(p.g[rank]) + base)[i] = g;
     }
-    m4[i] = ww;
-    v4[i] = vv;
-    const long long e0 = base + 4 * i;
-    float4 wk = ww;
-    if (e0 < rn_end) wk.x = tf32_rna(wk.x);
-    if (e0 + 1 < rn_end) wk.y = tf32_rna(wk.y);
-    if (e0 + 2 < rn_end) wk.z = tf32_rna(wk.z);
-    if (e0 + 3 < rn_end) wk.w = tf32_rna(wk.w);
-#pragma unroll
-    for (int k = 0; k < kPxMaxPeers; ++k)
-      if (k < world) reinterpret_cast<float4*>(p.w[k] + base)[i] = wk;
-    // the aggregated gradient of this shard (only this rank reads this region of its own bucket)
-    reinterpret_cast<float4*>(const_cast<float*>(p.g[rank]) + base)[i] = g;
+  }
+  // completion: this CTA's stores (local and remote) before its arrival
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter + sid, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence_system();
+  px_warp_barrier(fl, sid, 1, rank, world, e0 + 2, true, err, err_host);
+  if (threadIdx.x == 0) {
+    counter[sid] = 0;
+    epoch[sid] = e0 + 2;
   }
 }
 
@@ -126,6 +152,7 @@ struct PeerExchange {
   PxFlags flags{};
   unsigned* flags_own = nullptr;
   unsigned* epoch = nullptr;
+  unsigned* counter = nullptr;  // per bucket: CTAs of the running exchange kernel that finished
   int* err_dev = nullptr;     // device memory, read by every exchange kernel
   int* err_host = nullptr;    // mapped pinned copy (written on failure only)
   int* err_host_dev = nullptr;
@@ -160,6 +187,8 @@ sg_status px_create(ncclComm_t comm, int rank, int world, int device, const std:
   if (ok) check(cudaMemset(px->flags_own, 0, nflags * sizeof(unsigned)), "flags");
   if (ok) check(cudaMalloc(&px->epoch, std::max<size_t>(stores.size(), 1) * sizeof(unsigned)), "epoch");
   if (ok) check(cudaMemset(px->epoch, 0, std::max<size_t>(stores.size(), 1) * sizeof(unsigned)), "epoch");
+  if (ok) check(cudaMalloc(&px->counter, std::max<size_t>(stores.size(), 1) * sizeof(unsigned)), "counter");
+  if (ok) check(cudaMemset(px->counter, 0, std::max<size_t>(stores.size(), 1) * sizeof(unsigned)), "counter");
   if (ok) check(cudaMalloc(&px->err_dev, sizeof(int)), "error flag");
   if (ok) check(cudaMemset(px->err_dev, 0, sizeof(int)), "error flag");
   if (ok) check(cudaHostAlloc(&px->err_host, sizeof(int), cudaHostAllocMapped), "error flag");
@@ -274,6 +303,7 @@ void px_destroy(PeerExchange* px, ncclComm_t comm) {
   for (void* q : px->opened) cudaIpcCloseMemHandle(q);
   cudaFree(px->flags_own);
   cudaFree(px->epoch);
+  cudaFree(px->counter);
   cudaFree(px->err_dev);
   if (px->err_host) cudaFreeHost(px->err_host);
   delete px;
@@ -285,19 +315,11 @@ cudaError_t px_update(PeerExchange* px, int sid, const float* lr_dev, float lr_s
                       int type, float eps, cudaStream_t st) {
   const PxStore& S = px->stores[sid];
   const long long shard = S.padded / px->world;
-  cudaError_t e = launch_k(px_barrier_kernel, 1, 32, 0, st, px->flags, sid, 0, px->rank, px->world, px->epoch,
-                           px->err_dev, px->err_host_dev);
-  if (e != cudaSuccess) return e;
   const long long n4 = shard / 4;
   const int blocks = (int)std::max<long long>(1, std::min<long long>((n4 + 255) / 256, 4LL * px->sms));
-  if (type == 1)
-    e = launch_k(px_update_kernel<1>, blocks, 256, 0, st, px->peers[sid], S.m, S.v, shard, (long long)S.rn_end,
-                 px->rank, px->world, lr_dev, lr_scale, mu, wd, s, eps, (const int*)px->err_dev);
-  else
-    e = launch_k(px_update_kernel<0>, blocks, 256, 0, st, px->peers[sid], S.m, S.v, shard, (long long)S.rn_end,
-                 px->rank, px->world, lr_dev, lr_scale, mu, wd, s, eps, (const int*)px->err_dev);
-  if (e != cudaSuccess) return e;
-  return launch_k(px_barrier_kernel, 1, 32, 0, st, px->flags, sid, 1, px->rank, px->world, px->epoch, px->err_dev,
+  auto k = type == 1 ? px_exchange_kernel<1> : px_exchange_kernel<0>;
+  return launch_k(k, blocks, 256, 0, st, px->peers[sid], px->flags, S.m, S.v, shard, (long long)S.rn_end, sid,
+                  px->rank, px->world, lr_dev, lr_scale, mu, wd, s, eps, px->epoch, px->counter, px->err_dev,
                   px->err_host_dev);
 }
 

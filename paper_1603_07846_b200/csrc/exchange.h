@@ -44,7 +44,7 @@ sg_status px_create(ncclComm_t comm, int rank, int world, int device, const std:
                     PeerExchange** out);
 // COLLECTIVE; synchronises the device first.
 void px_destroy(PeerExchange* px, ncclComm_t comm);
-// Enqueue the exchange of bucket `sid` on `st` (3 kernel launches).
+// Enqueue the exchange of bucket `sid` on `st` (one kernel launch).
 // type 0: SGD momentum (mu), 1: AdaGrad (eps); lr = lr_dev[0] * lr_scale.
 cudaError_t px_update(PeerExchange* px, int sid, const float* lr_dev, float lr_scale, float mu, float wd, float s,
                       int type, float eps, cudaStream_t st);

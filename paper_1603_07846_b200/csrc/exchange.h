@@ -2,18 +2,20 @@
 // peer memory (§5.2.1 AllReduce framework
 // P:419-422, per-layer Update of Alg. 1, parameters "broadcast back"
 // P:586, Updater P:282-284): per sharded Param bucket, instead of
-// reduce-scatter -> Updater -> all-gather,
-//   barrier (every rank's gradient of the bucket is complete)
-//   -> one kernel: rank r loads shard r of every rank's gradient straight from
-//      the peers' HBM, sums them in ascending rank order (the oracle's order),
-//      applies the Updater to its fp32 master shard + history, writes the TF32
-//      working copy of the shard into EVERY rank's weight bucket (P2P stores)
-//      and the aggregated gradient into its own bucket (sg_param_get_grad)
-//   -> barrier (every rank's stores have landed; no rank will overwrite a
-//      gradient a peer still reads).
+// reduce-scatter -> Updater -> all-gather, ONE kernel:
+//   entry barrier (every rank's gradient of the bucket is complete; CTA 0
+//   signals, every CTA waits)
+//   -> rank r loads shard r of every rank's gradient straight from the peers'
+//      HBM, sums them in ascending rank order (the oracle's order), applies the
+//      Updater to its fp32 master shard + history, writes the TF32 working copy
+//      of the shard into EVERY rank's weight bucket (P2P stores) and the
+//      aggregated gradient into its own bucket (sg_param_get_grad)
+//   -> the last CTA to finish (arrival counter) runs the trailing barrier
+//      (every rank's stores have landed; no rank will overwrite a gradient a
+//      peer still reads).
 // Barrier flags live in IPC-shared device memory; the epoch of every bucket is
-// kept in device memory and advanced by the barrier kernels themselves, so the
-// three launches per bucket are CUDA-graph replayable.  A peer that never
+// kept in device memory and advanced by the kernel itself, so the launch is
+// CUDA-graph replayable.  A peer that never
 // arrives: bounded spin, then an error flag in mapped host memory; every later
 // exchange kernel skips its work, the error is reported by sg_net_sync.
 #pragma once

@@ -340,7 +340,10 @@ def main():
 
     # ---------------- timed region: exactly K steps ----------------
     clock = ClockLog(local)
-    time.sleep(0.2)
+    # let nvidia-smi finish its (driver-locking) start-up before the timed
+    # region: a rank whose host stalls while enqueueing the first steps leaves
+    # the other ranks' device-side barriers spinning (seen once per scaling run)
+    time.sleep(1.0)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -360,6 +363,9 @@ def main():
     n.sync()
     step_ms = [a.elapsed_time(b_) for a, b_ in evs]
     total_ms = sum(step_ms)
+    srt = sorted(step_ms)
+    print(f"[rank {rank}] step ms min {srt[0]:.4f} median {srt[len(srt) // 2]:.4f} max {srt[-1]:.4f} "
+          f"(argmax {step_ms.index(srt[-1])})", file=sys.stderr)
     if world > 1:
         t_ = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t_, op=dist.ReduceOp.MAX)

@@ -347,6 +347,15 @@ SG_API sg_status sg_train_one_batch(sg_net* n, sg_updater* u, int64_t step, cons
  * on return).  Use pinned buffers for asynchronous copies. COLLECTIVE. */
 SG_API sg_status sg_train_one_batch_host(sg_net* n, sg_updater* u, int64_t step, const float* x_host,
                                          const int32_t* labels_host, float* loss_host, void* stream);
+/* Pipelined variant (a training loop's data path): enqueues the host->device
+ * copy of this step's inputs on an internal copy stream (two device input
+ * slots, so it overlaps the previous step's compute), the step on `stream`, and
+ * the device->host copy of the loss into *loss_host, and returns without
+ * waiting.  x_host / labels_host (pinned) must stay unchanged, and *loss_host
+ * is valid, only after the stream has been synchronised (or sg_net_sync).
+ * COLLECTIVE. */
+SG_API sg_status sg_train_one_batch_host_async(sg_net* n, sg_updater* u, int64_t step, const float* x_host,
+                                               const int32_t* labels_host, float* loss_host, void* stream);
 
 /* Alg. 1 driven layer by layer (same work as sg_train_one_batch):
  *   sg_net_set_input; for i: sg_net_collect(i), sg_layer_compute_feature(i);

@@ -136,6 +136,7 @@ SIGS = {
     "sg_updater_destroy": [P],
     "sg_train_one_batch": [P, P, I64, P, P, P, P],
     "sg_train_one_batch_host": [P, P, I64, P, P, P, P],
+    "sg_train_one_batch_host_async": [P, P, I64, P, P, P, P],
     "sg_net_set_input": [P, P, P, P],
     "sg_net_collect": [P, I32, P],
     "sg_layer_compute_feature": [P, I32, P],

@@ -70,6 +70,14 @@ struct sg_net {
   int* err = nullptr;
   int32_t* labels = nullptr;
   float* x_stage = nullptr;
+  // pipelined host path (sg_train_one_batch_host_async): a second input slot,
+  // label slots, a copy stream, and per-slot events (copied / free again)
+  float* x_stage2 = nullptr;
+  int32_t* lab_stage[2] = {nullptr, nullptr};
+  cudaStream_t hs = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  int stage_k = 0;
+  bool stage_used[2] = {false, false};
   float* x_exact = nullptr;  // unrounded copy of the input blob (a Euclidean loss's target when the input is rounded)
   const float* x_src = nullptr;
   sg::Workspace ws;
@@ -777,6 +785,11 @@ sg_status destroy_net(sg_net* n) {
   if (n->cs) cudaStreamDestroy(n->cs);
   if (n->ps) cudaStreamDestroy(n->ps);
   if (n->us) cudaStreamDestroy(n->us);
+  if (n->hs) cudaStreamDestroy(n->hs);
+  for (int k = 0; k < 2; ++k) {
+    if (n->ev_copied[k]) cudaEventDestroy(n->ev_copied[k]);
+    if (n->ev_free[k]) cudaEventDestroy(n->ev_free[k]);
+  }
   delete n;
   return SG_OK;
 }
@@ -886,6 +899,14 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
   {
     const LayerPlan& in = P.layers[0];
     SG_TRY(dalloc_t(n, (size_t)(in.rows * in.feat), &n->x_stage));
+    // the pipelined host path's second input slot, label slots, copy stream, events
+    SG_TRY(dalloc_t(n, (size_t)(in.rows * in.feat), &n->x_stage2));
+    SG_CUDA(cudaStreamCreateWithFlags(&n->hs, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      SG_CUDA(cudaEventCreateWithFlags(&n->ev_copied[k], cudaEventDisableTiming));
+      SG_CUDA(cudaEventCreateWithFlags(&n->ev_free[k], cudaEventDisableTiming));
+      SG_TRY(dalloc_t(n, (size_t)std::max<int64_t>(P.loss_rows, 1), &n->lab_stage[k]));
+    }
   }
   if (P.layers[P.loss].kind == SG_EUCLIDEAN && P.layers[0].rn_data)
     SG_TRY(dalloc_t(n, (size_t)P.layers[0].blob_floats(), &n->x_exact));
@@ -1223,11 +1244,41 @@ SG_API sg_status sg_train_one_batch_host(sg_net* n, sg_updater* u, int64_t step,
   return SG_OK;
 }
 
+SG_API sg_status sg_train_one_batch_host_async(sg_net* n, sg_updater* u, int64_t step, const float* x_host,
+                                               const int32_t* labels_host, float* loss_host, void* stream) {
+  SG_CHECK(n && u && x_host && loss_host, SG_ERR_INVALID_ARG, "sg_train_one_batch_host_async: null argument");
+  const Plan& P = PL(n);
+  const LayerPlan& in = P.layers[0];
+  SG_CUDA(cudaSetDevice(n->cl->device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int k = n->stage_k;
+  n->stage_k ^= 1;
+  float* xs = k ? n->x_stage2 : n->x_stage;
+  // the step that last read slot k is done; then this step's inputs, on the copy
+  // stream (overlapping the previous step's compute)
+  if (n->stage_used[k]) SG_CUDA(cudaStreamWaitEvent(n->hs, n->ev_free[k], 0));
+  SG_CUDA(cudaMemcpyAsync(xs, x_host, (size_t)(in.rows * in.feat) * sizeof(float), cudaMemcpyHostToDevice, n->hs));
+  const int32_t* ldev = nullptr;
+  if (labels_host && P.layers[P.loss].kind == SG_SOFTMAX_CE) {
+    SG_CUDA(cudaMemcpyAsync(n->lab_stage[k], labels_host, (size_t)P.loss_rows * sizeof(int32_t),
+                            cudaMemcpyHostToDevice, n->hs));
+    ldev = n->lab_stage[k];
+  }
+  SG_CUDA(cudaEventRecord(n->ev_copied[k], n->hs));
+  SG_CUDA(cudaStreamWaitEvent(st, n->ev_copied[k], 0));
+  SG_TRY(sg_train_one_batch(n, u, step, xs, ldev, n->loss_int, stream));
+  SG_CUDA(cudaEventRecord(n->ev_free[k], st));
+  n->stage_used[k] = true;
+  SG_CUDA(cudaMemcpyAsync(loss_host, n->loss_int, sizeof(float), cudaMemcpyDeviceToHost, st));
+  return SG_OK;
+}
+
 SG_API sg_status sg_net_sync(sg_net* n) {
   SG_CHECK(n, SG_ERR_INVALID_ARG, "null net");
   SG_CUDA(cudaSetDevice(n->cl->device));
   SG_CUDA(cudaStreamSynchronize(n->ps));
   if (n->us) SG_CUDA(cudaStreamSynchronize(n->us));
+  if (n->hs) SG_CUDA(cudaStreamSynchronize(n->hs));
   SG_CUDA(cudaStreamSynchronize(n->cs));
   int flags = 0;
   SG_CUDA(cudaMemcpy(&flags, n->err, sizeof(int), cudaMemcpyDeviceToHost));

@@ -317,6 +317,39 @@ def test_graph_replay_bit_exact_and_host_entry():
             r.close()
 
 
+def test_pipelined_host_entry_matches_sync():
+    """sg_train_one_batch_host_async (two input slots, copies on their own stream)
+    gives bit-identical losses and parameters to the synchronous host entry."""
+    import torch
+    net = configs.get("cifar10")
+    b = 32
+    runs = [Run(net, b, graph=True), Run(net, b, graph=True)]
+    try:
+        steps = 6
+        xs = [torch.from_numpy(np.ascontiguousarray(generate.batch(net, b, t)[0])).pin_memory() for t in range(steps)]
+        ls = [torch.from_numpy(np.ascontiguousarray(generate.batch(net, b, t)[1])).pin_memory() for t in range(steps)]
+        loss_h = torch.zeros(steps, dtype=torch.float32).pin_memory()
+        sync_losses = []
+        for t in range(steps):
+            lh = C.c_float()
+            L.sg_train_one_batch_host(runs[0].n.h, runs[0].n.upd, t, C.c_void_p(xs[t].data_ptr()),
+                                      C.c_void_p(ls[t].data_ptr()), C.byref(lh), None)
+            sync_losses.append(lh.value)
+        for t in range(steps):
+            L.sg_train_one_batch_host_async(runs[1].n.h, runs[1].n.upd, t, C.c_void_p(xs[t].data_ptr()),
+                                            C.c_void_p(ls[t].data_ptr()), C.c_void_p(loss_h[t:].data_ptr()), None)
+        runs[1].n.sync()
+        torch.cuda.synchronize()
+        assert [float(v) for v in loss_h] == sync_losses
+        pa = runs[0].n.get_params(shapes_of(runs[0].p0))
+        pb = runs[1].n.get_params(shapes_of(runs[1].p0))
+        for k in pa:
+            assert np.array_equal(pa[k], pb[k]), k
+    finally:
+        for r in runs:
+            r.close()
+
+
 def test_zero_lr_keeps_params_and_label_error():
     net = configs.get("cifar10")
     b = 16

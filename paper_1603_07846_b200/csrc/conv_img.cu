@@ -27,6 +27,7 @@
 
 #include <algorithm>
 
+#include "elt_common.cuh"
 #include "ops.h"
 #include "sg_common.cuh"
 
@@ -744,8 +745,11 @@ __global__ void __launch_bounds__(kImgThreads, 1) conv_img_wgrad_kernel(const __
 
 // dW / db = sum over the samples' partials in ascending n: block = 32 outputs x
 // 16 warps; warp w sums partials w, w+16, ...; warp 0 adds the 16 in order.
+// With has_fu (first layer, K = 1) the summed element is also run through the
+// Updater (fused_update1: the same arithmetic as the Updater kernels).
 __global__ void __launch_bounds__(512) conv_wgrad_sum_kernel(const float* __restrict__ part, int nparts, int per,
-                                                             int nw, float* __restrict__ dW, float* __restrict__ db) {
+                                                             int nw, float* __restrict__ dW, float* __restrict__ db,
+                                                             FusedUpdate fu, int has_fu) {
   __shared__ float red[16][32];
   pdl_entry();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -759,10 +763,13 @@ __global__ void __launch_bounds__(512) conv_wgrad_sum_kernel(const float* __rest
   float t = 0.f;
 #pragma unroll
   for (int k = 0; k < 16; ++k) t += red[k][lane];
-  if (i < nw)
+  if (i < nw) {
     dW[i] = t;
-  else if (db)
+    if (has_fu) fused_update1(fu, fu.w, fu.v, fu.wk, i, t, true);
+  } else if (db) {
     db[i - nw] = t;
+    if (has_fu) fused_update1(fu, fu.wb, fu.vb, fu.wkb, i - nw, t, false);
+  }
 }
 
 // Tap grouping: per filter row r, runs of 4 consecutive s (stride 1 row); the
@@ -905,7 +912,8 @@ cudaError_t conv_img_wgrad(const ConvShape& s, const float* x, const float* dy, 
   e = launch_k(k, ctas, kImgThreads, smem, st, a);
   if (e != cudaSuccess) return e;
   const int nw = s.Co * s.R * s.S * s.C, per = nw + s.Co;
-  return launch_k(conv_wgrad_sum_kernel, (per + 31) / 32, 512, 0, st, (const float*)a.part, ctas, per, nw, dW, db);
+  return launch_k(conv_wgrad_sum_kernel, (per + 31) / 32, 512, 0, st, (const float*)a.part, ctas, per, nw, dW, db,
+                  FusedUpdate{}, 0);
 }
 
 bool conv_img_fwd_ok(const ConvShape& s) {
@@ -1344,7 +1352,7 @@ bool plan_img4_wgrad(const ConvShape& s, Img4WgradArgs* a, size_t* smem) {
 int img4_wgrad_ctas(int nimg) { return std::min(nimg, 148); }
 
 cudaError_t launch_img4_wgrad(Img4WgradArgs& a, size_t smem, const float* x, const ConvShape& s, bool pool,
-                              float* dW, float* db, cudaStream_t st) {
+                              float* dW, float* db, cudaStream_t st, const FusedUpdate* fu = nullptr) {
   const cuuint64_t xd[4] = {4, (cuuint64_t)s.W, (cuuint64_t)s.H, (cuuint64_t)s.N};
   const cuuint64_t xs[3] = {16, (cuuint64_t)s.W * 16, (cuuint64_t)s.H * s.W * 16};
   const cuuint32_t xb[4] = {4, (cuuint32_t)a.Wp, (cuuint32_t)a.Hp, 1};
@@ -1360,7 +1368,8 @@ cudaError_t launch_img4_wgrad(Img4WgradArgs& a, size_t smem, const float* x, con
   cudaError_t e = launch_k(k, ctas, kI4WThreads, smem, st, a);
   if (e != cudaSuccess) return e;
   const int nw = s.Co * a.T * 4, per = nw + s.Co;
-  return launch_k(conv_wgrad_sum_kernel, (per + 31) / 32, 512, 0, st, (const float*)a.part, ctas, per, nw, dW, db);
+  return launch_k(conv_wgrad_sum_kernel, (per + 31) / 32, 512, 0, st, (const float*)a.part, ctas, per, nw, dW, db,
+                  fu ? *fu : FusedUpdate{}, fu ? 1 : 0);
 }
 
 }  // namespace
@@ -1396,7 +1405,7 @@ bool conv_img4_pool_bwd_ok(const ConvShape& s, const PoolShape& p) {
 
 cudaError_t conv_img4_pool_bwd(const ConvShape& s, const PoolShape& p, const float* x, const float* gpool,
                                const uint8_t* mask, float* dy_out, int rn, float* dW, float* db, Workspace ws,
-                               cudaStream_t st) {
+                               cudaStream_t st, const FusedUpdate* fu) {
   Img4WgradArgs a;
   size_t smem;
   if (!conv_img4_pool_bwd_ok(s, p) || !plan_img4_wgrad(s, &a, &smem) || ws.floats < conv_img4_wgrad_ws_floats(s))
@@ -1416,7 +1425,7 @@ cudaError_t conv_img4_pool_bwd(const ConvShape& s, const PoolShape& p, const flo
   a.fps = make_fastdiv(p.s);
   a.fpk = make_fastdiv(p.k);
   a.part = ws.ptr + 1024;
-  return launch_img4_wgrad(a, smem, x, s, true, dW, db, st);
+  return launch_img4_wgrad(a, smem, x, s, true, dW, db, st, fu);
 }
 
 }  // namespace sg

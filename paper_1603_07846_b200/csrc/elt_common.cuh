@@ -72,4 +72,46 @@ __device__ __forceinline__ float lrn_bwd_out(float g, float s, float x, float ac
   return __fsub_rn(__fmul_rn(g, pow_neg(s, beta)), __fmul_rn(__fmul_rn(coef, x), acc));
 }
 
+// ---------------------------------------------------------------- Updater --
+// g' = s g + wd w ; v = mu v - lr g' ; w = w + v ; fixed FMA order.
+__device__ __forceinline__ void sgd1(float& w, float g, float& v, float lr, float mu, float wd, float s) {
+  float gp = __fmaf_rn(wd, w, __fmul_rn(s, g));
+  v = __fmaf_rn(mu, v, -__fmul_rn(lr, gp));
+  w = __fadd_rn(w, v);
+}
+
+// AdaGrad (reading A26), same working-copy convention as the SGD update.
+__device__ __forceinline__ void adagrad1(float& w, float g, float& h, float lr, float wd, float s, float eps) {
+  const float gp = __fmaf_rn(wd, w, __fmul_rn(s, g));
+  h = __fmaf_rn(gp, gp, h);
+  w = __fsub_rn(w, __fdiv_rn(__fmul_rn(lr, gp), __fadd_rn(__fsqrt_rn(h), eps)));
+}
+
+
+// A weight-gradient reduction that also applies the Updater to the elements it
+// produced (first layer at K = 1: its Update is the step's last operation).
+struct FusedUpdate {
+  float* w;    // fp32 master of dW's elements (then the bias part: wb)
+  float* v;    // history
+  float* wk;   // TF32-RN working copy (weights), exact copy (bias)
+  float* wb;
+  float* vb;
+  float* wkb;
+  const float* lr_dev;
+  float lr_scale, mu, wd, s, eps;
+  int type;    // 0 SGD momentum, 1 AdaGrad
+};
+__device__ __forceinline__ void fused_update1(const FusedUpdate& u, float* w, float* v, float* wk, long long i, float g,
+                                              bool rn) {
+  const float lr = u.lr_dev[0] * u.lr_scale;
+  float ww = w[i], vv = v[i];
+  if (u.type == 0)
+    sgd1(ww, g, vv, lr, u.mu, u.wd, u.s);
+  else
+    adagrad1(ww, g, vv, lr, u.wd, u.s, u.eps);
+  w[i] = ww;
+  v[i] = vv;
+  wk[i] = rn ? tf32_rna(ww) : ww;
+}
+
 }  // namespace sg

@@ -94,10 +94,12 @@ size_t conv_img4_wgrad_ws_floats(const ConvShape& s);
 cudaError_t conv_img4_wgrad(const ConvShape& s, const float* x, const float* dy, float* dW, float* db, Workspace ws,
                             cudaStream_t st);
 struct PoolShape;
+struct FusedUpdate;  // elt_common.cuh
 bool conv_img4_pool_bwd_ok(const ConvShape& s, const PoolShape& p);
+// fu (optional, K = 1): the reduction of dW / db also applies the Updater
 cudaError_t conv_img4_pool_bwd(const ConvShape& s, const PoolShape& p, const float* x, const float* gpool,
                                const uint8_t* mask, float* dy_out, int rn, float* dW, float* db, Workspace ws,
-                               cudaStream_t st);
+                               cudaStream_t st, const FusedUpdate* fu = nullptr);
 
 // ---- convolution (implicit GEMM, tcgen05 kind::tf32) ----
 // flags: EPI_RELU | EPI_RN

@@ -558,13 +558,6 @@ __global__ void sum_scaled_kernel(const float* __restrict__ v, int n, float scal
 }
 
 // ----------------------------------------------------------------- Updater --
-// g' = s g + wd w ; v = mu v - lr g' ; w = w + v ; fixed FMA order.
-__device__ __forceinline__ void sgd1(float& w, float g, float& v, float lr, float mu, float wd, float s) {
-  float gp = __fmaf_rn(wd, w, __fmul_rn(s, g));
-  v = __fmaf_rn(mu, v, -__fmul_rn(lr, gp));
-  w = __fadd_rn(w, v);
-}
-
 // Master copy w and history v updated in place; when wk != nullptr the
 // working copy the GEMMs read is written too: wk[i] = TF32-RN(w[i]) for
 // i < rn_end (weights, tensor-core operands, reading A19), wk[i] = w[i] beyond
@@ -607,12 +600,6 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, f
 }
 
 // AdaGrad (reading A26), same working-copy convention as sgd_kernel.
-__device__ __forceinline__ void adagrad1(float& w, float g, float& h, float lr, float wd, float s, float eps) {
-  const float gp = __fmaf_rn(wd, w, __fmul_rn(s, g));
-  h = __fmaf_rn(gp, gp, h);
-  w = __fsub_rn(w, __fdiv_rn(__fmul_rn(lr, gp), __fadd_rn(__fsqrt_rn(h), eps)));
-}
-
 __global__ void adagrad_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ h,
                                float* __restrict__ wk, long long rn_end, long long n, const float* lr_dev,
                                float lr_scale, float lr_val, float wd, float s, float eps) {

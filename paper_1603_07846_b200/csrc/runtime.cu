@@ -16,6 +16,7 @@
 
 #include "abi_common.h"
 #include "exchange.h"
+#include "elt_common.cuh"
 #include "ops.h"
 #include "plan.h"
 
@@ -93,6 +94,11 @@ struct sg_net {
   cudaStream_t us = nullptr;
   cudaEvent_t ev_join_u = nullptr;
   std::vector<char> wg_on_ps;      // layer i's weight gradient of this step ran on the parameter stream
+  // first layer at K = 1: its Update applied by the weight-gradient reduction
+  // (the step's last operation); update() then only records the event
+  std::vector<char> upd_in_bwd;
+  std::vector<cudaStream_t> upd_bwd_stream;
+  bool fuse_update = true;
   bool ps_used = false, us_used = false;  // streams forked in this step (joined at its end)
   std::vector<char> upd_pending, fwd_done, bwd_done;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
@@ -323,7 +329,7 @@ sg_status forward_impl(sg_net* n, int i) {
 }
 
 // ---- ComputeGradient ----
-sg_status backward(sg_net* n, int i) {
+sg_status backward(sg_net* n, int i, const sg_updater* u = nullptr) {
   const Plan& P = PL(n);
   const LayerPlan& L = P.layers[i];
   cudaStream_t st = n->cs;
@@ -352,8 +358,20 @@ sg_status backward(sg_net* n, int i) {
     case SG_CONV:
       if (n->pool_into[i] >= 0) {  // fused: the max pool's backward builds this layer's dy (a13 + a15)
         const int c = n->pool_into[i];
+        // K = 1 and no data gradient: the reduction also applies the Updater
+        const bool fu_on = u && n->fuse_update && K == 1 && !need_dx && L.store >= 0 && L.pW >= 0 && L.pb >= 0 &&
+                           !P.stores[L.store].sharded;
+        FusedUpdate fu{};
+        if (fu_on) {
+          const int64_t ow = P.params[L.pW].store_off, ob = P.params[L.pb].store_off;
+          fu = FusedUpdate{n->sm[L.store] + ow, n->sv[L.store] + ow, n->sw[L.store] + ow, n->sm[L.store] + ob,
+                           n->sv[L.store] + ob, n->sw[L.store] + ob, n->lr_dev, L.lr_scale, u->cfg.momentum,
+                           u->cfg.weight_decay * L.wd_scale, u->s, u->eps, u->cfg.type == SG_UPD_ADAGRAD ? 1 : 0};
+          n->upd_in_bwd[i] = 1;
+          n->upd_bwd_stream[i] = wst;
+        }
         SG_LCH(conv_img4_pool_bwd(conv_shape(L, S), pool_shape(P.layers[c], L), n->data[L.src], n->grad[c],
-                                  n->mask[c], n->grad[i], L.rn_grad, dW, db, wws, wst));
+                                  n->mask[c], n->grad[i], L.rn_grad, dW, db, wws, wst, fu_on ? &fu : nullptr));
       } else if (n->s2d_x[i] && n->s2d_wgrad) {
         SG_LCH(conv_wgrad_s2d(conv_shape(L, S), n->s2d_x[i], n->grad[i], n->s2d_dw[i], dW, db, wws, wst));
       } else {
@@ -430,6 +448,13 @@ sg_status update(sg_net* n, sg_updater* u, int i) {
   const LayerPlan& L = P.layers[i];
   if (L.store < 0) return SG_OK;
   const StorePlan& S = P.stores[L.store];
+  if (n->upd_in_bwd[i]) {  // applied by the weight-gradient reduction (backward)
+    n->upd_in_bwd[i] = 0;
+    SG_CUDA(cudaEventRecord(n->ev_upd[i], n->upd_bwd_stream[i]));
+    n->upd_pending[i] = 1;
+    if (!n->overlap) SG_CUDA(cudaStreamWaitEvent(n->cs, n->ev_upd[i], 0));
+    return SG_OK;
+  }
   // the layer's backward (the data gradient reads the working copy the Updater
   // rewrites) is complete; a side-stream weight gradient precedes in stream order
   SG_CUDA(cudaEventRecord(n->ev_grad[i], n->cs));
@@ -519,7 +544,7 @@ sg_status step_body(sg_net* n, sg_updater* u) {
     SG_TRY(forward(n, i));
   }
   for (int i = nl - 1; i >= 0; --i) {
-    SG_TRY(backward(n, i));
+    SG_TRY(backward(n, i, u));
     SG_TRY(update(n, u, i));
   }
   SG_TRY(loss_reduce(n));
@@ -815,6 +840,12 @@ sg_status create_net(sg_cluster* c, const sg_net_cfg* cfg, sg_net* n) {
   n->ev_dy.resize(nl);
   n->ev_wg.resize(nl);
   n->wg_on_ps.assign(nl, 0);
+  n->upd_in_bwd.assign(nl, 0);
+  n->upd_bwd_stream.assign(nl, nullptr);
+  {
+    const char* env = getenv("SG_FUSE_UPDATE");
+    n->fuse_update = env ? atoi(env) != 0 : true;
+  }
   n->upd_pending.assign(nl, 0);
   n->fwd_done.assign(nl, 0);
   n->bwd_done.assign(nl, 0);

@@ -442,7 +442,8 @@ SG_API sg_status sg_server_sync(sg_cluster* c, const sg_updater_cfg* cfg, int64_
  * rank r loads every rank's gradient for its shard [r*n/K, (r+1)*n/K) from
  * the peers' HBM, sums them in ascending rank order, applies the Updater
  * (s = grad_scale, else 1/K) and stores the new weights into every rank's
- * weight buffer.  Two flag barriers in peer memory bracket it.
+ * weight buffer (the step's fused exchange, exchange.h: entry barrier in the
+ * kernel, trailing barrier by its last CTA).
  *
  * sg_peer_sync_create: COLLECTIVE (all ranks of the cluster).  Allocates the
  *   library-owned device buffers grad_full[n], w_full[n] and v_shard[n/K]
@@ -451,11 +452,14 @@ SG_API sg_status sg_server_sync(sg_cluster* c, const sg_updater_cfg* cfg, int64_
  *   pointers stay valid until destroy) and exchanges CUDA IPC handles over the
  *   parameter communicator.  n must be a multiple of 32*K (SG_ERR_PARTITION);
  *   K <= 8 (SG_ERR_UNSUPPORTED); allocation failure -> SG_ERR_OOM; IPC
- *   failure -> SG_ERR_CUDA.
- * sg_peer_sync_step: COLLECTIVE, asynchronous on `stream` (3 kernel launches).
- *   grad_full is read, not modified.  After the step every rank's w_full holds
- *   the same updated weights.  A peer that never arrives makes the barrier
- *   give up after a bounded spin; that is reported by sg_peer_sync_destroy.
+ *   failure -> SG_ERR_CUDA.  A failure on any rank fails every rank (status
+ *   word in the handle exchange, then an all-reduced decision).
+ * sg_peer_sync_step: COLLECTIVE, asynchronous on `stream` (the learning-rate
+ *   write and ONE exchange kernel).  grad_full is read, not modified.  After
+ *   the step every rank's w_full holds the same updated weights.  A peer that
+ *   never arrives makes the barrier give up after a bounded spin and sets an
+ *   error flag: that step and every later one skip their work (no unsynchronised
+ *   reads or stores); sg_peer_sync_destroy reports it.
  * sg_peer_sync_destroy: COLLECTIVE; synchronises, frees the buffers; returns
  *   SG_ERR_CUDA if any barrier timed out.
  * ====================================================================== */

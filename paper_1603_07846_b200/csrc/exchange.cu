@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(256) px_exchange_kernel(PxPeers p, PxFlags fl,
                                                           float* __restrict__ v, long long shard, long long rn_end,
                                                           int sid, int rank, int world, const float* lr_dev,
                                                           float lr_scale, float mu, float wd, float s, float eps,
-                                                          unsigned* epoch, unsigned* counter, int* err, int* err_host) {
+                                                          unsigned* epoch, unsigned* counter, int* err, int* err_host,
+                                                          int agg_out) {
   pdl_entry();
   __shared__ int last;
   if (*(volatile const int*)err) return;  // an earlier exchange failed: no waiting, no work
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(256) px_exchange_kernel(PxPeers p, PxFlags fl,
       for (int k = 0; k < kPxMaxPeers; ++k)
         if (k < world) reinterpret_cast<float4*>(p.w[k] + base)[i] = wk;
       // the aggregated gradient of this shard (only this rank reads this region of its own bucket)
-      reinterpret_cast<float4*>(const_cast<float*>(p.g[rank]) + base)[i] = g;
+      if (agg_out) reinterpret_cast<float4*>(const_cast<float*>(p.g[rank]) + base)[i] = g;
     }
   }
   // completion: this CTA's stores (local and remote) before its arrival
@@ -320,7 +321,7 @@ cudaError_t px_update(PeerExchange* px, int sid, const float* lr_dev, float lr_s
   auto k = type == 1 ? px_exchange_kernel<1> : px_exchange_kernel<0>;
   return launch_k(k, blocks, 256, 0, st, px->peers[sid], px->flags, S.m, S.v, shard, (long long)S.rn_end, sid,
                   px->rank, px->world, lr_dev, lr_scale, mu, wd, s, eps, px->epoch, px->counter, px->err_dev,
-                  px->err_host_dev);
+                  px->err_host_dev, S.agg_out);
 }
 
 }  // namespace sg

@@ -35,6 +35,7 @@ struct PxStore {
   float* v;        // history shard [padded / K] (momentum or AdaGrad accumulator)
   int64_t padded;  // bucket elements, a multiple of 32 K
   int64_t rn_end;  // elements [0, rn_end) are the weight matrix (TF32-rounded working copy)
+  int agg_out = 1; // write the aggregated gradient of the shard back into g (0: g is only read)
 };
 
 struct PeerExchange;

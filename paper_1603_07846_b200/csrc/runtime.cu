@@ -1546,166 +1546,18 @@ SG_API sg_status sg_server_sync(sg_cluster* c, const sg_updater_cfg* cfg, int64_
 // ------------------------------------- C5 fused server sync over peer memory --
 // The worker-group -> server-group exchange of one flat Param (P:419-422,
 // P:527) as ONE kernel over NVLink peer memory instead of
-// reduce-scatter -> Updater -> all-gather: rank r reads every rank's gradient
-// for its shard [r*shard, (r+1)*shard) straight out of the peers' HBM (P2P
-// loads), sums them in ascending rank order, applies the SGD-momentum Updater
-// (same FMA order as sgd_kernel) and stores the new weights into
-// every rank's weight buffer (P2P stores).  Two single-block flag barriers
-// (system-scope release / acquire on per-rank flags in peer memory) bracket it:
-// "every gradient is ready" before, "every weight has landed" after.
-namespace sg_p2p {
-constexpr int kMaxPeers = 8;
-#ifndef SG_P2P_UNROLL
-#define SG_P2P_UNROLL 4
-#endif
-#ifndef SG_P2P_STREAMING
-#define SG_P2P_STREAMING 0
-#endif
-#ifndef SG_P2P_PULL
-#define SG_P2P_PULL 0
-#endif
-#ifndef SG_P2P_BLOCKS_PER_SM
-#define SG_P2P_BLOCKS_PER_SM 8
-#endif
-constexpr int kUnroll = SG_P2P_UNROLL;            // float4 per thread per iteration
-constexpr int kBlocksPerSm = SG_P2P_BLOCKS_PER_SM;  // 256-thread blocks per SM
-struct PeerPtrs {
-  const float* g[kMaxPeers];
-  float* w[kMaxPeers];
-  unsigned* flags[kMaxPeers];
-};
-
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// One block of 32 threads: lane j < world signals rank j (flag slot [rank]) and
-// then waits for slot [j] of its own flags to reach the epoch.  Bounded spin:
-// a peer that never arrives sets *err and the kernel exits (no GPU hang).
-__global__ void peer_barrier_kernel(PeerPtrs p, int rank, int world, unsigned epoch, int* err) {
-  const int j = threadIdx.x;
-  __threadfence_system();
-  if (j < world) st_release_sys(p.flags[j] + rank, epoch);
-  if (j < world) {
-    const unsigned* mine = p.flags[rank] + j;
-    long long spins = 0;
-    while (ld_acquire_sys(mine) < epoch) {
-      if (++spins > (1LL << 26)) {
-        atomicExch(err, 1);
-        break;
-      }
-      __nanosleep(64);
-    }
-  }
-  __syncthreads();
-  __threadfence_system();
-}
-
-// Each thread handles U float4 elements per grid-stride iteration, all of
-// their local and peer loads issued before any arithmetic (remote NVLink loads
-// have microsecond latency: more bytes in flight per thread).
-template <int U>
-__global__ void __launch_bounds__(256) peer_sync_kernel(PeerPtrs p, float* __restrict__ v, long long shard, int rank,
-                                                        int world, float lr, float mu, float wd, float s) {
-  const long long base = (long long)rank * shard;
-  const long long n4 = shard >> 2;
-  const float4* wl = reinterpret_cast<const float4*>(p.w[rank] + base);
-  float4* v4 = reinterpret_cast<float4*>(v);
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
-    float4 g[U], ww[U], vv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = i0 + u * stride;
-      if (i < n4) {
-        g[u] = reinterpret_cast<const float4*>(p.g[0] + base)[i];
-        ww[u] = wl[i];
-        vv[u] = v4[i];
-      }
-    }
-    for (int k = 1; k < world; ++k) {   // ascending rank order (deterministic)
-      float4 gk[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long i = i0 + u * stride;
-#if SG_P2P_STREAMING
-        if (i < n4) gk[u] = __ldcs(reinterpret_cast<const float4*>(p.g[k] + base) + i);
-#else
-        if (i < n4) gk[u] = reinterpret_cast<const float4*>(p.g[k] + base)[i];
-#endif
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        g[u].x = __fadd_rn(g[u].x, gk[u].x);
-        g[u].y = __fadd_rn(g[u].y, gk[u].y);
-        g[u].z = __fadd_rn(g[u].z, gk[u].z);
-        g[u].w = __fadd_rn(g[u].w, gk[u].w);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const long long i = i0 + u * stride;
-      if (i >= n4) continue;
-      float* wp = &ww[u].x;
-      float* vp = &vv[u].x;
-      const float* gp = &g[u].x;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float gq = __fmaf_rn(wd, wp[e], __fmul_rn(s, gp[e]));
-        vp[e] = __fmaf_rn(mu, vp[e], -__fmul_rn(lr, gq));
-        wp[e] = __fadd_rn(wp[e], vp[e]);
-      }
-      v4[i] = vv[u];
-#if SG_P2P_PULL
-      reinterpret_cast<float4*>(p.w[rank] + base)[i] = ww[u];
-#else
-#if SG_P2P_STREAMING
-      for (int k = 0; k < world; ++k) __stcs(reinterpret_cast<float4*>(p.w[k] + base) + i, ww[u]);
-#else
-      for (int k = 0; k < world; ++k) reinterpret_cast<float4*>(p.w[k] + base)[i] = ww[u];
-#endif
-#endif
-    }
-  }
-}
-// Pull variant (SG_P2P_PULL): after the middle barrier every rank copies the
-// other ranks' updated weight shards into its own buffer by P2P loads, so
-// NVLink carries loads only.
-template <int U>
-__global__ void __launch_bounds__(256) peer_pull_kernel(PeerPtrs p, long long shard, int rank, int world) {
-  const long long n4 = shard >> 2;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (int k = 1; k < world; ++k) {
-    const int src = (rank + k) % world;
-    const float4* from = reinterpret_cast<const float4*>(p.w[src] + (long long)src * shard);
-    float4* to = reinterpret_cast<float4*>(p.w[rank] + (long long)src * shard);
-    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n4; i0 += stride * U) {
-      float4 t[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (i0 + u * stride < n4) t[u] = from[i0 + u * stride];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (i0 + u * stride < n4) to[i0 + u * stride] = t[u];
-    }
-  }
-}
-}  // namespace sg_p2p
-using namespace sg_p2p;
-
+// reduce-scatter -> Updater -> all-gather: the step's fused exchange
+// (exchange.h / exchange.cu: entry barrier, ascending-rank sum of the shard's
+// gradients read straight out of the peers' HBM, SGD-momentum Updater on the
+// rank's shard of w_full, the new weights stored into every rank's w_full,
+// trailing barrier by the last CTA; a barrier timeout sets an error flag that
+// every later exchange kernel checks and skips its work on).  Here the master
+// shard IS the rank's slice of w_full and nothing is TF32-rounded (rn_end 0).
 struct sg_peer_sync {
   sg_cluster* c = nullptr;
   int64_t n = 0;
-  float *grad = nullptr, *w = nullptr, *v = nullptr;
-  unsigned* flags = nullptr;
-  int* err = nullptr;
-  unsigned epoch = 0;
-  PeerPtrs peers{};
+  float *grad = nullptr, *w = nullptr, *v = nullptr, *lr = nullptr;
+  sg::PeerExchange* px = nullptr;
 };
 
 extern "C" {
@@ -1713,60 +1565,30 @@ extern "C" {
 SG_API sg_status sg_peer_sync_create(sg_cluster* c, int64_t n, sg_peer_sync** out, float** grad_full_dev,
                                      float** w_full_dev, float** v_shard_dev) {
   SG_CHECK(c && out && grad_full_dev && w_full_dev && v_shard_dev, SG_ERR_INVALID_ARG, "sg_peer_sync_create: null argument");
-  SG_CHECK(c->world <= kMaxPeers, SG_ERR_UNSUPPORTED, "sg_peer_sync: at most %d ranks (got %d)", kMaxPeers, c->world);
+  SG_CHECK(c->world <= 8, SG_ERR_UNSUPPORTED, "sg_peer_sync: at most 8 ranks (got %d)", c->world);
   SG_CHECK(n > 0 && n % (32LL * c->world) == 0, SG_ERR_PARTITION, "partition error: n=%lld not a multiple of 32*K=%d",
            (long long)n, 32 * c->world);
   SG_CUDA(cudaSetDevice(c->device));
   sg_peer_sync* p = new sg_peer_sync();
   p->c = c;
   p->n = n;
-  auto fail = [&](cudaError_t e) {
-    cudaFree(p->grad); cudaFree(p->w); cudaFree(p->v); cudaFree(p->flags); cudaFree(p->err);
-    delete p;
-    return e;
-  };
+  const int64_t shard = n / c->world;
   cudaError_t e = cudaMalloc(&p->grad, n * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&p->w, n * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&p->v, n / c->world * sizeof(float));
-  if (e == cudaSuccess) e = cudaMalloc(&p->flags, kMaxPeers * sizeof(unsigned));
-  if (e == cudaSuccess) e = cudaMalloc(&p->err, sizeof(int));
-  if (e == cudaSuccess) e = cudaMemset(p->v, 0, n / c->world * sizeof(float));
-  if (e == cudaSuccess) e = cudaMemset(p->flags, 0, kMaxPeers * sizeof(unsigned));
-  if (e == cudaSuccess) e = cudaMemset(p->err, 0, sizeof(int));
-  if (e != cudaSuccess) SG_FAIL(SG_ERR_OOM, "sg_peer_sync_create: %s", cudaGetErrorString(fail(e)));
-  p->peers.g[c->rank] = p->grad;
-  p->peers.w[c->rank] = p->w;
-  p->peers.flags[c->rank] = p->flags;
-  if (c->world > 1) {
-    // exchange IPC handles of (grad, w, flags) over the parameter communicator
-    cudaIpcMemHandle_t h[3];
-    e = cudaIpcGetMemHandle(&h[0], p->grad);
-    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[1], p->w);
-    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h[2], p->flags);
-    if (e != cudaSuccess) SG_FAIL(SG_ERR_CUDA, "sg_peer_sync_create: IPC handle: %s", cudaGetErrorString(fail(e)));
-    std::vector<cudaIpcMemHandle_t> all(3 * c->world);
-    char* dbuf = nullptr;
-    e = cudaMalloc(&dbuf, sizeof(h) * (c->world + 1));
-    if (e != cudaSuccess) SG_FAIL(SG_ERR_OOM, "sg_peer_sync_create: %s", cudaGetErrorString(fail(e)));
-    cudaMemcpy(dbuf, h, sizeof(h), cudaMemcpyHostToDevice);
-    ncclResult_t r = ncclAllGather(dbuf, dbuf + sizeof(h), sizeof(h), ncclChar, c->comm_par, 0);
-    e = cudaDeviceSynchronize();
-    if (r == ncclSuccess && e == cudaSuccess) e = cudaMemcpy(all.data(), dbuf + sizeof(h), sizeof(h) * c->world, cudaMemcpyDeviceToHost);
-    cudaFree(dbuf);
-    if (r != ncclSuccess) {
-      fail(cudaSuccess);
-      SG_FAIL(SG_ERR_NCCL, "sg_peer_sync_create: handle exchange: %s", ncclGetErrorString(r));
-    }
-    for (int k = 0; k < c->world && e == cudaSuccess; ++k) {
-      if (k == c->rank) continue;
-      void* q[3] = {nullptr, nullptr, nullptr};
-      for (int j = 0; j < 3 && e == cudaSuccess; ++j)
-        e = cudaIpcOpenMemHandle(&q[j], all[3 * k + j], cudaIpcMemLazyEnablePeerAccess);
-      p->peers.g[k] = static_cast<const float*>(q[0]);
-      p->peers.w[k] = static_cast<float*>(q[1]);
-      p->peers.flags[k] = static_cast<unsigned*>(q[2]);
-    }
-    if (e != cudaSuccess) SG_FAIL(SG_ERR_CUDA, "sg_peer_sync_create: IPC open: %s", cudaGetErrorString(fail(e)));
+  if (e == cudaSuccess) e = cudaMalloc(&p->v, shard * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&p->lr, sizeof(float));
+  if (e == cudaSuccess) e = cudaMemset(p->v, 0, shard * sizeof(float));
+  // px_create is collective and runs even after a local allocation failure: the
+  // missing buffers fail its IPC step, and its status word makes every rank fail
+  sg::PxStore st{e == cudaSuccess ? p->grad : nullptr, e == cudaSuccess ? p->w : nullptr,
+                 e == cudaSuccess ? p->w + c->rank * shard : nullptr, p->v, n, 0};
+  st.agg_out = 0;  // grad_full is read, not modified
+  const sg_status ps = sg::px_create(c->comm_par, c->rank, c->world, c->device, {st}, &p->px);
+  if (ps != SG_OK || e != cudaSuccess) {
+    cudaFree(p->grad); cudaFree(p->w); cudaFree(p->v); cudaFree(p->lr);
+    delete p;
+    if (e != cudaSuccess) SG_FAIL(SG_ERR_OOM, "sg_peer_sync_create: %s", cudaGetErrorString(e));
+    return ps;
   }
   *grad_full_dev = p->grad;
   *w_full_dev = p->w;
@@ -1780,20 +1602,9 @@ SG_API sg_status sg_peer_sync_step(sg_peer_sync* p, const sg_updater_cfg* cfg, i
   sg_cluster* c = p->c;
   SG_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int64_t shard = p->n / c->world;
   const float s = cfg->grad_scale > 0 ? cfg->grad_scale : 1.f / c->world;
-  int dev_sms = 148;
-  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
-  if (c->world > 1) peer_barrier_kernel<<<1, 32, 0, st>>>(p->peers, c->rank, c->world, ++p->epoch, p->err);
-  const long long n4 = shard / 4;
-  const int blocks = (int)std::min<long long>((n4 + 255) / 256, (long long)kBlocksPerSm * dev_sms);
-  peer_sync_kernel<kUnroll><<<blocks, 256, 0, st>>>(p->peers, p->v, shard, c->rank, c->world, lr_at(*cfg, step),
-                                           cfg->momentum, cfg->weight_decay, s);
-  if (c->world > 1) peer_barrier_kernel<<<1, 32, 0, st>>>(p->peers, c->rank, c->world, ++p->epoch, p->err);
-#if SG_P2P_PULL
-  if (c->world > 1) peer_pull_kernel<kUnroll><<<blocks, 256, 0, st>>>(p->peers, shard, c->rank, c->world);
-#endif
-  SG_CUDA(cudaGetLastError());
+  SG_CUDA(sg::fill_scalar(p->lr, lr_at(*cfg, step), st));
+  SG_CUDA(sg::px_update(p->px, 0, p->lr, 1.f, cfg->momentum, cfg->weight_decay, s, 0, 0.f, st));
   return SG_OK;
 }
 
@@ -1802,24 +1613,9 @@ SG_API sg_status sg_peer_sync_destroy(sg_peer_sync* p) {
   sg_cluster* c = p->c;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  int err = 0;
-  cudaMemcpy(&err, p->err, sizeof(int), cudaMemcpyDeviceToHost);
-  if (c->world > 1) {
-    // nobody may still be reading / writing our buffers when they are freed
-    float* one = nullptr;
-    if (cudaMalloc(&one, sizeof(float)) == cudaSuccess) {
-      ncclAllReduce(one, one, 1, ncclFloat, ncclSum, c->comm_par, 0);
-      cudaDeviceSynchronize();
-      cudaFree(one);
-    }
-    for (int k = 0; k < c->world; ++k) {
-      if (k == c->rank) continue;
-      cudaIpcCloseMemHandle(const_cast<float*>(p->peers.g[k]));
-      cudaIpcCloseMemHandle(p->peers.w[k]);
-      cudaIpcCloseMemHandle(p->peers.flags[k]);
-    }
-  }
-  cudaFree(p->grad); cudaFree(p->w); cudaFree(p->v); cudaFree(p->flags); cudaFree(p->err);
+  const int err = sg::px_failed(p->px);
+  sg::px_destroy(p->px, c->world > 1 ? c->comm_par : nullptr);
+  cudaFree(p->grad); cudaFree(p->w); cudaFree(p->v); cudaFree(p->lr);
   delete p;
   SG_CHECK(err == 0, SG_ERR_CUDA, "sg_peer_sync: a peer barrier timed out (a rank did not arrive)");
   return SG_OK;

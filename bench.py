@@ -11,8 +11,11 @@ conventions in DESIGN.md "Measurement"):
 * value: training images/s of the whole job, device time (CUDA events on the
   launching stream) of exactly K steps, max over ranks, inputs resident in HBM,
   L2 flushed (256 MB write) before every timed step (flush excluded);
-* e2e: the same metric through sg_train_one_batch_host from pinned host
-  buffers (H2D of the step's inputs and D2H of the loss inside the timed region);
+* e2e: the same metric through the pipelined host entry
+  sg_train_one_batch_host_async from pinned host buffers (every step's H2D
+  input copy and D2H loss read inside the timed region; the next step's copy
+  overlaps the current step); e2e.sync_api_value: the synchronous
+  sg_train_one_batch_host (copy in, step, loss out, wait, every call);
 * roofline: the dominant operation of the step, from a second, profiled pass of
   the same graph with CUDA events around every layer operation;
 * cpu_baseline: the oracle (oracle/, float64 numpy) timed on this host's cores on

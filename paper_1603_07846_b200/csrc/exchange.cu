@@ -10,6 +10,7 @@ namespace sg {
 namespace {
 
 constexpr int kPxMaxPeers = 8;
+constexpr int kPxUnroll = 2;  // float4 per thread per round (U = 4 needs 255 registers with 8 peer slots)
 
 struct PxPeers {
   const float* g[kPxMaxPeers];  // rank k's gradient bucket
@@ -85,49 +86,60 @@ __global__ void __launch_bounds__(256) px_exchange_kernel(PxPeers p, PxFlags fl,
     const long long n4 = shard >> 2;
     float4* m4 = reinterpret_cast<float4*>(m);
     float4* v4 = reinterpret_cast<float4*>(v);
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
-         i += (long long)gridDim.x * blockDim.x) {
-      float4 gk[kPxMaxPeers];
+    // kPxUnroll float4 per thread per grid-stride round: every load (local and
+    // remote) of the round in flight before the arithmetic
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n4; i0 += kPxUnroll * stride) {
+      float4 gk[kPxUnroll][kPxMaxPeers];
 #pragma unroll
-      for (int k = 0; k < kPxMaxPeers; ++k)  // every peer load in flight before the sum
-        if (k < world) gk[k] = reinterpret_cast<const float4*>(p.g[k] + base)[i];
-      float4 g = gk[0];
+      for (int u = 0; u < kPxUnroll; ++u) {
+        const long long i = i0 + u * stride;
 #pragma unroll
-      for (int k = 1; k < kPxMaxPeers; ++k)
-        if (k < world) {
-          g.x = __fadd_rn(g.x, gk[k].x);
-          g.y = __fadd_rn(g.y, gk[k].y);
-          g.z = __fadd_rn(g.z, gk[k].z);
-          g.w = __fadd_rn(g.w, gk[k].w);
-        }
-      float4 ww = m4[i], vv = v4[i];
-      float* wp = &ww.x;
-      float* vp = &vv.x;
-      const float* gp = &g.x;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float gq = __fmaf_rn(wd, wp[e], __fmul_rn(s, gp[e]));
-        if (TYPE == 0) {
-          vp[e] = __fmaf_rn(mu, vp[e], -__fmul_rn(lr, gq));
-          wp[e] = __fadd_rn(wp[e], vp[e]);
-        } else {
-          vp[e] = __fmaf_rn(gq, gq, vp[e]);
-          wp[e] = __fsub_rn(wp[e], __fdiv_rn(__fmul_rn(lr, gq), __fadd_rn(__fsqrt_rn(vp[e]), eps)));
-        }
+        for (int k = 0; k < kPxMaxPeers; ++k)
+          if (k < world && i < n4) gk[u][k] = reinterpret_cast<const float4*>(p.g[k] + base)[i];
       }
-      m4[i] = ww;
-      v4[i] = vv;
-      const long long el = base + 4 * i;
-      float4 wk = ww;
-      if (el < rn_end) wk.x = tf32_rna(wk.x);
-      if (el + 1 < rn_end) wk.y = tf32_rna(wk.y);
-      if (el + 2 < rn_end) wk.z = tf32_rna(wk.z);
-      if (el + 3 < rn_end) wk.w = tf32_rna(wk.w);
 #pragma unroll
-      for (int k = 0; k < kPxMaxPeers; ++k)
-        if (k < world) reinterpret_cast<float4*>(p.w[k] + base)[i] = wk;
-      // the aggregated gradient of this shard (only this rank reads this region of its own bucket)
-      if (agg_out) reinterpret_cast<float4*>(const_cast<float*>(p.g[rank]) + base)[i] = g;
+      for (int u = 0; u < kPxUnroll; ++u) {
+        const long long i = i0 + u * stride;
+        if (i >= n4) break;
+        float4 g = gk[u][0];
+#pragma unroll
+        for (int k = 1; k < kPxMaxPeers; ++k)
+          if (k < world) {
+            g.x = __fadd_rn(g.x, gk[u][k].x);
+            g.y = __fadd_rn(g.y, gk[u][k].y);
+            g.z = __fadd_rn(g.z, gk[u][k].z);
+            g.w = __fadd_rn(g.w, gk[u][k].w);
+          }
+        float4 ww = m4[i], vv = v4[i];
+        float* wp = &ww.x;
+        float* vp = &vv.x;
+        const float* gp = &g.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float gq = __fmaf_rn(wd, wp[e], __fmul_rn(s, gp[e]));
+          if (TYPE == 0) {
+            vp[e] = __fmaf_rn(mu, vp[e], -__fmul_rn(lr, gq));
+            wp[e] = __fadd_rn(wp[e], vp[e]);
+          } else {
+            vp[e] = __fmaf_rn(gq, gq, vp[e]);
+            wp[e] = __fsub_rn(wp[e], __fdiv_rn(__fmul_rn(lr, gq), __fadd_rn(__fsqrt_rn(vp[e]), eps)));
+          }
+        }
+        m4[i] = ww;
+        v4[i] = vv;
+        const long long el = base + 4 * i;
+        float4 wk = ww;
+        if (el < rn_end) wk.x = tf32_rna(wk.x);
+        if (el + 1 < rn_end) wk.y = tf32_rna(wk.y);
+        if (el + 2 < rn_end) wk.z = tf32_rna(wk.z);
+        if (el + 3 < rn_end) wk.w = tf32_rna(wk.w);
+#pragma unroll
+        for (int k = 0; k < kPxMaxPeers; ++k)
+          if (k < world) reinterpret_cast<float4*>(p.w[k] + base)[i] = wk;
+        // the aggregated gradient of this shard (only this rank reads this region of its own bucket)
+        if (agg_out) reinterpret_cast<float4*>(const_cast<float*>(p.g[rank]) + base)[i] = g;
+      }
     }
   }
   // completion: this CTA's stores (local and remote) before its arrival

@@ -469,6 +469,19 @@ SG_API sg_status sg_peer_sync_create(sg_cluster* c, int64_t n, sg_peer_sync** ou
 SG_API sg_status sg_peer_sync_step(sg_peer_sync* p, const sg_updater_cfg* cfg, int64_t step, void* stream);
 SG_API sg_status sg_peer_sync_destroy(sg_peer_sync* p);
 
+/* The same exchange through NVSwitch multicast (NVLS): grad_full | w_full in one
+ * ncclMemAlloc'd, symmetrically registered NCCL window; ONE kernel per step:
+ * LSA barrier -> multimem.ld_reduce.add of rank r's shard (the switch sums the
+ * K gradients; the summation order is the switch's) -> Updater -> multimem.st
+ * of the new weights into every rank -> LSA barrier.  Same arguments and
+ * contract as sg_peer_sync_*; SG_ERR_UNSUPPORTED when the communicator has no
+ * multicast (no NVSwitch / NVLS).  All three calls are COLLECTIVE. */
+typedef struct sg_nvls_sync sg_nvls_sync;
+SG_API sg_status sg_nvls_sync_create(sg_cluster* c, int64_t n, sg_nvls_sync** out, float** grad_full_dev,
+                                     float** w_full_dev, float** v_shard_dev);
+SG_API sg_status sg_nvls_sync_step(sg_nvls_sync* p, const sg_updater_cfg* cfg, int64_t step, void* stream);
+SG_API sg_status sg_nvls_sync_destroy(sg_nvls_sync* p);
+
 #ifdef __cplusplus
 }
 #endif

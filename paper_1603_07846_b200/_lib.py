@@ -157,8 +157,11 @@ SIGS = {
     "sg_blob_set": [P, I32, I32, P, C.c_size_t, P],
     "sg_server_sync": [P, C.POINTER(UpdaterCfg), I64, P, P, P, I64, P],
     "sg_peer_sync_create": [P, I64, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)],
+    "sg_nvls_sync_create": [P, I64, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P)],
     "sg_peer_sync_step": [P, C.POINTER(UpdaterCfg), I64, P],
+    "sg_nvls_sync_step": [P, C.POINTER(UpdaterCfg), I64, P],
     "sg_peer_sync_destroy": [P],
+    "sg_nvls_sync_destroy": [P],
 }
 _RESTYPES = {"sg_last_error": C.c_char_p, "sg_abi_version": C.c_int32}
 

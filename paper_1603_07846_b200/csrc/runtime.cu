@@ -1622,3 +1622,5 @@ SG_API sg_status sg_peer_sync_destroy(sg_peer_sync* p) {
 }
 
 }  // extern "C"
+
+#include "nvls_impl.cuh"

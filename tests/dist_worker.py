@@ -282,15 +282,26 @@ def dev_view(ptr, n):
     return torch.as_tensor(_A(), device="cuda")
 
 
-def case_peer_sync(rank, world, cl):
-    """The fused peer-memory server sync (sg_peer_sync_*) against the oracle:
-    ascending-k gradient sum, then the Updater (oracle/updater.py), two steps."""
+def case_peer_sync(rank, world, cl, api="peer"):
+    """The fused peer-memory server sync (sg_peer_sync_*; api="nvls": the NVSwitch
+    multicast variant sg_nvls_sync_*) against the oracle: the gradient sum, then
+    the Updater (oracle/updater.py), two steps."""
     import ctypes as C
     n = 32 * world * 1000 + 32 * world * 3      # shard not a multiple of the 256-thread block
     cfg = PN.updater_cfg({"base_lr": 0.01, "momentum": 0.9, "weight_decay": 5e-4})
     grad_h, w_h = generate.server_sync_inputs(n, world, rank)
     h, gp, wp, vp = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
-    L.sg_peer_sync_create(cl.h, n, C.byref(h), C.byref(gp), C.byref(wp), C.byref(vp))
+    create = getattr(L, f"sg_{api}_sync_create")
+    step_fn = getattr(L, f"sg_{api}_sync_step")
+    destroy = getattr(L, f"sg_{api}_sync_destroy")
+    try:
+        create(cl.h, n, C.byref(h), C.byref(gp), C.byref(wp), C.byref(vp))
+    except L.SingaError as ex:
+        if api == "nvls" and ex.code == -12:   # SG_ERR_UNSUPPORTED: no multicast on this node
+            if rank == 0:
+                print(f"nvls sync K={world}: unsupported here ({ex})")
+            return
+        raise
     g, w = dev_view(gp.value, n), dev_view(wp.value, n)
     w.copy_(torch.from_numpy(w_h))
     torch.cuda.synchronize()
@@ -298,10 +309,10 @@ def case_peer_sync(rank, world, cl):
     for t in range(2):
         g.copy_(torch.from_numpy(generate.server_sync_inputs(n, world, rank)[0] * (t + 1)))
         torch.cuda.synchronize()
-        L.sg_peer_sync_step(h, C.byref(cfg), t, None)
+        step_fn(h, C.byref(cfg), t, None)
         torch.cuda.synchronize()
     wg = w.cpu().numpy().copy()
-    L.sg_peer_sync_destroy(h)
+    destroy(h)
     allw = [None] * world
     dist.all_gather_object(allw, wg)
     if rank == 0:
@@ -314,12 +325,13 @@ def case_peer_sync(rank, world, cl):
             ww, vv = OU.sgd_momentum(ww, vv, tot, cfgd, t, 1.0 / world)
         e = normwise(allw[0], ww)
         assert e < 1e-6, e
-        print(f"peer sync K={world}: weights identical on all ranks, err vs oracle {e:.2e}")
+        print(f"{api} sync K={world}: weights identical on all ranks, err vs oracle {e:.2e}")
 
 
 CASES = {"k_invariance": case_k_invariance, "hybrid": case_hybrid, "autoencoder": case_autoencoder,
          "isolated": case_isolated, "p2p_step": case_p2p_step,
-         "alexnet": case_alexnet, "server_sync": case_server_sync, "peer_sync": case_peer_sync}
+         "alexnet": case_alexnet, "server_sync": case_server_sync, "peer_sync": case_peer_sync,
+         "nvls_sync": lambda r, w, cl: case_peer_sync(r, w, cl, api="nvls")}
 
 if __name__ == "__main__":
     import faulthandler

@@ -27,10 +27,10 @@ def run_cases(k, cases, port):
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 def test_two_ranks():
-    run_cases(2, ["server_sync", "peer_sync", "k_invariance", "hybrid", "autoencoder", "isolated", "alexnet", "p2p_step"],
+    run_cases(2, ["server_sync", "peer_sync", "nvls_sync", "k_invariance", "hybrid", "autoencoder", "isolated", "alexnet", "p2p_step"],
               29611)
 
 
 @pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
 def test_four_ranks():
-    run_cases(4, ["server_sync", "peer_sync", "k_invariance", "hybrid", "isolated", "alexnet", "p2p_step"], 29613)
+    run_cases(4, ["server_sync", "peer_sync", "nvls_sync", "k_invariance", "hybrid", "isolated", "alexnet", "p2p_step"], 29613)

@@ -123,8 +123,37 @@ def main():
             ms, tms = float(tt[0].item()), float(tt[1].item())
             dist.barrier()
         # the fused peer-memory path (sg_peer_sync_*: one kernel, P2P loads / stores)
-        fms = None
+        # and the NVSwitch multicast path (sg_nvls_sync_*), when available
+        def fused(api):
+            h, gp, wp, vp = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+            try:
+                getattr(L, f"sg_{api}_sync_create")(cl.h, n, C.byref(h), C.byref(gp), C.byref(wp), C.byref(vp))
+            except L.SingaError:
+                return None
+            dev_view(gp.value, n).copy_(grad0)
+            dev_view(wp.value, n).fill_(0.01)
+            torch.cuda.synchronize()
+            dist.barrier()
+            step_fn = getattr(L, f"sg_{api}_sync_step")
+            with torch.cuda.stream(stream):
+                for t in range(args.warmup + args.iters):
+                    if t == args.warmup:
+                        torch.cuda.synchronize()
+                        dist.barrier()
+                        ev0.record(stream)
+                    step_fn(h, C.byref(cfg), t, C.c_void_p(stream.cuda_stream))
+                ev1.record(stream)
+            torch.cuda.synchronize()
+            r = ev0.elapsed_time(ev1) / args.iters
+            getattr(L, f"sg_{api}_sync_destroy")(h)
+            tt = torch.tensor([r], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return float(tt[0].item())
+
+        fms = nms = None
         if world > 1:
+            nms = fused("nvls")
+        if False:
             h, gp, wp, vp = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
             L.sg_peer_sync_create(cl.h, n, C.byref(h), C.byref(gp), C.byref(wp), C.byref(vp))
             dev_view(gp.value, n).copy_(grad0)
@@ -145,6 +174,8 @@ def main():
             tt = torch.tensor([fms], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             fms = float(tt[0].item())
+        if world > 1:
+            fms = fused("peer")
         t_s = ms * 1e-3
         line = {"workload": "updater_sweep", "params": n, "n_gpus": world, "iters": args.iters,
                 "warmup": args.warmup, "t_us": round(ms * 1e3, 2),
@@ -156,6 +187,7 @@ def main():
             line["torch_nccl_t_us"] = round(tms * 1e3, 2)
             line["fused_p2p_t_us"] = round(fms * 1e3, 2)
             line["fused_p2p_busbw_gbs"] = round(2 * (world - 1) / world * 4 * n / (fms * 1e-3) / 1e9, 1)
+            line["nvls_t_us"] = round(nms * 1e3, 2) if nms is not None else None
         else:
             a = 20 * n / t_s / 1e9
             line["upd_hbm_gbs"] = round(a, 1)
